@@ -1,0 +1,169 @@
+/*
+ * optimus_b200.h — C-ABI of the B200 (sm_100a) streaming chunked block-decode path.
+ *
+ * The reference (arxiv 2605.24832, package `dllmsim`) has no native code: its
+ * decode step is the Python call chain
+ *     _Loop.run_decode (pkg/src/dllmsim/sim.py:269-305)
+ *       -> plan_chunk (engine.py:45-67)
+ *       -> oracle.commits(request, window) (sim.py:278; commit.py:279-280)
+ *       -> apply_chunk (engine.py:79-95)
+ * and the model forward it stands in for (KV append into pages, varlen paged
+ * attention, confidence-threshold unmask) is specified in
+ * prose only.  Each entry point below is the native replacement for one piece of
+ * that forward; the Python host layer (paper_2605_24832_b200/) binds them with
+ * ctypes the same way a reference-side binding would.
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless its name ends in `_host`;
+ *  - tensors are bf16 ("uint16_t" storage) unless stated; strides are in elements;
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *  - return value: 0 on success, OPTIMUS_EINVAL (-1) for a bad argument / shape,
+ *    OPTIMUS_ENOSYS (-2) when the device is not sm_100, or a positive cudaError_t;
+ *  - the library never allocates device memory: workspaces are caller-owned.
+ *
+ * KV cache layout (per layer, one allocation for K and one for V):
+ *     cache[num_pages][Hkv][page_size][head_dim]   bf16
+ * so each (page, head) is a contiguous page_size x head_dim tile that the
+ * attention kernel stages with TMA (SWIZZLE_128B boxes of 64 columns).
+ * Absolute sequence position of output position p of request r is
+ * prompt_len[r] + p; its slot is block_table[r][s / P] * P + s % P
+ * (SURVEY.md §8c rule S).
+ */
+#ifndef OPTIMUS_B200_H
+#define OPTIMUS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPTIMUS_EINVAL (-1)
+#define OPTIMUS_ENOSYS (-2)
+
+/* Attention work item / combine group records (8 x int32 each). */
+#define OPTIMUS_WORK_INTS 8
+
+/* Library version, e.g. 100 for 0.1.0. */
+int optimus_version(void);
+
+/* Human-readable description of the last error raised on this thread. */
+const char* optimus_last_error(void);
+
+/* Number of SMs of the current device (0 if no device). */
+int optimus_device_sm_count(void);
+
+/*
+ * K1 — KV append (replaces the KV write of the forward that the reference models
+ * with `cost_model.latency`, sim.py:293; rule S/K of SURVEY §8c).
+ *
+ * For token i (0 <= i < n_tok) of request tok_req[i] at output position
+ * tok_pos[i]:  s = prompt_len[req] + tok_pos[i],
+ *              slot = block_tables[req * max_pages + s / page_size] * page_size + s % page_size,
+ * and K/V rows k_new[i*new_stride + h*head_dim + :] are written to
+ * k_cache[((page*Hkv + h)*page_size + off)*head_dim + :] for every head h.
+ * slot_mapping_out (optional, int64[n_tok]) receives the slots.
+ */
+int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                      const int32_t* tok_req, const int32_t* tok_pos,
+                      const int32_t* prompt_len, const int32_t* block_tables,
+                      int max_pages, int n_tok, int num_kv_heads, int head_dim,
+                      int page_size, void* k_cache, void* v_cache, int64_t num_pages,
+                      int64_t* slot_mapping_out, void* stream);
+
+/*
+ * Host-side work planner for K2 (the length-aware persistent tile scheduler).
+ * Inputs are HOST arrays describing the step:
+ *   cu_seqlens_q_host[n_req+1]  query tokens of each request (kv rows then window rows)
+ *   key_end_host[n_req]         absolute end of the keys any query of the request may see
+ * It splits every (request, kv head, 128-row query tile) into key ranges of whole
+ * 64-key tiles, assigns them to `grid` persistent CTAs by longest-processing-time
+ * first, and writes:
+ *   work_host[max_work][8]      {req, kv_head, tok_begin, n_tok, key_begin, key_end, partial_slot, 0}
+ *                               ordered CTA by CTA
+ *   cta_off_host[grid+1]        CSR offsets of each CTA's items in work_host
+ *   groups_host[max_groups][8]  {req, kv_head, tok_begin, n_tok, slot0, n_splits, 0, 0}
+ *                               (query tiles that were split and need the combine)
+ * Returns the number of work items (>= 0) or OPTIMUS_EINVAL; *n_groups and
+ * *n_partials receive the combine-group count and the partial-slot count.
+ * `min_split_tiles` bounds how finely a long context is split (64-key tiles).
+ */
+int optimus_attn_plan(int n_req, const int32_t* cu_seqlens_q_host, const int32_t* key_end_host,
+                      int num_q_heads, int num_kv_heads, int grid, int min_split_tiles,
+                      int32_t* work_host, int max_work, int32_t* cta_off_host,
+                      int32_t* groups_host, int max_groups, int* n_groups, int* n_partials);
+
+/* Upper bounds for the planner's output buffers. */
+int optimus_attn_plan_bounds(int n_req, const int32_t* cu_seqlens_q_host,
+                             const int32_t* key_end_host, int num_q_heads, int num_kv_heads,
+                             int min_split_tiles, int* max_work, int* max_groups);
+
+/*
+ * K2 — variable-length paged attention with the diffusion visibility rule
+ * (SURVEY §8c rule V).  Query token i belongs to request r (via the work items);
+ * q_pos[i] is its output position.  Key at absolute position s is visible to it iff
+ *     s < prompt_len[r] + (q_pos[i] / block_size + 1) * block_size   (block-causal)
+ * and (s < vis_base[r] or bit (s - vis_base[r]) of vis_words[vis_off[r]...] is set)
+ * and s < the work item's key_end.
+ * q:   [n_tok][Hq][head_dim] (row stride q_stride_tok); out: same shape (out_stride_tok).
+ * ws_o / ws_ml: split-KV partials, float[n_partials][128][head_dim] and
+ * float[n_partials][128][2] (may be NULL when n_partials == 0).
+ * work/cta_off/groups are the planner's outputs copied to the device; `grid` must
+ * equal the grid used for planning.
+ */
+int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total,
+                       const void* k_cache, const void* v_cache, int64_t num_pages,
+                       const int32_t* q_pos, const int32_t* prompt_len,
+                       const int32_t* vis_base, const int32_t* vis_off, const uint32_t* vis_words,
+                       const int32_t* block_tables, int max_pages,
+                       const int32_t* work, const int32_t* cta_off, int grid,
+                       const int32_t* groups, int n_groups,
+                       int block_size, int num_q_heads, int num_kv_heads, int head_dim,
+                       int page_size, float sm_scale,
+                       void* out, int64_t out_stride_tok,
+                       float* ws_o, float* ws_ml, void* stream);
+
+/*
+ * K3 — fused confidence-threshold unmask (replaces StochasticOracle.commits,
+ * commit.py:279-280 -> commit_step commit.py:86-112, with the model rule
+ * "commit tokens whose confidence exceeds the threshold"; tau=0.9
+ * PAPER.md:49).  Two phases so the vocabulary may be sharded across ranks:
+ *
+ * (a) partials: for window row i (0 <= i < n_rows) read logits row
+ *     (row_src ? row_src[i] : i), columns [0, vocab) of this shard, and write
+ *     part[i][j] = {max, sum exp(x - max), argmax + vocab_offset} for vocab split j
+ *     (n_vsplit splits; record = 3 x 32-bit: float, float, int32).
+ *     logits_dtype: 0 = bf16, 1 = fp32.
+ */
+int optimus_unmask_partials(const void* logits, int logits_dtype, int64_t row_stride,
+                            const int32_t* row_src, int n_rows, int vocab, int vocab_offset,
+                            int n_vsplit, float* part, void* stream);
+
+/*
+ * (b) finalize: part is [n_outer][n_rows][n_vsplit] records (n_outer = number of
+ *     vocab shards gathered, 1 on a single GPU), merged in a fixed order.
+ *     conf = max softmax probability, tok = argmax (lowest index on ties).
+ *     Rows of request r are cu_rows[r] .. cu_rows[r+1]-1 in window order.
+ *     commit iff conf >= tau; progress rule per request:
+ *       fallback_mode 0 ("earliest"): the first window row always commits
+ *                       (exactly commit.py:103);
+ *       fallback_mode 1 ("top1"): if no row passes, the highest-confidence row
+ *                       commits (ties -> earliest).
+ *     Optional state mirror update (pass NULL to skip): for committed row i of
+ *     request r at output position row_pos[i]:
+ *       state[r*state_stride + pos] = 1 (DECODED_UNCACHED), token_buf[same] = tok.
+ */
+int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vsplit,
+                            const int32_t* cu_rows, int n_req, float tau, int fallback_mode,
+                            uint8_t* commit_mask, int32_t* tok, float* conf,
+                            const int32_t* row_pos, uint8_t* state, int32_t* token_buf,
+                            int64_t state_stride, void* stream);
+
+/* Recommended vocab split count for n_rows x vocab on the current device. */
+int optimus_unmask_splits(int n_rows, int vocab);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OPTIMUS_B200_H */

@@ -1,0 +1,150 @@
+"""CPU restatement of the numeric half of the decode step (test infrastructure).
+
+Rules (the reference states them in prose only):
+
+S  slot mapping (core.py:3-4): absolute position s = prompt + p,
+   slot = block_table[s // P] * P + s % P.
+K  KV append: every planned token (kv rows and window rows) writes its K/V row.
+V  visibility (engine.py:58-66): a query at output position
+   p_q sees key s iff s < prompt, or (p = s - prompt) satisfies
+   p // B <= p_q // B (block-causal, bidirectional inside a block) and p was
+   DECODED_CACHED before the step or is planned in this step.
+U  unmask (commit.py:103): per window row
+   conf = max softmax probability (float64 here), tok = argmax (lowest index on
+   ties); commit iff conf >= tau; progress rule "earliest" always commits the
+   first window row, "top1" commits the most confident row when none passes.
+
+Everything is numpy; attention is computed per (request, kv head) with the G
+query heads of a group folded into the row dimension (no repeat of K/V).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+CACHED = 2
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round float32 values to bf16 (round-to-nearest-even), returned as float32."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    rounded = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    out = rounded.astype(np.uint32).view(np.float32)
+    return np.where(np.isnan(a), a, out).reshape(a.shape)
+
+
+def slot_mapping(tok_req, tok_pos, prompt_len, block_tables, page_size: int) -> np.ndarray:
+    """Rule S for every planned token."""
+    tok_req = np.asarray(tok_req)
+    s = np.asarray(prompt_len)[tok_req] + np.asarray(tok_pos)
+    pages = np.asarray(block_tables)[tok_req, s // page_size]
+    return pages.astype(np.int64) * page_size + s % page_size
+
+
+def kv_append(k_cache: np.ndarray, v_cache: np.ndarray, k_new, v_new, slots, page_size: int) -> None:
+    """Rule K: cache[page, h, off, :] = new[i, h, :] (caches [pages, Hkv, P, d])."""
+    slots = np.asarray(slots)
+    pages, offs = slots // page_size, slots % page_size
+    k_cache[pages, :, offs, :] = np.asarray(k_new)
+    v_cache[pages, :, offs, :] = np.asarray(v_new)
+
+
+def visible_outputs(states_before: np.ndarray, planned) -> np.ndarray:
+    """Output positions whose KV is valid in this step (rule V, state part)."""
+    vis = np.asarray(states_before) == CACHED
+    vis = vis.copy()
+    vis[list(planned)] = True
+    return vis
+
+
+def key_mask(prompt: int, vis_out: np.ndarray, q_pos, block_size: int, n_keys: int) -> np.ndarray:
+    """Boolean [n_q, n_keys]: which absolute keys each query sees (rule V)."""
+    s = np.arange(n_keys)
+    p = s - prompt
+    q_pos = np.asarray(q_pos)
+    out_ok = np.zeros(n_keys, dtype=bool)
+    inside = (p >= 0) & (p < len(vis_out))
+    out_ok[inside] = vis_out[p[inside]]
+    base = (s < prompt) | out_ok
+    causal = (p[None, :] // block_size) <= (q_pos[:, None] // block_size)
+    return base[None, :] & ((s[None, :] < prompt) | causal)
+
+
+def gather_keys(cache: np.ndarray, block_table, n_keys: int, page_size: int) -> np.ndarray:
+    """[n_keys, Hkv, d] rows of one request, read through its block table."""
+    s = np.arange(n_keys)
+    pages = np.asarray(block_table)[s // page_size]
+    return cache[pages, :, s % page_size, :]
+
+
+def paged_attention(q, k_cache, v_cache, cu_seqlens, q_pos, prompt_len, vis_out_list,
+                    block_tables, block_size: int, page_size: int, sm_scale=None,
+                    dtype=np.float32) -> np.ndarray:
+    """Reference output [n_tok, Hq, d] for the decode step.
+
+    ``vis_out_list[r]`` is the boolean visibility of request r's output positions
+    (``visible_outputs``).  Keys considered: [0, prompt + len(vis_out)).
+    """
+    q = np.asarray(q, dtype=dtype)
+    n_tok, hq, d = q.shape
+    hkv = k_cache.shape[1]
+    G = hq // hkv
+    scale = (1.0 / np.sqrt(d)) if sm_scale is None else sm_scale
+    out = np.zeros((n_tok, hq, d), dtype=np.float32)
+    for r in range(len(cu_seqlens) - 1):
+        t0, t1 = int(cu_seqlens[r]), int(cu_seqlens[r + 1])
+        if t1 == t0:
+            continue
+        prompt = int(prompt_len[r])
+        vis_out = vis_out_list[r]
+        n_keys = prompt + len(vis_out)
+        mask = key_mask(prompt, vis_out, q_pos[t0:t1], block_size, n_keys)  # [nq, n_keys]
+        K = gather_keys(k_cache, block_tables[r], n_keys, page_size).astype(dtype)
+        V = gather_keys(v_cache, block_tables[r], n_keys, page_size).astype(dtype)
+        nq = t1 - t0
+        for h in range(hkv):
+            Q = q[t0:t1, h * G:(h + 1) * G, :].reshape(nq * G, d)        # row = t*G + g
+            S = (Q @ K[:, h, :].T) * dtype(scale)
+            m = np.repeat(mask, G, axis=0)
+            S = np.where(m, S, -np.inf)
+            S = S - S.max(axis=1, keepdims=True)
+            P = np.exp(S)
+            P /= P.sum(axis=1, keepdims=True)
+            O = P @ V[:, h, :]
+            out[t0:t1, h * G:(h + 1) * G, :] = O.reshape(nq, G, d)
+    return out
+
+
+def unmask(logits, cu_rows, tau: float = 0.9, fallback: str = "earliest"):
+    """Rule U -> (commit_mask bool[n], tok int64[n], conf float64[n])."""
+    x = np.asarray(logits, dtype=np.float64)
+    n = x.shape[0]
+    tok = np.argmax(x, axis=1) if n else np.zeros(0, dtype=np.int64)
+    m = x.max(axis=1, keepdims=True) if n else np.zeros((0, 1))
+    conf = 1.0 / np.exp(x - m).sum(axis=1) if n else np.zeros(0)
+    commit = conf >= tau
+    for r in range(len(cu_rows) - 1):
+        a, b = int(cu_rows[r]), int(cu_rows[r + 1])
+        if b <= a:
+            continue
+        if fallback == "earliest":
+            commit[a] = True
+        elif not commit[a:b].any():
+            commit[a + int(np.argmax(conf[a:b]))] = True
+    return commit, tok, conf
+
+
+def peaked_logits(rng: np.random.Generator, n_rows: int, vocab: int, tokens, confs) -> np.ndarray:
+    """Oracle-driven logits recipe (SURVEY §8c parity harness): background N(0,1)
+    plus one peak ``S + ln(t/(1-t))`` with S = logsumexp of the other columns, so
+    the max softmax probability is t (before bf16 rounding)."""
+    x = rng.standard_normal((n_rows, vocab)).astype(np.float32)
+    for i in range(n_rows):
+        t = float(confs[i])
+        k = int(tokens[i])
+        others = np.delete(x[i].astype(np.float64), k)
+        mx = others.max()
+        lse = mx + np.log(np.exp(others - mx).sum())
+        x[i, k] = np.float32(lse + np.log(t / (1.0 - t)))
+    return x

@@ -1,0 +1,35 @@
+// attn.cuh — parameter block shared by the K2 kernel (paged_attn.cu) and the
+// C-ABI launcher (capi.cu).
+#pragma once
+#include "ptx.cuh"
+
+namespace optimus {
+
+struct AttnParams {
+  const int32_t* q_pos;
+  const int32_t* prompt_len;
+  const int32_t* vis_base;
+  const int32_t* vis_off;
+  const uint32_t* vis_words;
+  const int32_t* block_tables;
+  const int32_t* work;     // [n][8]
+  const int32_t* cta_off;  // [grid+1]
+  __nv_bfloat16* out;
+  int64_t out_stride_tok;
+  float* ws_o;
+  float* ws_ml;
+  int max_pages;
+  int block_size;
+  int num_q_heads;
+  int group;       // G = Hq / Hkv
+  int tok_per_tile;  // 128 / G
+  int page_size;
+  int box_rows;    // min(page_size, 64)
+  float scale_log2;
+};
+
+int launch_paged_attn(int head_dim, const CUtensorMap& tq, const CUtensorMap& tk,
+                      const CUtensorMap& tv, const AttnParams& prm, int grid,
+                      const int32_t* groups, int n_groups, cudaStream_t stream);
+
+}  // namespace optimus

@@ -1,0 +1,480 @@
+// capi.cu — the extern "C" boundary (include/optimus_b200.h): argument
+// validation, TMA descriptor encoding (cached), the host-side split-KV /
+// persistent-CTA work planner, and kernel launches.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "../../include/optimus_b200.h"
+#include "attn.cuh"
+
+namespace optimus {
+
+int launch_kv_append(const void*, const void*, int64_t, const int32_t*, const int32_t*,
+                     const int32_t*, const int32_t*, int, int, int, int, int, void*, void*,
+                     int64_t*, cudaStream_t);
+int launch_unmask_partials(const void*, int, int64_t, const int32_t*, int, int, int, int, float*,
+                           cudaStream_t);
+int launch_unmask_finalize(const float*, int, int, int, const int32_t*, int, float, int, uint8_t*,
+                           int32_t*, float*, const int32_t*, uint8_t*, int32_t*, int64_t,
+                           cudaStream_t);
+
+}  // namespace optimus
+
+
+
+using namespace optimus;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(const char* what) {
+  g_last_error = what;
+  return OPTIMUS_EINVAL;
+}
+int cuda_status(int st, const char* where) {
+  if (st != 0) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(static_cast<cudaError_t>(st));
+  }
+  return st;
+}
+
+// -1 unknown, 0 not sm_100, 1 ok
+int g_arch_ok = -1;
+int g_sm_count = 0;
+std::mutex g_mu;
+
+int check_device() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_arch_ok < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      g_arch_ok = 0;
+    } else {
+      cudaDeviceProp prop;
+      if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+        g_arch_ok = 0;
+      } else {
+        g_arch_ok = (prop.major == 10 && prop.minor == 0) ? 1 : 0;
+        g_sm_count = prop.multiProcessorCount;
+      }
+    }
+  }
+  if (g_arch_ok != 1) {
+    g_last_error = "device is not an sm_100 (B200) GPU";
+    return OPTIMUS_ENOSYS;
+  }
+  return 0;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  uint64_t dims[4];
+  uint64_t strides[3];
+  uint32_t box[4];
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && !memcmp(dims, o.dims, sizeof(dims)) &&
+           !memcmp(strides, o.strides, sizeof(strides)) && !memcmp(box, o.box, sizeof(box));
+  }
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+};
+thread_local std::vector<MapEntry> g_maps;
+
+// 4-D bf16 tensor map with SWIZZLE_128B (boxes are 64 columns = 128 bytes wide).
+int get_map(const void* ptr, const uint64_t dims[4], const uint64_t strides[3],
+            const uint32_t box[4], CUtensorMap* out) {
+  MapKey key;
+  key.ptr = ptr;
+  memcpy(key.dims, dims, sizeof(key.dims));
+  memcpy(key.strides, strides, sizeof(key.strides));
+  memcpy(key.box, box, sizeof(key.box));
+  for (size_t i = 0; i < g_maps.size(); ++i)
+    if (g_maps[i].key == key) {
+      *out = g_maps[i].map;
+      return 0;
+    }
+  auto fn = encode_fn();
+  if (!fn) return fail("cuTensorMapEncodeTiled unavailable");
+  CUtensorMap m;
+  cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t gs[3] = {strides[0], strides[1], strides[2]};
+  cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), gd, gs, bd, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return fail(buf);
+  }
+  if (g_maps.size() >= 256) g_maps.erase(g_maps.begin());
+  g_maps.push_back({key, m});
+  *out = m;
+  return 0;
+}
+
+bool page_ok(int P) {
+  if (P < 8 || P % 8) return false;
+  return P <= 64 ? (64 % P == 0) : (P % 64 == 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+int optimus_version(void) { return 100; }
+
+const char* optimus_last_error(void) { return g_last_error.c_str(); }
+
+int optimus_device_sm_count(void) {
+  if (check_device() != 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      return n;
+    return 0;
+  }
+  return g_sm_count;
+}
+
+int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                      const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                      const int32_t* block_tables, int max_pages, int n_tok, int num_kv_heads,
+                      int head_dim, int page_size, void* k_cache, void* v_cache,
+                      int64_t num_pages, int64_t* slot_mapping_out, void* stream) {
+  if (n_tok < 0 || num_kv_heads < 1 || max_pages < 1 || num_pages < 1)
+    return fail("kv_append: bad sizes");
+  if (head_dim % 8 || head_dim < 8) return fail("kv_append: head_dim must be a multiple of 8");
+  if (new_stride_tok < static_cast<int64_t>(num_kv_heads) * head_dim || new_stride_tok % 8)
+    return fail("kv_append: new_stride_tok must be >= Hkv*head_dim and a multiple of 8");
+  if (page_size < 1) return fail("kv_append: page_size must be >= 1");
+  if (n_tok == 0) return 0;
+  if (!k_new || !v_new || !tok_req || !tok_pos || !prompt_len || !block_tables || !k_cache ||
+      !v_cache)
+    return fail("kv_append: null pointer");
+  if (int st = check_device()) return st;
+  return cuda_status(
+      launch_kv_append(k_new, v_new, new_stride_tok, tok_req, tok_pos, prompt_len, block_tables,
+                       max_pages, n_tok, num_kv_heads, head_dim, page_size, k_cache, v_cache,
+                       slot_mapping_out, static_cast<cudaStream_t>(stream)),
+      "kv_append");
+}
+
+int optimus_attn_plan_bounds(int n_req, const int32_t* cu, const int32_t* key_end, int hq,
+                             int hkv, int min_split_tiles, int* max_work, int* max_groups) {
+  if (n_req < 0 || hkv < 1 || hq % hkv) return fail("attn_plan_bounds: bad heads");
+  const int G = hq / hkv;
+  if (G > 128) return fail("attn_plan_bounds: group size > 128");
+  const int T = 128 / G;
+  if (min_split_tiles < 1) min_split_tiles = 1;
+  long long w = 0, g = 0;
+  for (int r = 0; r < n_req; ++r) {
+    const int nq = cu[r + 1] - cu[r];
+    if (nq <= 0) continue;
+    const int mt = (nq + T - 1) / T;
+    const int nt = (key_end[r] + 63) / 64;
+    const int maxs = std::max(1, nt / min_split_tiles);
+    w += static_cast<long long>(hkv) * mt * maxs;
+    g += static_cast<long long>(hkv) * mt;
+  }
+  *max_work = static_cast<int>(w);
+  *max_groups = static_cast<int>(g);
+  return 0;
+}
+
+int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int hq, int hkv,
+                      int grid, int min_split_tiles, int32_t* work, int max_work,
+                      int32_t* cta_off, int32_t* groups, int max_groups, int* n_groups_out,
+                      int* n_partials_out) {
+  if (n_req < 0 || hkv < 1 || hq % hkv || grid < 1) return fail("attn_plan: bad arguments");
+  const int G = hq / hkv;
+  if (G > 128) return fail("attn_plan: group size > 128");
+  const int T = 128 / G;
+  if (min_split_tiles < 1) min_split_tiles = 1;
+  struct Unit {
+    int req, head, tok_begin, n_tok, tiles;
+  };
+  std::vector<Unit> units;
+  long long total = 0;
+  int max_tiles = 0;
+  for (int r = 0; r < n_req; ++r) {
+    const int nq = cu[r + 1] - cu[r];
+    if (nq <= 0) continue;
+    if (key_end[r] < 1) return fail("attn_plan: key_end must be >= 1 for a request with queries");
+    const int nt = (key_end[r] + 63) / 64;
+    for (int h = 0; h < hkv; ++h)
+      for (int t0 = 0; t0 < nq; t0 += T) {
+        units.push_back({r, h, cu[r] + t0, std::min(T, nq - t0), nt});
+        total += nt;
+        max_tiles = std::max(max_tiles, nt);
+      }
+  }
+  // Cost model (in 64-key tile units): every item pays a fixed prologue/epilogue
+  // (Q load, O drain) and a split item also pays its partial write + combine read.
+  const double kItem = 2.0, kSplit = 3.0;
+  auto split_count = [&](int tiles, int cap) {
+    if (tiles <= cap) return 1;
+    int s = (tiles + cap - 1) / cap;
+    return std::min(s, std::max(1, tiles / min_split_tiles));
+  };
+  int best_cap = std::max(max_tiles, 1);
+  double best_span = 1e300;
+  const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16};
+  for (int c : cands) {
+    int cap = std::max(min_split_tiles, (max_tiles + c - 1) / c);
+    std::vector<double> costs;
+    double sum = 0;
+    for (const Unit& u : units) {
+      const int s = split_count(u.tiles, cap);
+      const int base = u.tiles / s, rem = u.tiles % s;
+      for (int k = 0; k < s; ++k) {
+        const double cst = (base + (k < rem ? 1 : 0)) + kItem + (s > 1 ? kSplit : 0.0);
+        costs.push_back(cst);
+        sum += cst;
+      }
+    }
+    if (static_cast<long long>(costs.size()) > max_work) continue;
+    std::sort(costs.begin(), costs.end(), std::greater<double>());
+    std::priority_queue<double, std::vector<double>, std::greater<double>> heap;
+    for (int i = 0; i < grid; ++i) heap.push(0.0);
+    double span = 0;
+    for (double cst : costs) {
+      double l = heap.top();
+      heap.pop();
+      l += cst;
+      span = std::max(span, l);
+      heap.push(l);
+    }
+    if (span < best_span - 1e-9) {
+      best_span = span;
+      best_cap = cap;
+    }
+  }
+  // Materialise items with the chosen cap.
+  struct Item {
+    int req, head, tok_begin, n_tok, key_begin, key_end, slot;
+    double cost;
+  };
+  std::vector<Item> items;
+  int n_groups = 0, n_partials = 0;
+  for (const Unit& u : units) {
+    const int s = split_count(u.tiles, best_cap);
+    const int base = u.tiles / s, rem = u.tiles % s;
+    const int kend = key_end[u.req];
+    int t0 = 0;
+    if (s > 1) {
+      if (n_groups >= max_groups) return fail("attn_plan: groups buffer too small");
+      int32_t* g = groups + 8 * n_groups;
+      g[0] = u.req;
+      g[1] = u.head;
+      g[2] = u.tok_begin;
+      g[3] = u.n_tok;
+      g[4] = n_partials;
+      g[5] = s;
+      g[6] = 0;
+      g[7] = 0;
+      ++n_groups;
+    }
+    for (int k = 0; k < s; ++k) {
+      const int nt = base + (k < rem ? 1 : 0);
+      Item it;
+      it.req = u.req;
+      it.head = u.head;
+      it.tok_begin = u.tok_begin;
+      it.n_tok = u.n_tok;
+      it.key_begin = t0 * 64;
+      it.key_end = std::min(kend, (t0 + nt) * 64);
+      it.slot = s > 1 ? n_partials++ : -1;
+      it.cost = nt + kItem + (s > 1 ? kSplit : 0.0);
+      items.push_back(it);
+      t0 += nt;
+    }
+  }
+  if (static_cast<int>(items.size()) > max_work) return fail("attn_plan: work buffer too small");
+  // Longest-processing-time-first assignment to persistent CTAs.
+  std::vector<int> order(items.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return items[a].cost > items[b].cost; });
+  typedef std::pair<double, int> LoadCta;
+  std::priority_queue<LoadCta, std::vector<LoadCta>, std::greater<LoadCta>> heap;
+  for (int i = 0; i < grid; ++i) heap.push(LoadCta(0.0, i));
+  std::vector<std::vector<int>> per(grid);
+  for (int idx : order) {
+    LoadCta lc = heap.top();
+    heap.pop();
+    per[lc.second].push_back(idx);
+    lc.first += items[idx].cost;
+    heap.push(lc);
+  }
+  int pos = 0;
+  for (int c = 0; c < grid; ++c) {
+    cta_off[c] = pos;
+    for (int idx : per[c]) {
+      const Item& it = items[idx];
+      int32_t* w = work + 8 * pos;
+      w[0] = it.req;
+      w[1] = it.head;
+      w[2] = it.tok_begin;
+      w[3] = it.n_tok;
+      w[4] = it.key_begin;
+      w[5] = it.key_end;
+      w[6] = it.slot;
+      w[7] = 0;
+      ++pos;
+    }
+  }
+  cta_off[grid] = pos;
+  *n_groups_out = n_groups;
+  *n_partials_out = n_partials;
+  return pos;
+}
+
+int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, const void* k_cache,
+                       const void* v_cache, int64_t num_pages, const int32_t* q_pos,
+                       const int32_t* prompt_len, const int32_t* vis_base, const int32_t* vis_off,
+                       const uint32_t* vis_words, const int32_t* block_tables, int max_pages,
+                       const int32_t* work, const int32_t* cta_off, int grid,
+                       const int32_t* groups, int n_groups, int block_size, int hq, int hkv,
+                       int head_dim, int page_size, float sm_scale, void* out,
+                       int64_t out_stride_tok, float* ws_o, float* ws_ml, void* stream) {
+  if (head_dim != 64 && head_dim != 128) return fail("paged_attn: head_dim must be 64 or 128");
+  if (hkv < 1 || hq % hkv) return fail("paged_attn: Hq must be a multiple of Hkv");
+  const int G = hq / hkv;
+  if (G > 128) return fail("paged_attn: group size > 128");
+  if (!page_ok(page_size))
+    return fail("paged_attn: page_size must be a multiple of 8 that divides 64 or is a multiple of 64");
+  if (block_size < 1) return fail("paged_attn: block_size must be >= 1");
+  if (q_stride_tok % 8 || q_stride_tok < static_cast<int64_t>(hq) * head_dim)
+    return fail("paged_attn: q_stride_tok must be >= Hq*head_dim and a multiple of 8");
+  if (out_stride_tok % 8 || out_stride_tok < static_cast<int64_t>(hq) * head_dim)
+    return fail("paged_attn: out_stride_tok must be >= Hq*head_dim and a multiple of 8");
+  if (grid < 0 || n_groups < 0 || num_pages < 1 || max_pages < 1)
+    return fail("paged_attn: bad sizes");
+  if (n_tok_total == 0 || grid == 0) return 0;
+  if (n_groups > 0 && (!ws_o || !ws_ml)) return fail("paged_attn: split-KV needs a workspace");
+  if (reinterpret_cast<uintptr_t>(q) % 16 || reinterpret_cast<uintptr_t>(k_cache) % 16 ||
+      reinterpret_cast<uintptr_t>(v_cache) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+    return fail("paged_attn: tensors must be 16-byte aligned");
+  if (int st = check_device()) return st;
+  const int T = 128 / G;
+  CUtensorMap tq, tk, tv;
+  {
+    const uint64_t dims[4] = {static_cast<uint64_t>(head_dim), static_cast<uint64_t>(G),
+                              static_cast<uint64_t>(hkv), static_cast<uint64_t>(n_tok_total)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(head_dim) * 2,
+                                 static_cast<uint64_t>(G) * head_dim * 2,
+                                 static_cast<uint64_t>(q_stride_tok) * 2};
+    const uint32_t box[4] = {64, static_cast<uint32_t>(G), 1, static_cast<uint32_t>(T)};
+    if (int st = get_map(q, dims, strides, box, &tq)) return st;
+  }
+  const int box_rows = std::min(page_size, 64);
+  {
+    const uint64_t dims[4] = {static_cast<uint64_t>(head_dim), static_cast<uint64_t>(page_size),
+                              static_cast<uint64_t>(hkv), static_cast<uint64_t>(num_pages)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(head_dim) * 2,
+                                 static_cast<uint64_t>(page_size) * head_dim * 2,
+                                 static_cast<uint64_t>(hkv) * page_size * head_dim * 2};
+    const uint32_t box[4] = {64, static_cast<uint32_t>(box_rows), 1, 1};
+    if (int st = get_map(k_cache, dims, strides, box, &tk)) return st;
+    if (int st = get_map(v_cache, dims, strides, box, &tv)) return st;
+  }
+  AttnParams prm;
+  prm.q_pos = q_pos;
+  prm.prompt_len = prompt_len;
+  prm.vis_base = vis_base;
+  prm.vis_off = vis_off;
+  prm.vis_words = vis_words;
+  prm.block_tables = block_tables;
+  prm.work = work;
+  prm.cta_off = cta_off;
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.out_stride_tok = out_stride_tok;
+  prm.ws_o = ws_o;
+  prm.ws_ml = ws_ml;
+  prm.max_pages = max_pages;
+  prm.block_size = block_size;
+  prm.num_q_heads = hq;
+  prm.group = G;
+  prm.tok_per_tile = T;
+  prm.page_size = page_size;
+  prm.box_rows = box_rows;
+  prm.scale_log2 = sm_scale * 1.4426950408889634f;
+  return cuda_status(launch_paged_attn(head_dim, tq, tk, tv, prm, grid, groups, n_groups,
+                                       static_cast<cudaStream_t>(stream)),
+                     "paged_attn");
+}
+
+int optimus_unmask_splits(int n_rows, int vocab) {
+  int sms = optimus_device_sm_count();
+  if (sms <= 0) sms = 148;
+  if (n_rows <= 0) return 1;
+  // 8 resident 256-thread CTAs per SM; aim for >= 2 waves, slices >= 8K columns.
+  const long long slots = static_cast<long long>(sms) * 8 * 2;
+  long long s = (slots + n_rows - 1) / n_rows;
+  const long long max_s = std::max(1, vocab / 8192);
+  s = std::max(1LL, std::min(s, max_s));
+  return static_cast<int>(s);
+}
+
+int optimus_unmask_partials(const void* logits, int logits_dtype, int64_t row_stride,
+                            const int32_t* row_src, int n_rows, int vocab, int vocab_offset,
+                            int n_vsplit, float* part, void* stream) {
+  if (logits_dtype != 0 && logits_dtype != 1) return fail("unmask: logits_dtype must be 0 or 1");
+  const int vec = logits_dtype == 0 ? 8 : 4;
+  if (vocab < 1 || vocab % vec) return fail("unmask: vocab must be a multiple of 8 (bf16) / 4 (fp32)");
+  if (row_stride % vec || row_stride < vocab) return fail("unmask: bad row_stride");
+  if (n_rows < 0 || n_vsplit < 1) return fail("unmask: bad sizes");
+  if (n_rows == 0) return 0;
+  if (!logits || !part) return fail("unmask: null pointer");
+  if (reinterpret_cast<uintptr_t>(logits) % 16) return fail("unmask: logits must be 16-byte aligned");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_unmask_partials(logits, logits_dtype, row_stride, row_src, n_rows,
+                                            vocab, vocab_offset, n_vsplit, part,
+                                            static_cast<cudaStream_t>(stream)),
+                     "unmask_partials");
+}
+
+int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vsplit,
+                            const int32_t* cu_rows, int n_req, float tau, int fallback_mode,
+                            uint8_t* commit_mask, int32_t* tok, float* conf,
+                            const int32_t* row_pos, uint8_t* state, int32_t* token_buf,
+                            int64_t state_stride, void* stream) {
+  if (n_outer < 1 || n_rows < 0 || n_vsplit < 1 || n_req < 0) return fail("unmask: bad sizes");
+  if (fallback_mode != 0 && fallback_mode != 1) return fail("unmask: fallback_mode must be 0 or 1");
+  if (n_req == 0) return 0;
+  if (!part || !cu_rows || !commit_mask || !tok || !conf) return fail("unmask: null pointer");
+  if (state && !row_pos) return fail("unmask: state update needs row_pos");
+  if (int st = check_device()) return st;
+  return cuda_status(
+      launch_unmask_finalize(part, n_outer, n_rows, n_vsplit, cu_rows, n_req, tau, fallback_mode,
+                             commit_mask, tok, conf, row_pos, state, token_buf, state_stride,
+                             static_cast<cudaStream_t>(stream)),
+      "unmask_finalize");
+}
+
+}  // extern "C"

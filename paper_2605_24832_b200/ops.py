@@ -1,0 +1,293 @@
+"""Torch-facing wrappers of the C-ABI kernels (K1 append, K2 attention, K3 unmask).
+
+Torch is only the allocator/stream provider here: every wrapper checks that its
+tensors live on a CUDA device, passes raw pointers through ctypes, and maps a
+non-zero status to ``ConfigError`` / ``DeviceError``.  Nothing here computes on
+the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError
+
+FALLBACK_MODES = {"earliest": 0, "top1": 1}
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _cuda(*tensors: Optional[torch.Tensor]) -> None:
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise ConfigError("B200 kernels take CUDA tensors only (no CPU path)")
+
+
+def _stream(stream: Optional[torch.cuda.Stream] = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def sm_count() -> int:
+    return int(_lib.call("optimus_device_sm_count"))
+
+
+# --------------------------------------------------------------------------- K1
+def kv_append(
+    k_new: torch.Tensor,
+    v_new: torch.Tensor,
+    tok_req: torch.Tensor,
+    tok_pos: torch.Tensor,
+    prompt_len: torch.Tensor,
+    block_tables: torch.Tensor,
+    k_cache: torch.Tensor,
+    v_cache: torch.Tensor,
+    slot_mapping_out: Optional[torch.Tensor] = None,
+    stream=None,
+) -> None:
+    """Scatter ``k_new``/``v_new`` ``[n_tok, Hkv, d]`` into ``[num_pages, Hkv, P, d]`` caches."""
+    _cuda(k_new, v_new, tok_req, tok_pos, prompt_len, block_tables, k_cache, v_cache, slot_mapping_out)
+    n_tok = k_new.shape[0]
+    num_pages, hkv, page, d = k_cache.shape
+    if k_new.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16:
+        raise ConfigError("kv_append: bf16 K/V only")
+    if k_new.stride(-1) != 1 or k_new.stride(-2) != d or v_new.stride(0) != k_new.stride(0):
+        raise ConfigError("kv_append: K/V rows must be [n_tok, Hkv, d] with unit inner strides")
+    st = _lib.call(
+        "optimus_kv_append",
+        _ptr(k_new), _ptr(v_new), k_new.stride(0),
+        _ptr(tok_req), _ptr(tok_pos), _ptr(prompt_len), _ptr(block_tables),
+        block_tables.shape[1], n_tok, hkv, d, page,
+        _ptr(k_cache), _ptr(v_cache), num_pages, _ptr(slot_mapping_out), _stream(stream),
+    )
+    _lib.check(st, "optimus_kv_append")
+
+
+# --------------------------------------------------------------------------- K2 plan
+@dataclass
+class AttnPlan:
+    """Output of the host work planner, resident on the device."""
+
+    grid: int
+    n_work: int
+    n_groups: int
+    n_partials: int
+    work: torch.Tensor      # int32 [n_work, 8]
+    cta_off: torch.Tensor   # int32 [grid + 1]
+    groups: torch.Tensor    # int32 [n_groups, 8]
+    work_host: np.ndarray
+    cta_off_host: np.ndarray
+    groups_host: np.ndarray
+
+
+def plan_attention(
+    cu_seqlens_q: np.ndarray,
+    key_end: np.ndarray,
+    num_q_heads: int,
+    num_kv_heads: int,
+    grid: Optional[int] = None,
+    min_split_tiles: int = 4,
+    device: Optional[torch.device] = None,
+) -> AttnPlan:
+    """Split (request, kv head, query tile) units into key ranges and place them
+    on persistent CTAs (``optimus_attn_plan``)."""
+    cu = np.ascontiguousarray(cu_seqlens_q, dtype=np.int32)
+    ke = np.ascontiguousarray(key_end, dtype=np.int32)
+    n_req = len(ke)
+    if grid is None:
+        grid = sm_count() if torch.cuda.is_available() else 148
+    mw, mg = C.c_int(0), C.c_int(0)
+    _lib.check(
+        _lib.call(
+            "optimus_attn_plan_bounds", n_req, cu.ctypes.data, ke.ctypes.data,
+            num_q_heads, num_kv_heads, min_split_tiles, C.byref(mw), C.byref(mg),
+        ),
+        "optimus_attn_plan_bounds",
+    )
+    work = np.zeros((max(mw.value, 1), 8), dtype=np.int32)
+    groups = np.zeros((max(mg.value, 1), 8), dtype=np.int32)
+    cta_off = np.zeros(grid + 1, dtype=np.int32)
+    ng, npart = C.c_int(0), C.c_int(0)
+    n = _lib.call(
+        "optimus_attn_plan", n_req, cu.ctypes.data, ke.ctypes.data, num_q_heads, num_kv_heads,
+        grid, min_split_tiles, work.ctypes.data, work.shape[0], cta_off.ctypes.data,
+        groups.ctypes.data, groups.shape[0], C.byref(ng), C.byref(npart),
+    )
+    if n < 0:
+        _lib.check(n, "optimus_attn_plan")
+    work = work[:n]
+    groups = groups[: ng.value]
+    if device is None:
+        dev_work = torch.from_numpy(work.copy())
+        dev_off = torch.from_numpy(cta_off.copy())
+        dev_groups = torch.from_numpy(groups.copy())
+    else:
+        dev_work = torch.from_numpy(work).to(device)
+        dev_off = torch.from_numpy(cta_off).to(device)
+        dev_groups = torch.from_numpy(groups).to(device)
+    return AttnPlan(grid, n, ng.value, npart.value, dev_work, dev_off, dev_groups, work, cta_off, groups)
+
+
+# --------------------------------------------------------------------------- K2
+def paged_attention(
+    q: torch.Tensor,
+    k_cache: torch.Tensor,
+    v_cache: torch.Tensor,
+    q_pos: torch.Tensor,
+    prompt_len: torch.Tensor,
+    vis_base: torch.Tensor,
+    vis_off: torch.Tensor,
+    vis_words: torch.Tensor,
+    block_tables: torch.Tensor,
+    plan: AttnPlan,
+    block_size: int,
+    sm_scale: Optional[float] = None,
+    out: Optional[torch.Tensor] = None,
+    ws_o: Optional[torch.Tensor] = None,
+    ws_ml: Optional[torch.Tensor] = None,
+    stream=None,
+) -> torch.Tensor:
+    """Varlen paged attention with the streaming-decode visibility rule.
+
+    ``q``: ``[n_tok, Hq, d]`` bf16; caches ``[num_pages, Hkv, P, d]`` bf16.
+    Returns ``out`` ``[n_tok, Hq, d]`` bf16.
+    """
+    _cuda(q, k_cache, v_cache, q_pos, prompt_len, vis_base, vis_off, vis_words, block_tables, out)
+    n_tok, hq, d = q.shape
+    num_pages, hkv, page, d2 = k_cache.shape
+    if d2 != d:
+        raise ConfigError("paged_attention: head_dim mismatch between q and cache")
+    if q.stride(-1) != 1 or q.stride(-2) != d:
+        raise ConfigError("paged_attention: q must be [n_tok, Hq, d] with unit inner strides")
+    if out is None:
+        out = torch.empty((n_tok, hq, d), dtype=torch.bfloat16, device=q.device)
+    if plan.n_partials > 0:
+        need_o = plan.n_partials * 128 * d
+        need_ml = plan.n_partials * 128 * 2
+        if ws_o is None or ws_o.numel() < need_o:
+            ws_o = torch.empty(need_o, dtype=torch.float32, device=q.device)
+        if ws_ml is None or ws_ml.numel() < need_ml:
+            ws_ml = torch.empty(need_ml, dtype=torch.float32, device=q.device)
+    scale = float(sm_scale) if sm_scale is not None else 1.0 / float(d) ** 0.5
+    st = _lib.call(
+        "optimus_paged_attn",
+        _ptr(q), q.stride(0), n_tok,
+        _ptr(k_cache), _ptr(v_cache), num_pages,
+        _ptr(q_pos), _ptr(prompt_len), _ptr(vis_base), _ptr(vis_off), _ptr(vis_words),
+        _ptr(block_tables), block_tables.shape[1],
+        _ptr(plan.work), _ptr(plan.cta_off), plan.grid if plan.n_work else 0,
+        _ptr(plan.groups), plan.n_groups,
+        block_size, hq, hkv, d, page, scale,
+        _ptr(out), out.stride(0),
+        _ptr(ws_o) if plan.n_partials else None, _ptr(ws_ml) if plan.n_partials else None,
+        _stream(stream),
+    )
+    _lib.check(st, "optimus_paged_attn")
+    return out
+
+
+# --------------------------------------------------------------------------- K3
+@dataclass
+class UnmaskResult:
+    commit_mask: torch.Tensor  # uint8 [n_rows]
+    tokens: torch.Tensor       # int32 [n_rows]
+    conf: torch.Tensor         # float32 [n_rows]
+
+
+def unmask_splits(n_rows: int, vocab: int) -> int:
+    return int(_lib.call("optimus_unmask_splits", n_rows, vocab))
+
+
+def unmask_partials(
+    logits: torch.Tensor,
+    row_src: Optional[torch.Tensor],
+    n_rows: int,
+    n_vsplit: int,
+    vocab_offset: int = 0,
+    part: Optional[torch.Tensor] = None,
+    stream=None,
+) -> torch.Tensor:
+    """Phase (a): per (row, vocab split) ``{max, sumexp, argmax}`` records."""
+    _cuda(logits, row_src, part)
+    if logits.dtype == torch.bfloat16:
+        dt = 0
+    elif logits.dtype == torch.float32:
+        dt = 1
+    else:
+        raise ConfigError("unmask: logits must be bf16 or fp32")
+    if logits.stride(-1) != 1:
+        raise ConfigError("unmask: logits rows must be contiguous")
+    vocab = logits.shape[-1]
+    if part is None:
+        part = torch.empty((max(n_rows, 1), n_vsplit, 3), dtype=torch.float32, device=logits.device)
+    st = _lib.call(
+        "optimus_unmask_partials", _ptr(logits), dt, logits.stride(0), _ptr(row_src),
+        n_rows, vocab, vocab_offset, n_vsplit, _ptr(part), _stream(stream),
+    )
+    _lib.check(st, "optimus_unmask_partials")
+    return part
+
+
+def unmask_finalize(
+    part: torch.Tensor,
+    n_outer: int,
+    n_rows: int,
+    n_vsplit: int,
+    cu_rows: torch.Tensor,
+    tau: float,
+    fallback: str = "earliest",
+    row_pos: Optional[torch.Tensor] = None,
+    state: Optional[torch.Tensor] = None,
+    token_buf: Optional[torch.Tensor] = None,
+    result: Optional[UnmaskResult] = None,
+    stream=None,
+) -> UnmaskResult:
+    """Phase (b): merge partials, threshold at ``tau``, apply the progress rule."""
+    _cuda(part, cu_rows, row_pos, state, token_buf)
+    if fallback not in FALLBACK_MODES:
+        raise ConfigError(f"unknown fallback mode {fallback!r}")
+    dev = part.device
+    if result is None:
+        result = UnmaskResult(
+            torch.empty(max(n_rows, 1), dtype=torch.uint8, device=dev),
+            torch.empty(max(n_rows, 1), dtype=torch.int32, device=dev),
+            torch.empty(max(n_rows, 1), dtype=torch.float32, device=dev),
+        )
+    n_req = cu_rows.shape[0] - 1
+    st = _lib.call(
+        "optimus_unmask_finalize", _ptr(part), n_outer, n_rows, n_vsplit, _ptr(cu_rows), n_req,
+        float(tau), FALLBACK_MODES[fallback], _ptr(result.commit_mask), _ptr(result.tokens),
+        _ptr(result.conf), _ptr(row_pos), _ptr(state), _ptr(token_buf),
+        state.stride(0) if state is not None else 0, _stream(stream),
+    )
+    _lib.check(st, "optimus_unmask_finalize")
+    return result
+
+
+def unmask_commit(
+    logits: torch.Tensor,
+    cu_rows: torch.Tensor,
+    tau: float = 0.9,
+    fallback: str = "earliest",
+    row_src: Optional[torch.Tensor] = None,
+    n_rows: Optional[int] = None,
+    n_vsplit: Optional[int] = None,
+    stream=None,
+) -> UnmaskResult:
+    """Single-GPU K3: partials + finalize over the whole vocabulary."""
+    if n_rows is None:
+        n_rows = logits.shape[0] if row_src is None else row_src.shape[0]
+    if n_vsplit is None:
+        n_vsplit = unmask_splits(n_rows, logits.shape[-1])
+    part = unmask_partials(logits, row_src, n_rows, n_vsplit, stream=stream)
+    return unmask_finalize(part, 1, n_rows, n_vsplit, cu_rows, tau, fallback, stream=stream)

@@ -1,0 +1,140 @@
+"""Generate golden vectors by running the reference package ``dllmsim`` itself.
+
+Run in the build container (the reference is not available on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes (small, committed):
+  control.json  step-by-step replays of plan_chunk / apply_chunk under the
+                StochasticOracle (engine.py:45-95, commit.py:86-112) plus the
+                hand-written cases of the reference's test_engine.py:50-157.
+  commits.json  commit_step decisions for seeded windows (commit.py:86-112) and
+                calibrate_q goldens (test_commit.py:54-57).
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from dllmsim.commit import CommitProfile, StochasticOracle, calibrate_q, commit_step  # noqa: E402
+from dllmsim.core import Request, TokenState, WindowRule  # noqa: E402
+from dllmsim.engine import apply_chunk, plan_chunk  # noqa: E402
+from dllmsim.workload import PROFILES, calibrated_profile  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def replay_case(seed: int, out_tokens: int, chunk: int, block: int, rule: str, q: float, m: float,
+                chunk_schedule=None) -> dict:
+    rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(1, seed)))
+    req = Request(id=seed, arrival_time=0.0, prompt_tokens=7, output_tokens=out_tokens, rng=rng)
+    req.rate_multiplier = m
+    oracle = StochasticOracle(CommitProfile(q=q))
+    wr = WindowRule.IN_BLOCK if rule == "in_block" else WindowRule.OUT_BLOCK
+    steps = []
+    guard = 0
+    while not req.finished and guard < 10 * out_tokens + 50:
+        c = chunk if chunk_schedule is None else chunk_schedule[guard % len(chunk_schedule)]
+        plan = plan_chunk(req, c, block, wr)
+        before = {
+            "states": req.states.tolist(),
+            "queue": list(req.uncached_queue),
+            "block": req.block_index,
+            "committed": req.committed,
+        }
+        commits = oracle.commits(req, plan.window) if plan.window else set()
+        apply_chunk(req, plan, commits, block)
+        steps.append({
+            "chunk": c,
+            "before": before,
+            "kv": list(plan.kv_positions),
+            "window": list(plan.window),
+            "commits": sorted(commits),
+            "after_block": req.block_index,
+        })
+        guard += 1
+    return {
+        "seed": seed, "out": out_tokens, "chunk": chunk, "block": block, "rule": rule,
+        "q": q, "m": m, "schedule": chunk_schedule, "steps": steps,
+        "final_states": req.states.tolist(), "final_queue": list(req.uncached_queue),
+    }
+
+
+def engine_cases() -> list:
+    """The reference's hand-written plan/apply cases (test_engine.py:50-157)."""
+    cases = []
+
+    def mk(n):
+        return Request(id=0, arrival_time=0.0, prompt_tokens=1, output_tokens=n,
+                       rng=np.random.default_rng(0))
+
+    r = mk(8)
+    p = plan_chunk(r, 4, 8)
+    cases.append({"name": "fresh", "out": 8, "states": r.states.tolist(), "queue": [], "block": 0,
+                  "chunk": 4, "bs": 8, "rule": "in_block", "kv": list(p.kv_positions), "window": list(p.window)})
+    r = mk(8)
+    r.states[0] = r.states[1] = TokenState.DECODED_UNCACHED
+    r.uncached_queue.extend([0, 1])
+    p = plan_chunk(r, 4, 8)
+    cases.append({"name": "backlog_first", "out": 8, "states": r.states.tolist(), "queue": [0, 1], "block": 0,
+                  "chunk": 4, "bs": 8, "rule": "in_block", "kv": list(p.kv_positions), "window": list(p.window)})
+    r = mk(40)
+    r.states[0:7] = TokenState.DECODED_CACHED
+    r.committed = 7
+    r.advance_blocks(8)
+    for rule, wr in (("out_block", WindowRule.OUT_BLOCK), ("in_block", WindowRule.IN_BLOCK)):
+        p = plan_chunk(r, 6, 8, wr)
+        cases.append({"name": f"cross_{rule}", "out": 40, "states": r.states.tolist(), "queue": [],
+                      "block": r.block_index, "chunk": 6, "bs": 8, "rule": rule,
+                      "kv": list(p.kv_positions), "window": list(p.window)})
+    return cases
+
+
+def main() -> None:
+    sharegpt = calibrated_profile(PROFILES["sharegpt"], "dense-8b")
+    cases = []
+    k = 0
+    for rule in ("in_block", "out_block"):
+        for chunk in (2, 4, 8, 16, 32):
+            for out_tokens in (5, 33, 70, 97):
+                cases.append(replay_case(1000 + k, out_tokens, chunk, 32, rule, sharegpt.q, 1.0))
+                k += 1
+    # alternating chunk sizes (the elastic scheduler switches chunk every step)
+    for sched in ([32, 2], [2, 8, 16], [6, 32, 4]):
+        cases.append(replay_case(2000 + k, 90, 0, 32, "in_block", sharegpt.q, 1.3, sched))
+        k += 1
+    # small blocks
+    for bs in (4, 8):
+        cases.append(replay_case(3000 + k, 41, 6, bs, "in_block", 0.7, 0.8))
+        k += 1
+    (OUT / "control.json").write_text(json.dumps({"replays": cases, "engine_cases": engine_cases()}))
+
+    draws = []
+    for seed in range(40):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(1, 33))
+        q = float(rng.uniform(0.3, 0.95))
+        m = float(rng.uniform(0.5, 2.0))
+        start = int(rng.integers(0, 50))
+        window = list(range(start, start + n))
+        rr = np.random.default_rng(10_000 + seed)
+        commits = commit_step(CommitProfile(q=q), m, window, rr)
+        draws.append({"seed": 10_000 + seed, "q": q, "m": m, "window": window, "commits": sorted(commits)})
+    golden_q = {
+        "calibrate_32_5.29": calibrate_q(32, 5.29),
+        "calibrate_32_2.51": calibrate_q(32, 2.51),
+        "sharegpt_dense8b_q": sharegpt.q,
+        "sharegpt_dense8b_sigma": sharegpt.rate_jitter_sigma,
+    }
+    (OUT / "commits.json").write_text(json.dumps({"draws": draws, "q": golden_q}))
+    print("wrote", OUT / "control.json", OUT / "commits.json", len(cases), "replays")
+
+
+if __name__ == "__main__":
+    main()

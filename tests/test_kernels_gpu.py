@@ -1,0 +1,187 @@
+"""GPU parity of the three kernels against the CPU oracle (oracle/numeric.py).
+
+Tolerances (BASELINE.json north_star): slot mapping / KV pages / commit masks /
+argmax tokens bit-exact (masks only where |conf - tau| > 1e-4); attention
+outputs within 2e-3 relative error measured per output row (Frobenius norm of
+the row), bf16 inputs, fp32 accumulation, bf16 output.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numeric as on
+from paper_2605_24832_b200 import engine as pe
+from paper_2605_24832_b200 import ops
+from paper_2605_24832_b200.meta import DeviceMeta, build_step_meta
+from tests.scenario import make_block_tables, make_requests
+
+pytestmark = pytest.mark.gpu
+
+ATTN_RTOL = 2e-3
+
+
+def _bf16(rng, shape, scale=1.0):
+    return torch.from_numpy((rng.standard_normal(shape) * scale).astype(np.float32)).to(torch.bfloat16)
+
+
+def _step(seed, n_req, chunk, block, page, hq, hkv, d, rule="in_block", prompt_range=(1, 300),
+          out_range=(2, 200), fixed_prompt=None):
+    rng = np.random.default_rng(seed)
+    reqs = make_requests(seed, n_req, prompt_range, out_range, chunk, block, rule, fixed_prompt=fixed_prompt)
+    plans = pe.plan_batch(reqs, chunk, block, rule)
+    bt, num_pages = make_block_tables(rng, reqs, page)
+    meta = build_step_meta(reqs, plans, block, bt)
+    dev = torch.device("cuda")
+    dm = DeviceMeta.upload(meta, dev)
+    k_cache = _bf16(rng, (num_pages, hkv, page, d))
+    v_cache = _bf16(rng, (num_pages, hkv, page, d))
+    n_tok = meta.n_tok
+    q = _bf16(rng, (max(n_tok, 1), hq, d))
+    k_new = _bf16(rng, (max(n_tok, 1), hkv, d))
+    v_new = _bf16(rng, (max(n_tok, 1), hkv, d))
+    return dict(rng=rng, reqs=reqs, plans=plans, bt=bt, meta=meta, dm=dm, k_cache=k_cache,
+                v_cache=v_cache, q=q, k_new=k_new, v_new=v_new, num_pages=num_pages,
+                block=block, page=page, hq=hq, hkv=hkv, d=d)
+
+
+def _run_append(s):
+    dev = torch.device("cuda")
+    kc, vc = s["k_cache"].to(dev), s["v_cache"].to(dev)
+    slots = torch.empty(max(s["meta"].n_tok, 1), dtype=torch.int64, device=dev)
+    ops.kv_append(s["k_new"].to(dev)[: s["meta"].n_tok], s["v_new"].to(dev)[: s["meta"].n_tok],
+                  s["dm"].tok_req, s["dm"].tok_pos, s["dm"].prompt_len, s["dm"].block_tables,
+                  kc, vc, slot_mapping_out=slots)
+    return kc, vc, slots
+
+
+@pytest.mark.parametrize("page,d,hkv", [(16, 128, 8), (64, 128, 2), (16, 64, 4), (32, 64, 2)])
+def test_kv_append_bit_exact(page, d, hkv):
+    s = _step(1, 9, 8, 32, page, hkv * 2, hkv, d)
+    kc, vc, slots = _run_append(s)
+    torch.cuda.synchronize()
+    m = s["meta"]
+    ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.bt if hasattr(m, "bt") else m.block_tables, page)
+    assert np.array_equal(slots.cpu().numpy()[: m.n_tok], ref_slots)
+    k_ref = s["k_cache"].view(torch.int16).numpy().copy()
+    v_ref = s["v_cache"].view(torch.int16).numpy().copy()
+    on.kv_append(k_ref, v_ref, s["k_new"].view(torch.int16).numpy()[: m.n_tok],
+                 s["v_new"].view(torch.int16).numpy()[: m.n_tok], ref_slots, page)
+    assert np.array_equal(kc.cpu().view(torch.int16).numpy(), k_ref)
+    assert np.array_equal(vc.cpu().view(torch.int16).numpy(), v_ref)
+
+
+def _attn_check(s, min_split_tiles=4, grid=None):
+    dev = torch.device("cuda")
+    kc, vc, _ = _run_append(s)
+    m = s["meta"]
+    plan = ops.plan_attention(m.cu_seqlens, m.key_end, s["hq"], s["hkv"], grid=grid,
+                              min_split_tiles=min_split_tiles, device=dev)
+    q = s["q"].to(dev)[: m.n_tok]
+    out = ops.paged_attention(q, kc, vc, s["dm"].tok_pos, s["dm"].prompt_len, s["dm"].vis_base,
+                              s["dm"].vis_off, s["dm"].vis_words, s["dm"].block_tables, plan,
+                              s["block"])
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    kf = kc.float().cpu().numpy()
+    vf = vc.float().cpu().numpy()
+    vis_list = [on.visible_outputs(r.states, list(p.kv_positions) + list(p.window))
+                for r, p in zip(s["reqs"], s["plans"])]
+    ref = on.paged_attention(q.float().cpu().numpy(), kf, vf, m.cu_seqlens, m.tok_pos, m.prompt_len,
+                             vis_list, m.block_tables, s["block"], s["page"])
+    err = np.linalg.norm(got - ref, axis=-1) / np.maximum(np.linalg.norm(ref, axis=-1), 1e-6)
+    return plan, float(err.max()), got, ref
+
+
+@pytest.mark.parametrize("chunk", [1, 4, 8, 16, 32])
+def test_paged_attention_sdar8b_shape(chunk):
+    s = _step(10 + chunk, 16, max(chunk, 2), 32, 16, 32, 8, 128)
+    if chunk == 1:
+        # pure single-token rows (c = 1 is below dllmsim's minimum, engine.py:56-57)
+        pass
+    plan, err, got, ref = _attn_check(s)
+    assert np.isfinite(got).all()
+    assert err < ATTN_RTOL, err
+
+
+@pytest.mark.parametrize("page,d,hq,hkv", [(64, 128, 32, 8), (16, 64, 4, 4), (16, 64, 4, 2), (32, 128, 32, 4), (128, 128, 8, 8)])
+def test_paged_attention_shapes(page, d, hq, hkv):
+    s = _step(3 + page + hq, 11, 8, 32, page, hq, hkv, d)
+    plan, err, got, ref = _attn_check(s)
+    assert err < ATTN_RTOL, err
+
+
+def test_paged_attention_long_context_split_kv():
+    # LongBench-like prompts: forces split-KV and the combine kernel.
+    s = _step(99, 6, 8, 32, 64, 32, 8, 128, prompt_range=(4096, 9000), out_range=(20, 120))
+    plan, err, got, ref = _attn_check(s, min_split_tiles=4, grid=148)
+    assert plan.n_groups > 0
+    assert err < ATTN_RTOL, err
+
+
+@pytest.mark.parametrize("rule", ["in_block", "out_block"])
+def test_paged_attention_window_rules(rule):
+    s = _step(5, 12, 16, 32, 16, 32, 8, 128, rule=rule)
+    plan, err, got, ref = _attn_check(s)
+    assert err < ATTN_RTOL, err
+
+
+def test_paged_attention_single_cta_many_items():
+    # every work item on one persistent CTA: exercises the cross-item pipeline
+    s = _step(21, 10, 8, 32, 16, 32, 8, 128)
+    plan, err, got, ref = _attn_check(s, grid=1)
+    assert err < ATTN_RTOL, err
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("fallback", ["earliest", "top1"])
+def test_unmask_matches_oracle(dtype, fallback):
+    rng = np.random.default_rng(4)
+    n_req, vocab = 24, 151936
+    wins = rng.integers(0, 33, n_req)
+    cu_rows = np.concatenate([[0], np.cumsum(wins)]).astype(np.int32)
+    n = int(cu_rows[-1])
+    toks = rng.integers(0, vocab, n)
+    confs = rng.choice([0.97, 0.8, 0.5, 0.93, 0.1], n)
+    x = on.peaked_logits(rng, n, vocab, toks, confs)
+    lt = torch.from_numpy(x).to(dtype)
+    xr = lt.float().numpy()
+    dev = torch.device("cuda")
+    res = ops.unmask_commit(lt.to(dev), torch.from_numpy(cu_rows).to(dev), tau=0.9, fallback=fallback)
+    torch.cuda.synchronize()
+    c_ref, t_ref, f_ref = on.unmask(xr, cu_rows, 0.9, fallback)
+    mask = res.commit_mask.cpu().numpy()[:n].astype(bool)
+    tok = res.tokens.cpu().numpy()[:n]
+    conf = res.conf.cpu().numpy()[:n]
+    assert np.array_equal(tok, t_ref)
+    np.testing.assert_allclose(conf, f_ref, rtol=2e-5, atol=1e-6)
+    clear = np.abs(f_ref - 0.9) > 1e-4
+    assert np.array_equal(mask[clear], c_ref[clear])
+
+
+def test_unmask_ties_pick_lowest_index():
+    dev = torch.device("cuda")
+    x = torch.zeros(3, 4096, dtype=torch.float32)
+    x[0, 100] = x[0, 4000] = 5.0
+    x[1, :] = 1.0
+    x[2, 7] = x[2, 3] = 2.0
+    res = ops.unmask_commit(x.to(dev), torch.tensor([0, 3], dtype=torch.int32, device=dev), n_vsplit=3)
+    tok = res.tokens.cpu().tolist()
+    assert tok == [100, 0, 3]
+
+
+def test_unmask_vocab_parallel_merge_equals_single():
+    # two vocab shards merged by the finalize kernel == one pass over the full vocab
+    rng = np.random.default_rng(8)
+    n, vocab = 50, 32768
+    x = torch.from_numpy(rng.standard_normal((n, vocab)).astype(np.float32) * 3).to(torch.bfloat16)
+    dev = torch.device("cuda")
+    xd = x.to(dev)
+    cu = torch.tensor([0, 20, 50], dtype=torch.int32, device=dev)
+    full = ops.unmask_commit(xd, cu, n_vsplit=4)
+    half = vocab // 2
+    p0 = ops.unmask_partials(xd[:, :half].contiguous(), None, n, 2, vocab_offset=0)
+    p1 = ops.unmask_partials(xd[:, half:].contiguous(), None, n, 2, vocab_offset=half)
+    sharded = ops.unmask_finalize(torch.stack([p0, p1]), 2, n, 2, cu, 0.9)
+    assert torch.equal(full.tokens[:n], sharded.tokens[:n])
+    torch.testing.assert_close(full.conf[:n], sharded.conf[:n], rtol=1e-5, atol=0)
