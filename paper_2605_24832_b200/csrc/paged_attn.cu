@@ -19,8 +19,10 @@
 //            the row max/sum need no shuffles; online softmax in the exp2 domain
 //            with a lazy rescale (O in TMEM is only rescaled when the running max
 //            grows by more than 2^8); P goes to shared memory as the A operand of
-//            the PV MMA.  Epilogue normalises O and stores bf16, or writes fp32
-//            split-KV partials for the combine kernel.
+//            the PV MMA, split into two bf16 planes P = hi + lo so the PV product
+//            carries ~16 mantissa bits of P (the tensor pipe has the headroom:
+//            this kernel is HBM-bound).  Epilogue normalises O and stores bf16,
+//            or writes fp32 split-KV partials for the combine kernel.
 // Work items are planned on the host (optimus_attn_plan): long contexts are split
 // into key ranges and items are distributed longest-first over the CTAs.
 #include "attn.cuh"
@@ -38,7 +40,8 @@ struct AttnSmem {
   static constexpr int KB = HD / 64;
   static constexpr uint32_t Q_BYTES = KB * kBlockM * 128;
   static constexpr uint32_t KT_BYTES = KB * kTileN * 128;
-  static constexpr uint32_t P_BYTES = kBlockM * 128;
+  static constexpr uint32_t P_HALF = kBlockM * 128;       // one bf16 [128][64] plane
+  static constexpr uint32_t P_BYTES = 2 * P_HALF;          // hi + lo planes
   static constexpr uint32_t OFF_Q = 0;
   static constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr uint32_t OFF_V = OFF_K + STAGES * KT_BYTES;
@@ -202,10 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tm_o0 + ob * HD;
 #pragma unroll
           for (int ks = 0; ks < kTileN / 16; ++ks) {
-            const uint64_t a = umma_sdesc_sw128(sP_a + (t & 1) * L::P_BYTES + ks * 32, 16, 1024);
+            const uint32_t pa = sP_a + (t & 1) * L::P_BYTES + ks * 32;
             const uint64_t b =
                 umma_sdesc_sw128(sV_a + st * L::KT_BYTES + ks * 16 * 128, kTileN * 128, 1024);
-            umma_bf16_ss(d, a, b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16_ss(d, umma_sdesc_sw128(pa, 16, 1024), b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16_ss(d, umma_sdesc_sw128(pa + L::P_HALF, 16, 1024), b, idesc_o, 1u);
           }
           umma_commit(&pv_done[t & 1]);
           umma_commit(&kv_empty[st]);
@@ -308,13 +312,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
             float e[8];
+            uint32_t hi[4], lo[4];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               e[k] = fast_exp2(x[c8 * 8 + k] - m_use);
               rs += e[k];
             }
-            st_shared_v4(pbase + ((c8 ^ sw) << 4), pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]),
-                         pack_bf16x2(e[4], e[5]), pack_bf16x2(e[6], e[7]));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              hi[k] = pack_bf16x2(e[2 * k], e[2 * k + 1]);
+              lo[k] = pack_bf16x2(e[2 * k] - __uint_as_float(hi[k] << 16),
+                                  e[2 * k + 1] - __uint_as_float(hi[k] & 0xFFFF0000u));
+            }
+            const uint32_t cofs = (c8 ^ sw) << 4;
+            st_shared_v4(pbase + cofs, hi[0], hi[1], hi[2], hi[3]);
+            st_shared_v4(pbase + L::P_HALF + cofs, lo[0], lo[1], lo[2], lo[3]);
           }
           l += rs;
           fence_proxy_async_smem();

@@ -1,0 +1,283 @@
+"""The per-step decode call on B200: plan-all -> one device step -> apply-all.
+
+Reference call chain (``pkg/src/dllmsim/sim.py:269-305``, streaming branch of
+``_Loop.run_decode``): for each request of the batch ``plan_chunk`` ->
+``oracle.commits(req, plan.window)`` -> ``consume`` -> ``apply_chunk``, then one
+latency charge for the whole batch.  Every per-request input is request-local
+(SURVEY §3.2), so reordering into plan-all / device step / apply-all changes no
+output; ``StreamingDecoder.step`` does exactly that with the real forward in the
+middle:
+
+    host:   plans = plan_batch(batch, chunk, B, rule)            (engine.py mirror)
+            meta  = build_step_meta(...) -> ONE pinned H2D copy
+    device: for each layer: forward.qkv -> K1 kv_append -> K2 paged_attn
+                            -> forward.post_attn
+            forward.logits (window rows) -> K3 unmask partials + finalize
+    host:   ONE D2H of commit masks/tokens -> apply_batch       (engine.py mirror)
+
+``B200Oracle`` is the same device step behind the reference's oracle protocol
+(``commits(request, window)`` / ``consume``, engine.py:105-110, sim.py:278-280)
+so it plugs into ``Scenario.oracle_factory`` (sim.py:64) unchanged.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import ops
+from .core import rule_value
+from .engine import ChunkPlan, StepSummary, apply_batch, plan_batch
+from .errors import ConfigError
+from .kvcache import BlockTables, PagedKVCache, PagePool
+from .meta import DeviceMeta, build_step_meta
+
+
+@dataclass(frozen=True)
+class DecodeConfig:
+    """Knobs of the decode path.
+
+    ``block_size`` / ``window_rule`` / chunk size are the reference's knobs
+    (scheduler.py:140-200); ``confidence_threshold``, ``page_size``,
+    ``fallback`` and the model shape are new (SURVEY §5 config keys).
+    """
+
+    num_layers: int = 36
+    num_q_heads: int = 32
+    num_kv_heads: int = 8
+    head_dim: int = 128
+    vocab: int = 151936
+    block_size: int = 32
+    page_size: int = 64
+    window_rule: str = "in_block"
+    confidence_threshold: float = 0.9
+    fallback: str = "earliest"
+    max_batch: int = 64
+    max_pages_per_req: int = 512
+    num_pages: int = 16384
+    min_split_tiles: int = 4
+    logits_dtype: torch.dtype = torch.bfloat16
+
+    def __post_init__(self):
+        if self.num_q_heads % self.num_kv_heads:
+            raise ConfigError("num_q_heads must be a multiple of num_kv_heads")
+        if not 0.0 < self.confidence_threshold <= 1.0:
+            raise ConfigError("confidence_threshold must lie in (0, 1]")
+        rule_value(self.window_rule)
+        if self.fallback not in ops.FALLBACK_MODES:
+            raise ConfigError(f"fallback must be one of {sorted(ops.FALLBACK_MODES)}")
+
+
+class Forward:
+    """What the decode step needs from the model (the reference has none:
+    ``SPEC.md:14`` puts weights out of scope).  Implementations: synthetic
+    SDAR-shaped activations (bench / parity) and a tiny random-init dLLM."""
+
+    def begin_step(self, dmeta: DeviceMeta) -> None:  # pragma: no cover - interface
+        pass
+
+    def qkv(self, layer: int, dmeta: DeviceMeta):  # -> (q [n,Hq,d], k [n,Hkv,d], v [n,Hkv,d])
+        raise NotImplementedError
+
+    def post_attn(self, layer: int, attn_out: torch.Tensor, dmeta: DeviceMeta) -> None:
+        pass
+
+    def logits(self, dmeta: DeviceMeta):  # -> (logits [rows, V], row_src or None)
+        raise NotImplementedError
+
+
+class StreamingDecoder:
+    """Batched streaming chunked block decoding over a paged KV cache."""
+
+    def __init__(self, cfg: DecodeConfig, forward: Forward, device="cuda",
+                 cache: Optional[PagedKVCache] = None):
+        self.cfg = cfg
+        self.forward = forward
+        self.device = torch.device(device)
+        self.cache = cache or PagedKVCache(cfg.num_layers, cfg.num_pages, cfg.num_kv_heads,
+                                           cfg.page_size, cfg.head_dim, device=self.device)
+        self.pool = PagePool(self.cache.num_pages)
+        self.tables = BlockTables(self.pool, cfg.max_batch, cfg.max_pages_per_req, cfg.page_size)
+        self.grid = ops.sm_count()
+        self._pinned = None
+        self._dev_buf = None
+        self._ws_o = None
+        self._ws_ml = None
+        self._attn_out = None
+        self.last_meta: Optional[DeviceMeta] = None
+        self.last_plan: Optional[ops.AttnPlan] = None
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        # multi-GPU: a TensorParallelUnmask merges vocab-shard partials across ranks
+        self.unmask_impl = None
+
+    # ------------------------------------------------------------------ admission
+    def admit(self, request) -> int:
+        """Give a request a batch slot and pages for its prompt + first block."""
+        first = min(request.output_tokens, self.cfg.block_size)
+        return self.tables.admit(request.id, request.prompt_tokens + first)
+
+    def release(self, request) -> None:
+        self.tables.release(request.id)
+
+    def _ensure_pages(self, requests, plans) -> np.ndarray:
+        rows = np.empty(len(requests), dtype=np.int64)
+        for i, (req, plan) in enumerate(zip(requests, plans)):
+            slot = self.tables.slot(req.id)
+            if slot is None:
+                slot = self.admit(req)
+            rows[i] = slot
+            hi = max(plan.window[-1] if plan.window else -1,
+                     max(plan.kv_positions) if plan.kv_positions else -1)
+            if hi >= 0:
+                self.tables.ensure(slot, req.prompt_tokens + hi + 1)
+        return rows
+
+    # ------------------------------------------------------------------ device step
+    def prepare(self, requests: Sequence, plans: Sequence[ChunkPlan]) -> DeviceMeta:
+        rows = self._ensure_pages(requests, plans)
+        bt = self.tables.table[rows]
+        meta = build_step_meta(requests, plans, self.cfg.block_size, bt)
+        dm = DeviceMeta.upload(meta, self.device, self._pinned, self._dev_buf)
+        self._pinned = dm.__dict__["pinned"]
+        self._dev_buf = dm.buf
+        self.h2d_bytes = dm.h2d_bytes
+        plan = ops.plan_attention(meta.cu_seqlens, meta.key_end, self.cfg.num_q_heads,
+                                  self.cfg.num_kv_heads, grid=self.grid,
+                                  min_split_tiles=self.cfg.min_split_tiles, device=self.device)
+        self.h2d_bytes += plan.work_host.nbytes + plan.cta_off_host.nbytes + plan.groups_host.nbytes
+        dm.__dict__["attn_plan"] = plan
+        dm.__dict__["slots"] = rows
+        self.last_meta = dm
+        self.last_plan = plan
+        return dm
+
+    def _workspaces(self, plan: ops.AttnPlan, n_tok: int):
+        cfg = self.cfg
+        if plan.n_partials:
+            need = plan.n_partials * 128 * cfg.head_dim
+            if self._ws_o is None or self._ws_o.numel() < need:
+                self._ws_o = torch.empty(need, dtype=torch.float32, device=self.device)
+                self._ws_ml = torch.empty(plan.n_partials * 256, dtype=torch.float32, device=self.device)
+            elif self._ws_ml.numel() < plan.n_partials * 256:
+                self._ws_ml = torch.empty(plan.n_partials * 256, dtype=torch.float32, device=self.device)
+        shape = (max(n_tok, 1), cfg.num_q_heads, cfg.head_dim)
+        if self._attn_out is None or self._attn_out.shape[0] < shape[0]:
+            self._attn_out = torch.empty(shape, dtype=torch.bfloat16, device=self.device)
+        return self._attn_out[: max(n_tok, 1)]
+
+    def run_layers(self, dm: DeviceMeta) -> None:
+        """K1 + K2 for every layer (the part repeated L times per step)."""
+        cfg = self.cfg
+        m = dm.host
+        plan = dm.__dict__["attn_plan"]
+        out = self._workspaces(plan, m.n_tok)
+        self.forward.begin_step(dm)
+        for layer in range(cfg.num_layers):
+            q, k, v = self.forward.qkv(layer, dm)
+            kc, vc = self.cache.layer(layer)
+            if m.n_tok:
+                ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc)
+                ops.paged_attention(q, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off,
+                                    dm.vis_words, dm.block_tables, plan, cfg.block_size,
+                                    out=out[: m.n_tok], ws_o=self._ws_o, ws_ml=self._ws_ml)
+            self.forward.post_attn(layer, out[: m.n_tok], dm)
+
+    def run_unmask(self, dm: DeviceMeta) -> ops.UnmaskResult:
+        m = dm.host
+        logits, row_src = self.forward.logits(dm)
+        if self.unmask_impl is not None:
+            return self.unmask_impl(self, dm, logits, row_src)
+        n_vsplit = ops.unmask_splits(m.n_rows, logits.shape[-1])
+        part = ops.unmask_partials(logits, row_src, m.n_rows, n_vsplit)
+        return ops.unmask_finalize(part, 1, m.n_rows, n_vsplit, dm.cu_rows,
+                                   self.cfg.confidence_threshold, self.cfg.fallback)
+
+    def device_step(self, dm: DeviceMeta) -> ops.UnmaskResult:
+        self.run_layers(dm)
+        return self.run_unmask(dm)
+
+    def fetch_commits(self, dm: DeviceMeta, res: ops.UnmaskResult) -> list:
+        """One D2H copy of the commit mask -> per-request commit sets."""
+        m = dm.host
+        if m.n_rows == 0:
+            return [set() for _ in range(m.n_req)]
+        mask = res.commit_mask[: m.n_rows].cpu().numpy().astype(bool)
+        self.d2h_bytes = m.n_rows
+        rows = np.flatnonzero(mask)
+        req_of = m.row_req[rows]
+        pos = m.row_pos[rows]
+        out = [set() for _ in range(m.n_req)]
+        for r, p in zip(req_of.tolist(), pos.tolist()):
+            out[r].add(p)
+        return out
+
+    # ------------------------------------------------------------------ the call
+    def step(self, requests: Sequence, chunk_size: int) -> list:
+        """One streaming decode iteration for the whole batch (sim.py:269-305)."""
+        cfg = self.cfg
+        plans = plan_batch(requests, chunk_size, cfg.block_size, cfg.window_rule)
+        dm = self.prepare(requests, plans)
+        res = self.device_step(dm)
+        commits = self.fetch_commits(dm, res)
+        summaries = apply_batch(requests, plans, commits, cfg.block_size)
+        for req in requests:
+            if req.finished:
+                self.release(req)
+        return summaries
+
+
+class B200Oracle:
+    """The reference's commit-oracle protocol served by the B200 decode step.
+
+    ``commits(request, window)`` (commit.py:279-280 signature) runs the device
+    step for the batch that ``prime(requests, plans)`` / ``commits_batch``
+    announced, or — used standalone inside ``dllmsim``'s ``_Loop`` — for the
+    single request it is asked about.  ``consume`` is a no-op kept for protocol
+    parity (commit.py:310-312).
+    """
+
+    def __init__(self, decoder: StreamingDecoder):
+        self.decoder = decoder
+        self._cache: dict = {}
+
+    def commits_batch(self, requests: Sequence, plans: Sequence[ChunkPlan]) -> list:
+        idx = [i for i, p in enumerate(plans) if p.kv_positions or p.window]
+        sub_r = [requests[i] for i in idx]
+        sub_p = [plans[i] for i in idx]
+        result = [set() for _ in requests]
+        if sub_r:
+            dm = self.decoder.prepare(sub_r, sub_p)
+            res = self.decoder.device_step(dm)
+            for i, c in zip(idx, self.decoder.fetch_commits(dm, res)):
+                result[i] = c
+        for req, plan, c in zip(requests, plans, result):
+            self._cache[(req.id, tuple(plan.window))] = c
+        return result
+
+    def commits(self, request, window) -> set:
+        key = (request.id, tuple(window))
+        if key in self._cache:
+            return self._cache.pop(key)
+        # Standalone use inside dllmsim's loop: a non-empty window means plan_chunk
+        # had capacity left after the backlog (engine.py:58-59), so the plan's kv
+        # positions are the whole uncached queue.
+        plan = ChunkPlan(kv_positions=tuple(request.uncached_queue), window=tuple(window))
+        [c] = self.commits_batch([request], [plan])
+        self._cache.pop(key, None)
+        return c
+
+    def consume(self, request, committed) -> None:
+        return None
+
+
+def run_decode_batched(decoder: StreamingDecoder, batch: Sequence, chunk_size: int) -> tuple:
+    """Batched twin of ``_Loop.run_decode``'s streaming branch: returns
+    (computed_tokens, committed_tokens, summaries) for the iteration record."""
+    summaries = decoder.step(batch, chunk_size)
+    computed = sum(s.computed for s in summaries)
+    committed = sum(len(s.commits) for s in summaries)
+    return computed, committed, summaries
