@@ -337,6 +337,9 @@ def main():
     plan = dm.__dict__["attn_plan"]
     out = dec._workspaces(plan, m.n_tok)
     s = torch.cuda.current_stream()
+    # keep the GPU busy while the whole sequence is enqueued, so host launch
+    # latency never shows up between a kernel's start/end events
+    torch.cuda._sleep(int(2e9 * 0.02))
     for rep in range(3):
         for layer in range(cfg.num_layers):
             q, k, v = fwd.qkv(layer, dm)
@@ -361,6 +364,7 @@ def main():
     k3_us = float(np.mean([e[0].elapsed_time(e[1]) for e in kt["k3"]])) * 1e3
 
     # ---- end to end through the public per-step call (closed loop, live state)
+    dec.release_all(reqs)
     e2e = run_e2e(args, dec, fwd, e2e_pool, world, dev)
 
     hbm, peak_kind = peaks()

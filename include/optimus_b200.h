@@ -50,6 +50,10 @@ int optimus_version(void);
 /* Human-readable description of the last error raised on this thread. */
 const char* optimus_last_error(void);
 
+/* Diagnostics: record a per-CTA globaltimer timeline of K2 into `buf`
+ * (device, uint64[grid][512]); NULL disables (the default). */
+void optimus_set_attn_trace(unsigned long long* buf);
+
 /* Number of SMs of the current device (0 if no device). */
 int optimus_device_sm_count(void);
 

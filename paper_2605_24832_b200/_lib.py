@@ -24,6 +24,7 @@ SIGNATURES = {
     "optimus_version": (_i32, []),
     "optimus_last_error": (C.c_char_p, []),
     "optimus_device_sm_count": (_i32, []),
+    "optimus_set_attn_trace": (None, [_vp]),
     "optimus_kv_append": (
         _i32,
         [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp],

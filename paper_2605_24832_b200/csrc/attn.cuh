@@ -26,6 +26,7 @@ struct AttnParams {
   int page_size;
   int box_rows;    // min(page_size, 64)
   float scale_log2;
+  unsigned long long* trace;  // optional per-CTA timeline (diagnostics), nullptr in production
 };
 
 int launch_paged_attn(int head_dim, const CUtensorMap& tq, const CUtensorMap& tk,

@@ -34,6 +34,7 @@ using namespace optimus;
 namespace {
 
 thread_local std::string g_last_error;
+unsigned long long* g_trace = nullptr;  // optimus_set_attn_trace (diagnostics)
 
 int fail(const char* what) {
   g_last_error = what;
@@ -147,6 +148,8 @@ bool page_ok(int P) {
 extern "C" {
 
 int optimus_version(void) { return 100; }
+
+void optimus_set_attn_trace(unsigned long long* buf) { g_trace = buf; }
 
 const char* optimus_last_error(void) { return g_last_error.c_str(); }
 
@@ -424,6 +427,7 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
   prm.page_size = page_size;
   prm.box_rows = box_rows;
   prm.scale_log2 = sm_scale * 1.4426950408889634f;
+  prm.trace = g_trace;
   return cuda_status(launch_paged_attn(head_dim, tq, tk, tv, prm, grid, groups, n_groups,
                                        static_cast<cudaStream_t>(stream)),
                      "paged_attn");

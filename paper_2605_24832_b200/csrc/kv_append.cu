@@ -10,42 +10,39 @@
 // window rows produce provisional KV that the visibility rule of K2 hides
 // until the position is recomputed with its committed token.
 //
-// Pure streaming: one warp per token; each lane moves 16-byte vectors, so a
-// token's Hkv*head_dim*2 bytes of K (and of V) are read and written once.
+// Pure streaming: each K/V byte is read once and written once.
 #include "ptx.cuh"
 
 namespace optimus {
 
+// One thread per 16-byte vector of a (token, head) row: n_tok*Hkv*head_dim/8
+// independent load/store pairs for K and for V, so the scatter runs at full
+// memory-level parallelism instead of one serial loop per token.
 __global__ void __launch_bounds__(256) kv_append_kernel(
     const uint4* __restrict__ k_new, const uint4* __restrict__ v_new, int64_t new_stride_vec,
     const int32_t* __restrict__ tok_req, const int32_t* __restrict__ tok_pos,
     const int32_t* __restrict__ prompt_len, const int32_t* __restrict__ block_tables,
     int max_pages, int n_tok, int hkv, int vec_per_head, int page_size, uint4* __restrict__ k_cache,
     uint4* __restrict__ v_cache, int64_t* __restrict__ slot_out) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= n_tok) return;
-  const int r = tok_req[warp];
-  const int s = prompt_len[r] + tok_pos[warp];
-  const int page = block_tables[static_cast<int64_t>(r) * max_pages + s / page_size];
+  const int per_tok = hkv * vec_per_head;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= static_cast<int64_t>(n_tok) * per_tok) return;
+  const int t = static_cast<int>(gid / per_tok);
+  const int i = static_cast<int>(gid - static_cast<int64_t>(t) * per_tok);
+  const int h = i / vec_per_head;
+  const int c = i - h * vec_per_head;
+  const int r = __ldg(tok_req + t);
+  const int s = __ldg(prompt_len + r) + __ldg(tok_pos + t);
+  const int page = __ldg(block_tables + static_cast<int64_t>(r) * max_pages + s / page_size);
   const int off = s % page_size;
-  if (lane == 0 && slot_out != nullptr)
-    slot_out[warp] = static_cast<int64_t>(page) * page_size + off;
-  const int total = hkv * vec_per_head;
-  const uint4* ksrc = k_new + static_cast<int64_t>(warp) * new_stride_vec;
-  const uint4* vsrc = v_new + static_cast<int64_t>(warp) * new_stride_vec;
-  // (page, head, off) row base in 16-byte vectors.
-  const int64_t page_base = static_cast<int64_t>(page) * hkv * page_size;
-#pragma unroll 4
-  for (int i = lane; i < total; i += 32) {
-    const int h = i / vec_per_head;
-    const int c = i - h * vec_per_head;
-    const int64_t dst = ((page_base + static_cast<int64_t>(h) * page_size + off) * vec_per_head) + c;
-    const uint4 kv = __ldg(ksrc + i);
-    const uint4 vv = __ldg(vsrc + i);
-    k_cache[dst] = kv;
-    v_cache[dst] = vv;
-  }
+  const int64_t src = static_cast<int64_t>(t) * new_stride_vec + i;
+  const uint4 kv = __ldg(k_new + src);
+  const uint4 vv = __ldg(v_new + src);
+  const int64_t dst =
+      ((static_cast<int64_t>(page) * hkv + h) * page_size + off) * vec_per_head + c;
+  k_cache[dst] = kv;
+  v_cache[dst] = vv;
+  if (i == 0 && slot_out != nullptr) slot_out[t] = static_cast<int64_t>(page) * page_size + off;
 }
 
 int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_tok,
@@ -55,8 +52,9 @@ int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_to
                      cudaStream_t stream) {
   if (n_tok == 0) return 0;
   const int vec_per_head = head_dim / 8;  // 8 bf16 per 16-byte vector
+  const int64_t total = static_cast<int64_t>(n_tok) * hkv * vec_per_head;
   const int threads = 256;
-  const int blocks = (n_tok * 32 + threads - 1) / threads;
+  const int blocks = static_cast<int>((total + threads - 1) / threads);
   kv_append_kernel<<<blocks, threads, 0, stream>>>(
       static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
       tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok, hkv, vec_per_head, page_size,

@@ -32,6 +32,17 @@ namespace optimus {
 constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
 constexpr int kThreads = 256;  // 8 warps
+constexpr int kTraceSlots = 512;  // per CTA: [role*128 + i]
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace(const AttnParams& p, int role, int i) {
+  if (p.trace != nullptr && i < 128)
+    p.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + role * 128 + i] = gtimer();
+}
 
 
 
@@ -81,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace(p, 3, 127);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_q);
@@ -116,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace(p, 3, 126);
   const uint32_t tm_s0 = tmem_base;           // S buffers: columns [0,64) and [64,128)
   const uint32_t tm_o0 = tmem_base + 128;     // O buffers: [128,128+HD) and [128+HD,128+2HD)
 
@@ -144,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kt = key_begin; kt < key_end; kt += kTileN, ++tile_ctr) {
           const int st = tile_ctr % STAGES;
           mbar_wait(&kv_empty[st], ((tile_ctr / STAGES) & 1) ^ 1);
+          trace(p, 0, tile_ctr);
           int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
           if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
           mbar_arrive_expect_tx(&kv_full[st], n_chunks * chunk_tx);
@@ -180,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int st = t % STAGES;
           mbar_wait(&kv_full[st], (t / STAGES) & 1);
           tc_fence_after();
+          trace(p, 1, t);
           const uint32_t d = tm_s0 + (t & 1) * kTileN;
 #pragma unroll
           for (int ks = 0; ks < HD / 16; ++ks) {
@@ -256,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sb = t & 1;
         mbar_wait(&s_full[sb], (t >> 1) & 1);
         tc_fence_after();
+        if (threadIdx.x == 128) trace(p, 2, t);
         if (warp_valid) {
           uint32_t sr[2][32];
           tmem_ld32(tm_s0 + lane_off + sb * kTileN, sr[0]);
@@ -333,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
+        if (threadIdx.x == 128) trace(p, 3, t);
       }
       tile_ctr += n_tiles;
       // ---------------------------------------------------------- epilogue
@@ -379,49 +396,70 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&o_empty[ob]);
     }
   }
+  if (threadIdx.x == 0) trace(p, 2, 127);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  if (threadIdx.x == 64) trace(p, 2, 126);
 }
 
 // Split-KV combine: merge the (m, l, O) partials of every split query tile.
+// One warp per output row (grid.x = group, grid.y = 8-row slab): lane s reads the
+// (m, l) of split s, the warp reduces the merged max / denominator with shuffles,
+// then every lane accumulates a 4-column float4 slice over the splits.
 template <int HD>
-__global__ void __launch_bounds__(128) attn_combine_kernel(const int32_t* __restrict__ groups,
+__global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __restrict__ groups,
                                                            const float* __restrict__ ws_o,
                                                            const float* __restrict__ ws_ml,
                                                            __nv_bfloat16* __restrict__ out,
                                                            int64_t out_stride_tok, int group_sz) {
   const int* gr = groups + 8 * blockIdx.x;
   const int head = gr[1], tok_begin = gr[2], n_tok = gr[3], slot0 = gr[4], n_split = gr[5];
-  const int rows = n_tok * group_sz;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int PER = HD / 32;
-  for (int r = warp; r < rows; r += 4) {
-    float mx = -INFINITY;
-    for (int s = 0; s < n_split; ++s) {
-      const float2 ml = reinterpret_cast<const float2*>(ws_ml)[static_cast<int64_t>(slot0 + s) * kBlockM + r];
-      if (ml.y > 0.f) mx = fmaxf(mx, ml.x);
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n_tok * group_sz) return;
+  const float2* ml = reinterpret_cast<const float2*>(ws_ml);
+  float mx = -INFINITY;
+  for (int s = lane; s < n_split; s += 32) {
+    const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
+    if (v.y > 0.f) mx = fmaxf(mx, v.x);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  float den = 0.f;
+  for (int s = lane; s < n_split; s += 32) {
+    const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
+    if (v.y > 0.f) den += exp2f(v.x - mx) * v.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xFFFFFFFFu, den, o);
+  constexpr int PER = HD / 32;  // columns per lane (4 for HD=128, 2 for HD=64)
+  float acc[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+  for (int s = 0; s < n_split; ++s) {
+    const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
+    if (!(v.y > 0.f)) continue;
+    const float wgt = exp2f(v.x - mx);
+    const float* src = ws_o + (static_cast<int64_t>(slot0 + s) * kBlockM + r) * HD + lane * PER;
+    if constexpr (PER == 4) {
+      const float4 o = *reinterpret_cast<const float4*>(src);
+      acc[0] += wgt * o.x; acc[1] += wgt * o.y; acc[2] += wgt * o.z; acc[3] += wgt * o.w;
+    } else {
+      const float2 o = *reinterpret_cast<const float2*>(src);
+      acc[0] += wgt * o.x; acc[1] += wgt * o.y;
     }
-    float acc[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) acc[i] = 0.f;
-    float den = 0.f;
-    for (int s = 0; s < n_split; ++s) {
-      const float2 ml = reinterpret_cast<const float2*>(ws_ml)[static_cast<int64_t>(slot0 + s) * kBlockM + r];
-      if (!(ml.y > 0.f)) continue;
-      const float wgt = exp2f(ml.x - mx);
-      den += wgt * ml.y;
-      const float* src = ws_o + (static_cast<int64_t>(slot0 + s) * kBlockM + r) * HD + lane * PER;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) acc[i] += wgt * src[i];
-    }
-    const float inv = den > 0.f ? 1.f / den : 0.f;
-    const int t = r / group_sz, g = r - t * group_sz;
-    __nv_bfloat16* dst = out + static_cast<int64_t>(tok_begin + t) * out_stride_tok +
-                         static_cast<int64_t>(head * group_sz + g) * HD + lane * PER;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) dst[i] = __float2bfloat16_rn(acc[i] * inv);
+  }
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  const int t = r / group_sz, g = r - t * group_sz;
+  __nv_bfloat16* dst = out + static_cast<int64_t>(tok_begin + t) * out_stride_tok +
+                       static_cast<int64_t>(head * group_sz + g) * HD + lane * PER;
+  if constexpr (PER == 4) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(acc[0] * inv, acc[1] * inv),
+                                                pack_bf16x2(acc[2] * inv, acc[3] * inv));
+  } else {
+    *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(acc[0] * inv, acc[1] * inv);
   }
 }
 
@@ -443,8 +481,8 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (n_groups > 0) {
-    attn_combine_kernel<HD><<<n_groups, 128, 0, stream>>>(groups, prm.ws_o, prm.ws_ml, prm.out,
-                                                          prm.out_stride_tok, prm.group);
+    attn_combine_kernel<HD><<<dim3(n_groups, kBlockM / 8), 256, 0, stream>>>(
+        groups, prm.ws_o, prm.ws_ml, prm.out, prm.out_stride_tok, prm.group);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return static_cast<int>(e);
   }

@@ -123,6 +123,11 @@ class StreamingDecoder:
     def release(self, request) -> None:
         self.tables.release(request.id)
 
+    def release_all(self, requests) -> None:
+        for r in requests:
+            if self.tables.slot(r.id) is not None:
+                self.tables.release(r.id)
+
     def _ensure_pages(self, requests, plans) -> np.ndarray:
         rows = np.empty(len(requests), dtype=np.int64)
         for i, (req, plan) in enumerate(zip(requests, plans)):

@@ -1,0 +1,106 @@
+"""Kernel micro-benchmarks on the bench workload (diagnostics, not the contract)."""
+import argparse, sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+import bench
+from paper_2605_24832_b200 import ops
+from paper_2605_24832_b200.decode import DecodeConfig, StreamingDecoder
+from paper_2605_24832_b200.engine import plan_batch
+from paper_2605_24832_b200.synthetic import SyntheticForward
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="sharegpt")
+ap.add_argument("--chunk", type=int, default=32)
+ap.add_argument("--page", type=int, default=64)
+ap.add_argument("--batch", type=int, default=64)
+ap.add_argument("--layers", type=int, default=36)
+ap.add_argument("--seed", type=int, default=0)
+a = ap.parse_args()
+a.steps = 1
+dev = torch.device("cuda")
+reqs = bench.workload_requests(a)
+P = a.page
+cfg = DecodeConfig(num_layers=a.layers, page_size=P, max_batch=a.batch,
+                   num_pages=bench.pages_needed(reqs, P) + 64,
+                   max_pages_per_req=max((r.prompt_tokens + r.output_tokens + P - 1) // P for r in reqs) + 1)
+fwd = SyntheticForward(cfg, a.batch * a.chunk, a.batch, device=dev)
+dec = StreamingDecoder(cfg, fwd, device=dev)
+for l in range(cfg.num_layers):
+    dec.cache.k[l].normal_(); dec.cache.v[l].normal_()
+plans = plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule)
+dm = dec.prepare(reqs, plans)
+dec.device_step(dm)
+torch.cuda.synchronize()
+m = dm.host
+plan = dm.__dict__["attn_plan"]
+out = dec._workspaces(plan, m.n_tok)
+k2b, k1b, k3b, vis, flops = bench.algorithmic_bytes(dm, cfg)
+print(f"n_tok={m.n_tok} rows={m.n_rows} vis_keys={vis} k2_bytes={k2b/1e6:.1f}MB work={plan.n_work} groups={plan.n_groups}")
+
+def k1(l):
+    q, k, v = fwd.qkv(l, dm); kc, vc = dec.cache.layer(l)
+    ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc)
+def k2(l):
+    q, k, v = fwd.qkv(l, dm); kc, vc = dec.cache.layer(l)
+    ops.paged_attention(q, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off, dm.vis_words,
+                        dm.block_tables, plan, cfg.block_size, out=out[: m.n_tok], ws_o=dec._ws_o, ws_ml=dec._ws_ml)
+def k3():
+    dec.run_unmask(dm)
+
+def timed(fn, reps=10, label=""):
+    s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn(); s.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.synchronize()
+    for _ in range(3): g.replay()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps): g.replay()
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print(f"{label:40s} {ms*1e3:9.1f} us")
+    return ms
+
+L = cfg.num_layers
+t_k2_same = timed(lambda: [k2(0) for _ in range(L)], label="K2 x L same layer")
+t_k2 = timed(lambda: [k2(l) for l in range(L)], label="K2 x L layers")
+t_k1 = timed(lambda: [k1(l) for l in range(L)], label="K1 x L layers")
+t_both = timed(lambda: [(k1(l), k2(l)) for l in range(L)], label="K1+K2 x L layers")
+t_k3 = timed(k3, label="K3")
+t_step = timed(lambda: dec.device_step(dm), label="full step")
+print(f"K2 per launch (layers): {t_k2/L*1e3:.1f} us -> {k2b/(t_k2/L*1e-3)/1e9:.0f} GB/s; same-layer {t_k2_same/L*1e3:.1f} us")
+print(f"K1 per launch: {t_k1/L*1e3:.2f} us -> {k1b/(t_k1/L*1e-3)/1e9:.0f} GB/s ; K3 {t_k3*1e3:.1f} us -> {k3b/(t_k3*1e-3)/1e9:.0f} GB/s")
+
+# ---- timeline trace of one K2 launch
+from paper_2605_24832_b200 import _lib
+tr = torch.zeros((plan.grid, 512), dtype=torch.int64, device=dev)
+_lib.call("optimus_set_attn_trace", tr.data_ptr())
+k2(0)
+torch.cuda.synchronize()
+_lib.call("optimus_set_attn_trace", None)
+t = tr.cpu().numpy().astype(np.float64)
+t0 = t[t > 0].min()
+np.set_printoptions(linewidth=200, precision=0, suppress=True)
+for c in (0, 1, 70, 147):
+    n = int((t[c, 128:256] > 0).sum())
+    print(f"CTA {c}: tiles={n}")
+    for role, name in enumerate(["prod_issue", "mma_S", "smx_Sready", "smx_Pdone"]):
+        v = t[c, role * 128: role * 128 + min(n, 40)]
+        print(f"  {name:11s}", ((v - t0) / 1e3).round(2))
+entry = t[:, 3 * 128 + 127]; setup = t[:, 3 * 128 + 126]; fin = t[:, 2 * 128 + 127]; out_ = t[:, 2 * 128 + 126]
+print("entry (us) pctl", np.percentile((entry - t0) / 1e3, [0, 50, 100]).round(2))
+print("setup done    ", np.percentile((setup - t0) / 1e3, [0, 50, 100]).round(2))
+print("work finished ", np.percentile((fin - t0) / 1e3, [0, 50, 100]).round(2))
+print("dealloc done  ", np.percentile((out_ - t0) / 1e3, [0, 50, 100]).round(2))
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+torch.cuda._sleep(int(1e8))
+e0.record(); k2(0); e1.record(); torch.cuda.synchronize()
+print("single launch event time (us):", e0.elapsed_time(e1) * 1e3)
+ends = np.where(t > 0, t, 0).max(axis=1)
+print("CTA end times (us) pctl:", np.percentile((ends - t0) / 1e3, [0, 50, 90, 100]).round(1))
