@@ -90,17 +90,18 @@ int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_t
  *                               (query tiles that were split and need the combine)
  * Returns the number of work items (>= 0) or OPTIMUS_EINVAL; *n_groups and
  * *n_partials receive the combine-group count and the partial-slot count.
- * `min_split_tiles` bounds how finely a long context is split (64-key tiles).
+ * `min_split_tiles` bounds how finely a long context is split (64-key tiles);
+ * an item never spans more than 255 pages of `page_size` keys.
  */
 int optimus_attn_plan(int n_req, const int32_t* cu_seqlens_q_host, const int32_t* key_end_host,
                       int num_q_heads, int num_kv_heads, int grid, int min_split_tiles,
-                      int32_t* work_host, int max_work, int32_t* cta_off_host,
+                      int page_size, int32_t* work_host, int max_work, int32_t* cta_off_host,
                       int32_t* groups_host, int max_groups, int* n_groups, int* n_partials);
 
 /* Upper bounds for the planner's output buffers. */
 int optimus_attn_plan_bounds(int n_req, const int32_t* cu_seqlens_q_host,
                              const int32_t* key_end_host, int num_q_heads, int num_kv_heads,
-                             int min_split_tiles, int* max_work, int* max_groups);
+                             int min_split_tiles, int page_size, int* max_work, int* max_groups);
 
 /*
  * K2 — variable-length paged attention with the diffusion visibility rule

@@ -29,10 +29,10 @@ SIGNATURES = {
         _i32,
         [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp],
     ),
-    "optimus_attn_plan_bounds": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "optimus_attn_plan_bounds": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "optimus_attn_plan": (
         _i32,
-        [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp],
+        [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp],
     ),
     "optimus_paged_attn": (
         _i32,

@@ -24,9 +24,11 @@ struct AttnParams {
   int group;       // G = Hq / Hkv
   int tok_per_tile;  // 128 / G
   int page_size;
+  int page_shift;  // log2(page_size)
   int box_rows;    // min(page_size, 64)
   float scale_log2;
-  unsigned long long* trace;  // optional per-CTA timeline (diagnostics), nullptr in production
+  unsigned long long* trace;
+  int dbg;  // diagnostics: bit0 skip lo-plane PV, bit1 skip S MMA, bit2 skip softmax math, bit3 skip PV  // optional per-CTA timeline (diagnostics), nullptr in production
 };
 
 int launch_paged_attn(int head_dim, const CUtensorMap& tq, const CUtensorMap& tk,

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <queue>
@@ -138,10 +139,9 @@ int get_map(const void* ptr, const uint64_t dims[4], const uint64_t strides[3],
   return 0;
 }
 
-bool page_ok(int P) {
-  if (P < 8 || P % 8) return false;
-  return P <= 64 ? (64 % P == 0) : (P % 64 == 0);
-}
+// Page sizes: powers of two from 8 to 1024 keys (a 64-key tile covers whole pages,
+// or whole tiles fit in one page).
+bool page_ok(int P) { return P >= 8 && P <= 1024 && (P & (P - 1)) == 0; }
 
 }  // namespace
 
@@ -187,8 +187,18 @@ int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_t
       "kv_append");
 }
 
+namespace {
+// An item's key range must span at most 255 pages (the kernel stages an item's page
+// ids in shared memory, kMaxUnitPages = 256).
+int item_tile_cap(int page_size) {
+  const long long cap = (255LL * std::max(page_size, 1)) / 64;
+  return static_cast<int>(std::max(1LL, std::min(cap, 1LL << 20)));
+}
+}  // namespace
+
 int optimus_attn_plan_bounds(int n_req, const int32_t* cu, const int32_t* key_end, int hq,
-                             int hkv, int min_split_tiles, int* max_work, int* max_groups) {
+                             int hkv, int min_split_tiles, int page_size, int* max_work,
+                             int* max_groups) {
   if (n_req < 0 || hkv < 1 || hq % hkv) return fail("attn_plan_bounds: bad heads");
   const int G = hq / hkv;
   if (G > 128) return fail("attn_plan_bounds: group size > 128");
@@ -200,7 +210,8 @@ int optimus_attn_plan_bounds(int n_req, const int32_t* cu, const int32_t* key_en
     if (nq <= 0) continue;
     const int mt = (nq + T - 1) / T;
     const int nt = (key_end[r] + 63) / 64;
-    const int maxs = std::max(1, nt / min_split_tiles);
+    const int cap = item_tile_cap(page_size);
+    const int maxs = std::max(std::max(1, nt / min_split_tiles), (nt + cap - 1) / cap);
     w += static_cast<long long>(hkv) * mt * maxs;
     g += static_cast<long long>(hkv) * mt;
   }
@@ -210,7 +221,7 @@ int optimus_attn_plan_bounds(int n_req, const int32_t* cu, const int32_t* key_en
 }
 
 int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int hq, int hkv,
-                      int grid, int min_split_tiles, int32_t* work, int max_work,
+                      int grid, int min_split_tiles, int page_size, int32_t* work, int max_work,
                       int32_t* cta_off, int32_t* groups, int max_groups, int* n_groups_out,
                       int* n_partials_out) {
   if (n_req < 0 || hkv < 1 || hq % hkv || grid < 1) return fail("attn_plan: bad arguments");
@@ -239,10 +250,11 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
   // Cost model (in 64-key tile units): every item pays a fixed prologue/epilogue
   // (Q load, O drain) and a split item also pays its partial write + combine read.
   const double kItem = 2.0, kSplit = 3.0;
+  const int hard_cap = item_tile_cap(page_size);
   auto split_count = [&](int tiles, int cap) {
-    if (tiles <= cap) return 1;
-    int s = (tiles + cap - 1) / cap;
-    return std::min(s, std::max(1, tiles / min_split_tiles));
+    int s = 1;
+    if (tiles > cap) s = std::min((tiles + cap - 1) / cap, std::max(1, tiles / min_split_tiles));
+    return std::max(s, (tiles + hard_cap - 1) / hard_cap);
   };
   int best_cap = std::max(max_tiles, 1);
   double best_span = 1e300;
@@ -370,7 +382,7 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
   const int G = hq / hkv;
   if (G > 128) return fail("paged_attn: group size > 128");
   if (!page_ok(page_size))
-    return fail("paged_attn: page_size must be a multiple of 8 that divides 64 or is a multiple of 64");
+    return fail("paged_attn: page_size must be a power of two in [8, 1024]");
   if (block_size < 1) return fail("paged_attn: block_size must be >= 1");
   if (q_stride_tok % 8 || q_stride_tok < static_cast<int64_t>(hq) * head_dim)
     return fail("paged_attn: q_stride_tok must be >= Hq*head_dim and a multiple of 8");
@@ -425,9 +437,14 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
   prm.group = G;
   prm.tok_per_tile = T;
   prm.page_size = page_size;
+  prm.page_shift = __builtin_ctz(static_cast<unsigned>(page_size));
   prm.box_rows = box_rows;
   prm.scale_log2 = sm_scale * 1.4426950408889634f;
   prm.trace = g_trace;
+  {
+    const char* e = getenv("OPTIMUS_DBG");
+    prm.dbg = e ? atoi(e) : 0;
+  }
   return cuda_status(launch_paged_attn(head_dim, tq, tk, tv, prm, grid, groups, n_groups,
                                        static_cast<cudaStream_t>(stream)),
                      "paged_attn");

@@ -152,7 +152,8 @@ class StreamingDecoder:
         self.h2d_bytes = dm.h2d_bytes
         plan = ops.plan_attention(meta.cu_seqlens, meta.key_end, self.cfg.num_q_heads,
                                   self.cfg.num_kv_heads, grid=self.grid,
-                                  min_split_tiles=self.cfg.min_split_tiles, device=self.device)
+                                  min_split_tiles=self.cfg.min_split_tiles, device=self.device,
+                                  page_size=self.cfg.page_size)
         self.h2d_bytes += plan.work_host.nbytes + plan.cta_off_host.nbytes + plan.groups_host.nbytes
         dm.__dict__["attn_plan"] = plan
         dm.__dict__["slots"] = rows

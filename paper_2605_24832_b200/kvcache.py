@@ -108,8 +108,8 @@ class PagedKVCache:
 
     def __init__(self, num_layers: int, num_pages: int, num_kv_heads: int, page_size: int,
                  head_dim: int, device="cuda", dtype=torch.bfloat16):
-        if page_size % 8 or not (64 % page_size == 0 or page_size % 64 == 0):
-            raise ConfigError("page_size must be a multiple of 8 dividing 64 (or a multiple of 64)")
+        if page_size < 8 or page_size > 1024 or page_size & (page_size - 1):
+            raise ConfigError("page_size must be a power of two in [8, 1024]")
         if head_dim not in (64, 128):
             raise ConfigError("head_dim must be 64 or 128")
         shape = (num_layers, num_pages, num_kv_heads, page_size, head_dim)

@@ -98,6 +98,7 @@ def plan_attention(
     grid: Optional[int] = None,
     min_split_tiles: int = 4,
     device: Optional[torch.device] = None,
+    page_size: int = 16,
 ) -> AttnPlan:
     """Split (request, kv head, query tile) units into key ranges and place them
     on persistent CTAs (``optimus_attn_plan``)."""
@@ -110,7 +111,7 @@ def plan_attention(
     _lib.check(
         _lib.call(
             "optimus_attn_plan_bounds", n_req, cu.ctypes.data, ke.ctypes.data,
-            num_q_heads, num_kv_heads, min_split_tiles, C.byref(mw), C.byref(mg),
+            num_q_heads, num_kv_heads, min_split_tiles, page_size, C.byref(mw), C.byref(mg),
         ),
         "optimus_attn_plan_bounds",
     )
@@ -120,7 +121,7 @@ def plan_attention(
     ng, npart = C.c_int(0), C.c_int(0)
     n = _lib.call(
         "optimus_attn_plan", n_req, cu.ctypes.data, ke.ctypes.data, num_q_heads, num_kv_heads,
-        grid, min_split_tiles, work.ctypes.data, work.shape[0], cta_off.ctypes.data,
+        grid, min_split_tiles, page_size, work.ctypes.data, work.shape[0], cta_off.ctypes.data,
         groups.ctypes.data, groups.shape[0], C.byref(ng), C.byref(npart),
     )
     if n < 0:

@@ -81,7 +81,7 @@ def _attn_check(s, min_split_tiles=4, grid=None):
     kc, vc, _ = _run_append(s)
     m = s["meta"]
     plan = ops.plan_attention(m.cu_seqlens, m.key_end, s["hq"], s["hkv"], grid=grid,
-                              min_split_tiles=min_split_tiles, device=dev)
+                              min_split_tiles=min_split_tiles, device=dev, page_size=s["page"])
     q = s["q"].to(dev)[: m.n_tok]
     out = ops.paged_attention(q, kc, vc, s["dm"].tok_pos, s["dm"].prompt_len, s["dm"].vis_base,
                               s["dm"].vis_off, s["dm"].vis_words, s["dm"].block_tables, plan,

@@ -56,9 +56,10 @@ def test_bitmaps_match_oracle_rule_v(rule, chunk):
         assert list(meta.tok_pos[meta.row_tok[a:b]]) == list(plan.window)
 
 
-def _plan(cu, ke, hq, hkv, grid, min_split=4):
+def _plan(cu, ke, hq, hkv, grid, min_split=4, page_size=64):
     from paper_2605_24832_b200.ops import plan_attention
-    return plan_attention(np.asarray(cu), np.asarray(ke), hq, hkv, grid=grid, min_split_tiles=min_split)
+    return plan_attention(np.asarray(cu), np.asarray(ke), hq, hkv, grid=grid, min_split_tiles=min_split,
+                          page_size=page_size)
 
 
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (4, 4), (4, 2), (32, 4)])
@@ -69,7 +70,7 @@ def test_planner_covers_every_key_tile_once(hq, hkv):
     cu = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
     ke = rng.integers(1, 9000, n).astype(np.int32)
     for grid in (1, 7, 148):
-        plan = _plan(cu, ke, hq, hkv, grid)
+        plan = _plan(cu, ke, hq, hkv, grid, page_size=64)
         G = hq // hkv
         T = 128 // G
         w = plan.work_host
@@ -94,6 +95,8 @@ def test_planner_covers_every_key_tile_once(hq, hkv):
                     else:
                         assert all(x[2] >= 0 for x in ranges)
         assert not cover
+        # an item never spans more than 255 pages (kernel stages its page ids in smem)
+        assert (((w[:, 5] - 1) // 64) - (w[:, 4] // 64) + 1 <= 255).all()
         slots = sorted(s for s in w[:, 6] if s >= 0)
         assert slots == list(range(plan.n_partials))
         for g in plan.groups_host:

@@ -79,28 +79,23 @@ print(f"K1 per launch: {t_k1/L*1e3:.2f} us -> {k1b/(t_k1/L*1e-3)/1e9:.0f} GB/s ;
 
 # ---- timeline trace of one K2 launch
 from paper_2605_24832_b200 import _lib
-tr = torch.zeros((plan.grid, 512), dtype=torch.int64, device=dev)
+tr = torch.zeros((plan.grid, 1024), dtype=torch.int64, device=dev)
 _lib.call("optimus_set_attn_trace", tr.data_ptr())
 k2(0)
 torch.cuda.synchronize()
 _lib.call("optimus_set_attn_trace", None)
 t = tr.cpu().numpy().astype(np.float64)
-t0 = t[t > 0].min()
-np.set_printoptions(linewidth=200, precision=0, suppress=True)
-for c in (0, 1, 70, 147):
+np.set_printoptions(linewidth=220, precision=0, suppress=True)
+for c in (0, 70):
+    c0 = t[c, 3 * 128 + 126]  # clock at setup done
     n = int((t[c, 128:256] > 0).sum())
-    print(f"CTA {c}: tiles={n}")
-    for role, name in enumerate(["prod_issue", "mma_S", "smx_Sready", "smx_Pdone"]):
-        v = t[c, role * 128: role * 128 + min(n, 40)]
-        print(f"  {name:11s}", ((v - t0) / 1e3).round(2))
-entry = t[:, 3 * 128 + 127]; setup = t[:, 3 * 128 + 126]; fin = t[:, 2 * 128 + 127]; out_ = t[:, 2 * 128 + 126]
-print("entry (us) pctl", np.percentile((entry - t0) / 1e3, [0, 50, 100]).round(2))
-print("setup done    ", np.percentile((setup - t0) / 1e3, [0, 50, 100]).round(2))
-print("work finished ", np.percentile((fin - t0) / 1e3, [0, 50, 100]).round(2))
-print("dealloc done  ", np.percentile((out_ - t0) / 1e3, [0, 50, 100]).round(2))
+    print(f"CTA {c}: tiles={n} (cycles since setup, /100)")
+    for role, name in [(4, "prod_top"), (0, "prod_kfree"), (5, "prod_Kissued"), (6, "prod_vfree"), (7, "prod_Vissued"), (1, "mma_S"), (2, "smx_Sready"), (3, "smx_Pdone")]:
+        v = t[c, role * 128: role * 128 + min(n, 30)]
+        print(f"  {name:12s}", ((v - c0) / 100).round(0))
+    fin = t[c, 2 * 128 + 127]
+    print("  work finished at", (fin - c0) / 1e3, "kcycles")
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 torch.cuda._sleep(int(1e8))
 e0.record(); k2(0); e1.record(); torch.cuda.synchronize()
 print("single launch event time (us):", e0.elapsed_time(e1) * 1e3)
-ends = np.where(t > 0, t, 0).max(axis=1)
-print("CTA end times (us) pctl:", np.percentile((ends - t0) / 1e3, [0, 50, 90, 100]).round(1))
