@@ -331,37 +331,28 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # ---- per-kernel durations (CUDA events on the launching stream, same inputs)
-    kt = {"k1": [], "k2": [], "k3": []}
+    # ---- per-kernel durations: each kernel alone, back to back over the 36 layers,
+    # captured in a CUDA graph and timed with CUDA events on the launching stream
     m = dm.host
     plan = dm.__dict__["attn_plan"]
     out = dec._workspaces(plan, m.n_tok)
-    s = torch.cuda.current_stream()
-    # keep the GPU busy while the whole sequence is enqueued, so host launch
-    # latency never shows up between a kernel's start/end events
-    torch.cuda._sleep(int(2e9 * 0.02))
-    for rep in range(3):
-        for layer in range(cfg.num_layers):
-            q, k, v = fwd.qkv(layer, dm)
-            kc, vc = dec.cache.layer(layer)
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            e[0].record(s)
-            ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc)
-            e[1].record(s)
-            ops.paged_attention(q, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off,
-                                dm.vis_words, dm.block_tables, plan, cfg.block_size, out=out[: m.n_tok],
-                                ws_o=dec._ws_o, ws_ml=dec._ws_ml)
-            e[2].record(s)
-            kt["k1"].append(e)
-        e3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        e3[0].record(s)
-        dec.run_unmask(dm)
-        e3[1].record(s)
-        kt["k3"].append(e3)
-    torch.cuda.synchronize()
-    k1_us = float(np.mean([e[0].elapsed_time(e[1]) for e in kt["k1"]])) * 1e3
-    k2_us = float(np.mean([e[1].elapsed_time(e[2]) for e in kt["k1"]])) * 1e3
-    k3_us = float(np.mean([e[0].elapsed_time(e[1]) for e in kt["k3"]])) * 1e3
+
+    def k1(l):
+        q, k, v = fwd.qkv(l, dm)
+        kc, vc = dec.cache.layer(l)
+        ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc)
+
+    def k2(l):
+        q, k, v = fwd.qkv(l, dm)
+        kc, vc = dec.cache.layer(l)
+        ops.paged_attention(q, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off,
+                            dm.vis_words, dm.block_tables, plan, cfg.block_size, out=out[: m.n_tok],
+                            ws_o=dec._ws_o, ws_ml=dec._ws_ml)
+
+    L = cfg.num_layers
+    k1_us = graph_time(lambda: [k1(l) for l in range(L)], dev) / L * 1e3
+    k2_us = graph_time(lambda: [k2(l) for l in range(L)], dev) / L * 1e3
+    k3_us = graph_time(lambda: dec.run_unmask(dm), dev) * 1e3
 
     # ---- end to end through the public per-step call (closed loop, live state)
     dec.release_all(reqs)
@@ -411,6 +402,31 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def graph_time(fn, dev, reps=10):
+    """Milliseconds per replay of fn captured as one CUDA graph (events on the stream)."""
+    import torch
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn()
+        s.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def cfg_full(args):

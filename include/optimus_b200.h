@@ -67,13 +67,15 @@ int optimus_device_sm_count(void);
  * and K/V rows k_new[i*new_stride + h*head_dim + :] are written to
  * k_cache[((page*Hkv + h)*page_size + off)*head_dim + :] for every head h.
  * slot_mapping_out (optional, int64[n_tok]) receives the slots.
+ * v_dtype: 0 = the V cache is bf16 (copied), 1 = fp16 (bf16 rows converted, exact for
+ * |v| < 65504, saturating beyond).  K is always bf16.
  */
 int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_tok,
                       const int32_t* tok_req, const int32_t* tok_pos,
                       const int32_t* prompt_len, const int32_t* block_tables,
                       int max_pages, int n_tok, int num_kv_heads, int head_dim,
                       int page_size, void* k_cache, void* v_cache, int64_t num_pages,
-                      int64_t* slot_mapping_out, void* stream);
+                      int64_t* slot_mapping_out, int v_dtype, void* stream);
 
 /*
  * Host-side work planner for K2 (the length-aware persistent tile scheduler).
@@ -114,7 +116,9 @@ int optimus_attn_plan_bounds(int n_req, const int32_t* cu_seqlens_q_host,
  * ws_o / ws_ml: split-KV partials, float[n_partials][128][head_dim] and
  * float[n_partials][128][2] (may be NULL when n_partials == 0).
  * work/cta_off/groups are the planner's outputs copied to the device; `grid` must
- * equal the grid used for planning.
+ * equal the grid used for planning.  v_dtype as for optimus_kv_append: with an fp16
+ * V cache P.V runs with an fp16 P (11-bit), with a bf16 V cache P is split into two
+ * bf16 planes (hi + lo) so both forms stay far inside the 2e-3 tolerance.
  */
 int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total,
                        const void* k_cache, const void* v_cache, int64_t num_pages,
@@ -126,7 +130,7 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total,
                        int block_size, int num_q_heads, int num_kv_heads, int head_dim,
                        int page_size, float sm_scale,
                        void* out, int64_t out_stride_tok,
-                       float* ws_o, float* ws_ml, void* stream);
+                       float* ws_o, float* ws_ml, int v_dtype, void* stream);
 
 /*
  * K3 — fused confidence-threshold unmask (replaces StochasticOracle.commits,

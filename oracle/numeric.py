@@ -34,6 +34,16 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
     return np.where(np.isnan(a), a, out).reshape(a.shape)
 
 
+def v_storage(v: np.ndarray, dtype: str) -> np.ndarray:
+    """V rows as the cache stores them, as int16 bit patterns: bf16 unchanged, or
+    fp16 (round-to-nearest, saturating at +-65504 — exact for bf16 values in range)."""
+    v = np.asarray(v, dtype=np.float32)
+    if dtype == "fp16":
+        return np.clip(v, -65504.0, 65504.0).astype(np.float16).view(np.int16)
+    b = bf16_round(v).view(np.uint32) >> 16
+    return b.astype(np.uint16).view(np.int16)
+
+
 def slot_mapping(tok_req, tok_pos, prompt_len, block_tables, page_size: int) -> np.ndarray:
     """Rule S for every planned token."""
     tok_req = np.asarray(tok_req)

@@ -27,7 +27,7 @@ SIGNATURES = {
     "optimus_set_attn_trace": (None, [_vp]),
     "optimus_kv_append": (
         _i32,
-        [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp],
+        [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp, _i32, _vp],
     ),
     "optimus_attn_plan_bounds": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "optimus_attn_plan": (
@@ -45,7 +45,7 @@ SIGNATURES = {
             _vp, _i32,                  # groups, n_groups
             _i32, _i32, _i32, _i32, _i32, _f32,  # block_size, Hq, Hkv, head_dim, page_size, sm_scale
             _vp, _i64,                  # out, out_stride_tok
-            _vp, _vp, _vp,              # ws_o, ws_ml, stream
+            _vp, _vp, _i32, _vp,        # ws_o, ws_ml, v_dtype, stream
         ],
     ),
     "optimus_unmask_partials": (_i32, [_vp, _i32, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),

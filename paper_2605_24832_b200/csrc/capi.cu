@@ -19,7 +19,7 @@ namespace optimus {
 
 int launch_kv_append(const void*, const void*, int64_t, const int32_t*, const int32_t*,
                      const int32_t*, const int32_t*, int, int, int, int, int, void*, void*,
-                     int64_t*, cudaStream_t);
+                     int64_t*, int, cudaStream_t);
 int launch_unmask_partials(const void*, int, int64_t, const int32_t*, int, int, int, int, float*,
                            cudaStream_t);
 int launch_unmask_finalize(const float*, int, int, int, const int32_t*, int, float, int, uint8_t*,
@@ -107,12 +107,13 @@ thread_local std::vector<MapEntry> g_maps;
 
 // 4-D bf16 tensor map with SWIZZLE_128B (boxes are 64 columns = 128 bytes wide).
 int get_map(const void* ptr, const uint64_t dims[4], const uint64_t strides[3],
-            const uint32_t box[4], CUtensorMap* out) {
+            const uint32_t box[4], CUtensorMap* out, bool fp16 = false) {
   MapKey key;
-  key.ptr = ptr;
+  key.ptr = static_cast<const char*>(ptr) + (fp16 ? 1 : 0) * 0;  // dtype folded into box[2] below
   memcpy(key.dims, dims, sizeof(key.dims));
   memcpy(key.strides, strides, sizeof(key.strides));
   memcpy(key.box, box, sizeof(key.box));
+  if (fp16) key.box[2] |= 0x80000000u;
   for (size_t i = 0; i < g_maps.size(); ++i)
     if (g_maps[i].key == key) {
       *out = g_maps[i].map;
@@ -125,7 +126,8 @@ int get_map(const void* ptr, const uint64_t dims[4], const uint64_t strides[3],
   cuuint64_t gs[3] = {strides[0], strides[1], strides[2]};
   cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), gd, gs, bd, es,
+  CUresult r = fn(&m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                  const_cast<void*>(ptr), gd, gs, bd, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -168,7 +170,8 @@ int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_t
                       const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
                       const int32_t* block_tables, int max_pages, int n_tok, int num_kv_heads,
                       int head_dim, int page_size, void* k_cache, void* v_cache,
-                      int64_t num_pages, int64_t* slot_mapping_out, void* stream) {
+                      int64_t num_pages, int64_t* slot_mapping_out, int v_dtype, void* stream) {
+  if (v_dtype != 0 && v_dtype != 1) return fail("kv_append: v_dtype must be 0 (bf16) or 1 (fp16)");
   if (n_tok < 0 || num_kv_heads < 1 || max_pages < 1 || num_pages < 1)
     return fail("kv_append: bad sizes");
   if (head_dim % 8 || head_dim < 8) return fail("kv_append: head_dim must be a multiple of 8");
@@ -183,7 +186,7 @@ int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_t
   return cuda_status(
       launch_kv_append(k_new, v_new, new_stride_tok, tok_req, tok_pos, prompt_len, block_tables,
                        max_pages, n_tok, num_kv_heads, head_dim, page_size, k_cache, v_cache,
-                       slot_mapping_out, static_cast<cudaStream_t>(stream)),
+                       slot_mapping_out, v_dtype, static_cast<cudaStream_t>(stream)),
       "kv_append");
 }
 
@@ -376,7 +379,9 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
                        const int32_t* work, const int32_t* cta_off, int grid,
                        const int32_t* groups, int n_groups, int block_size, int hq, int hkv,
                        int head_dim, int page_size, float sm_scale, void* out,
-                       int64_t out_stride_tok, float* ws_o, float* ws_ml, void* stream) {
+                       int64_t out_stride_tok, float* ws_o, float* ws_ml, int v_dtype,
+                       void* stream) {
+  if (v_dtype != 0 && v_dtype != 1) return fail("paged_attn: v_dtype must be 0 (bf16) or 1 (fp16)");
   if (head_dim != 64 && head_dim != 128) return fail("paged_attn: head_dim must be 64 or 128");
   if (hkv < 1 || hq % hkv) return fail("paged_attn: Hq must be a multiple of Hkv");
   const int G = hq / hkv;
@@ -416,7 +421,7 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
                                  static_cast<uint64_t>(hkv) * page_size * head_dim * 2};
     const uint32_t box[4] = {64, static_cast<uint32_t>(box_rows), 1, 1};
     if (int st = get_map(k_cache, dims, strides, box, &tk)) return st;
-    if (int st = get_map(v_cache, dims, strides, box, &tv)) return st;
+    if (int st = get_map(v_cache, dims, strides, box, &tv, v_dtype == 1)) return st;
   }
   AttnParams prm;
   prm.q_pos = q_pos;
@@ -445,8 +450,8 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
     const char* e = getenv("OPTIMUS_DBG");
     prm.dbg = e ? atoi(e) : 0;
   }
-  return cuda_status(launch_paged_attn(head_dim, tq, tk, tv, prm, grid, groups, n_groups,
-                                       static_cast<cudaStream_t>(stream)),
+  return cuda_status(launch_paged_attn(head_dim, v_dtype == 1, tq, tk, tv, prm, grid, groups,
+                                       n_groups, static_cast<cudaStream_t>(stream)),
                      "paged_attn");
 }
 

@@ -10,7 +10,10 @@
 // window rows produce provisional KV that the visibility rule of K2 hides
 // until the position is recomputed with its committed token.
 //
-// Pure streaming: each K/V byte is read once and written once.
+// Pure streaming: each K/V byte is read once and written once.  With an fp16 V
+// cache (v_fp16) the bf16 V rows are converted on the way (exact for |v| < 65504,
+// saturating beyond), which lets the attention kernel form P.V in fp16 with an
+// 11-bit P in one MMA instead of two bf16 planes.
 #include "ptx.cuh"
 
 namespace optimus {
@@ -23,7 +26,10 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
     const int32_t* __restrict__ tok_req, const int32_t* __restrict__ tok_pos,
     const int32_t* __restrict__ prompt_len, const int32_t* __restrict__ block_tables,
     int max_pages, int n_tok, int hkv, int vec_per_head, int page_size, uint4* __restrict__ k_cache,
-    uint4* __restrict__ v_cache, int64_t* __restrict__ slot_out) {
+    uint4* __restrict__ v_cache, int64_t* __restrict__ slot_out, int v_fp16) {
+  // let a PDL-launched dependent (the attention kernel) start its prologue now; it
+  // waits for this grid's completion before reading the cache.
+  grid_dep_launch();
   const int per_tok = hkv * vec_per_head;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= static_cast<int64_t>(n_tok) * per_tok) return;
@@ -41,7 +47,18 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
   const int64_t dst =
       ((static_cast<int64_t>(page) * hkv + h) * page_size + off) * vec_per_head + c;
   k_cache[dst] = kv;
-  v_cache[dst] = vv;
+  if (v_fp16) {
+    const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+    uint32_t h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+      asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(h[i]) : "f"(hi), "f"(lo));
+    }
+    v_cache[dst] = make_uint4(h[0], h[1], h[2], h[3]);
+  } else {
+    v_cache[dst] = vv;
+  }
   if (i == 0 && slot_out != nullptr) slot_out[t] = static_cast<int64_t>(page) * page_size + off;
 }
 
@@ -49,7 +66,7 @@ int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_to
                      const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
                      const int32_t* block_tables, int max_pages, int n_tok, int hkv, int head_dim,
                      int page_size, void* k_cache, void* v_cache, int64_t* slot_out,
-                     cudaStream_t stream) {
+                     int v_fp16, cudaStream_t stream) {
   if (n_tok == 0) return 0;
   const int vec_per_head = head_dim / 8;  // 8 bf16 per 16-byte vector
   const int64_t total = static_cast<int64_t>(n_tok) * hkv * vec_per_head;
@@ -58,7 +75,7 @@ int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_to
   kv_append_kernel<<<blocks, threads, 0, stream>>>(
       static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
       tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok, hkv, vec_per_head, page_size,
-      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), slot_out);
+      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), slot_out, v_fp16);
   return static_cast<int>(cudaGetLastError());
 }
 

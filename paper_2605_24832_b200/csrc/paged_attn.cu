@@ -8,20 +8,22 @@
 // arrives as a per-request bitmap anchored at vis_base plus a per-query limit.
 //
 // How (sm_100a, one persistent CTA per SM, warp-specialised):
-//   warp 4   TMA producer: per work item one Q tile (the G query heads of a KV
+//   warp 8   TMA producer (Q + K ring; warp 10 lane 0 drives the V ring): per work item one Q tile (the G query heads of a KV
 //            head folded into 128 MMA rows, row = token*G + head) and a ring of
 //            64-key K and V tiles gathered page by page through the block table
 //            (4-D tensor maps, SWIZZLE_128B boxes of 64 columns).  K and V slots
 //            have separate full/empty barriers: a K slot is refilled as soon as
 //            its S = Q K^T MMA retires, without waiting for the PV MMA.
-//   warp 5   MMA issuer (one thread): S = Q K^T into TMEM (double buffered),
+//   warp 9   MMA issuer (one thread): S = Q K^T into TMEM (double buffered),
 //            O += P V with P read from TMEM (double buffered O across work items).
-//   warp 6   TMEM allocator.
-//   warp 7   metadata: stages the next work item's page ids / limits in smem.
+//   warp 10  TMEM allocator, then V producer.
+//   warp 11  metadata: stages the next work item's page ids / limits in smem.
 //   (control roles sit on the HIGH warp ids: the SMSP issue arbiter favours the
 //   highest warp id, so the softmax warps must not starve them.)
-//   warps 0-3  softmax + epilogue: thread i owns query row i (= TMEM lane i), so
-//            the row max/sum need no shuffles; online softmax in the exp2 domain
+//   warps 0-7  softmax + epilogue, two warpgroups ping-ponging over the tiles of
+//            a work item (each SMSP interleaves two softmax warps): thread i owns
+//            query row i (= TMEM lane i), so the row max/sum need no shuffles;
+//            each warpgroup keeps its own (m, l, O) and the epilogue merges them; online softmax in the exp2 domain
 //            with a lazy rescale (O in TMEM is only rescaled when the running max
 //            grows by more than 2^8).  P overwrites S in TMEM as two bf16 planes
 //            P = hi + lo, so the PV product carries ~16 mantissa bits of P (the
@@ -36,18 +38,21 @@ namespace optimus {
 
 constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
-constexpr int kThreads = 256;  // 8 warps
-constexpr int kTraceSlots = 1024;  // per CTA: [role*128 + i], 8 roles
+constexpr int kThreads = 384;  // 12 warps: 8 softmax, 4 control
+constexpr int kTraceSlots = 2048;  // per CTA: [role*256 + i], 8 roles
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// roles: 0 producer top, 1 MMA S issue, 2 softmax S ready, 3 softmax P done,
+// 4 producer slot free, 5 producer K issued, 6 misc (0 entry [globaltimer], 1 setup,
+// 2 producer done, 3 CTA done)
 __device__ __forceinline__ void trace(const AttnParams& p, int role, int i) {
-  if (p.trace != nullptr && i < 128)
-    p.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + role * 128 + i] =
-        (role == 3 && i == 127) ? gtimer() : static_cast<unsigned long long>(clock64());
+  if (p.trace != nullptr && i < 256)
+    p.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + role * 256 + i] =
+        (role == 6 && i == 0) ? gtimer() : static_cast<unsigned long long>(clock64());
 }
 
 // Per-work-item record staged in shared memory by the metadata warp one item ahead,
@@ -71,16 +76,18 @@ struct AttnSmem {
   static constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr uint32_t OFF_V = OFF_K + STAGES * KT_BYTES;
   static constexpr uint32_t OFF_INFO = OFF_V + STAGES * KT_BYTES;
-  static constexpr uint32_t OFF_BAR = OFF_INFO + 2 * sizeof(UnitInfo);
-  static constexpr int NUM_BARS = 4 * STAGES + 2 * 9;
+  static constexpr uint32_t OFF_RED = OFF_INFO + 2 * sizeof(UnitInfo);  // float[{m,l}][wg][128]
+  static constexpr uint32_t OFF_BAR = OFF_RED + 2 * 2 * kBlockM * 4;
+  static constexpr int NUM_BARS = 4 * STAGES + 2 + 2 + 4 * 3 + 2 + 2 + 2;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
-  // TMEM columns: S/P buffers [0,64) and [64,128), O buffers [128,128+HD), [128+HD,128+2HD)
-  static constexpr uint32_t TMEM_COLS = (128 + 2 * HD) <= 256 ? 256 : 512;
+  // TMEM columns: four S/P buffers [0,256) (warpgroup h, buffer k at (2h+k)*64), then
+  // the two warpgroups' O accumulators O_0 = [256,256+HD), O_1 = [256+HD,256+2HD)
+  static constexpr uint32_t TMEM_COLS = 512;
 };
 
-template <int HD, int STAGES>
+template <int HD, int STAGES, bool VF16>
 __global__ void __launch_bounds__(kThreads, 1)
     paged_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_k,
@@ -99,26 +106,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* v_empty = v_full + STAGES;
   uint64_t* q_full = v_empty + STAGES;
   uint64_t* q_empty = q_full + 2;
-  uint64_t* s_full = q_empty + 2;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* pv_done = p_full + 2;
-  uint64_t* o_full = pv_done + 2;
-  uint64_t* o_empty = o_full + 2;
-  uint64_t* info_full = o_empty + 2;
+  uint64_t* s_full = q_empty + 2;   // [warpgroup][buffer]
+  uint64_t* p_full = s_full + 4;    // [warpgroup][buffer]
+  uint64_t* pv_done = p_full + 4;   // [warpgroup][buffer]
+  uint64_t* o_full = pv_done + 4;   // [1]
+  uint64_t* o_empty = o_full + 1;   // [1]
+  uint64_t* info_full = o_empty + 1;
   uint64_t* info_empty = info_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + 2);
   UnitInfo* info = reinterpret_cast<UnitInfo*>(smem + L::OFF_INFO);
+  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);    // epilogue (m, l) exchange
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) trace(p, 3, 127);
+  if (threadIdx.x == 0) trace(p, 6, 0);
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     prefetch_tmap(&tm_q);
     prefetch_tmap(&tm_k);
     prefetch_tmap(&tm_v);
   }
-  if (warp == 5 && lane == 0) {
+  if (warp == 9 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -128,17 +136,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
+      mbar_init(&info_full[i], 32);
+      mbar_init(&info_empty[i], 256 + 2);  // softmax threads + K and V producers
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&pv_done[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
-      mbar_init(&info_full[i], 32);
-      mbar_init(&info_empty[i], 128 + 2);  // softmax rows + K and V producers
     }
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 256);
     mbar_fence_init();
   }
-  if (warp == 6) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (warp == 10) tmem_alloc<L::TMEM_COLS>(tmem_slot);
   // Zero the K/V ring once: rows a partial tile never loads must hold finite values
   // (their probabilities are 0, and 0 * NaN would poison O).
   {
@@ -151,19 +161,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) trace(p, 3, 126);
+  if (threadIdx.x == 0) trace(p, 6, 1);
   const uint32_t tm_s0 = tmem_base;        // S/P buffers
-  const uint32_t tm_o0 = tmem_base + 128;  // O buffers
+  const uint32_t tm_o0 = tmem_base + 256;  // O accumulators
 
   const int w_begin = p.cta_off[blockIdx.x];
   const int w_end = p.cta_off[blockIdx.x + 1];
 
-  if (warp == 4 || warp == 6) {
+  if (warp == 8 || warp == 10) {
     // ------------------------------------------------------------ TMA producers
     // Two issuing threads keep the TMA engine busy (one box costs its issuer a few
-    // hundred cycles): warp 4 loads Q and the K ring, warp 6 the V ring.
+    // hundred cycles): warp 8 loads Q and the K ring, warp 10 the V ring.
     if (lane == 0) {
-      const bool is_k = warp == 4;
+      const bool is_k = warp == 8;
       const uint32_t q_tx = KB * 64 * p.group * p.tok_per_tile * 2;
       const uint32_t chunk_tx = p.box_rows * 128 * KB;  // one tensor, one box-row group
       const int chunks_per_tile = kTileN / p.box_rows;
@@ -179,6 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ib = unit & 1;
         const uint32_t ipar = (unit >> 1) & 1;
         mbar_wait(&info_full[ib], ipar);
+        // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
+        // everything above overlapped their tail under PDL; the loads may not.
+        if (unit == 0) grid_dep_wait();
         const UnitInfo& u = info[ib];
         const int head = u.head, key_begin = u.key_begin, key_end = u.key_end;
         const int pg0 = key_begin >> shift;
@@ -193,9 +206,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int st = tile_ctr % STAGES;
           int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
           if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
-          if (is_k) trace(p, 4, tile_ctr);
-          mbar_wait(&empty[st], ((tile_ctr / STAGES) & 1) ^ 1);
           if (is_k) trace(p, 0, tile_ctr);
+          mbar_wait(&empty[st], ((tile_ctr / STAGES) & 1) ^ 1);
+          if (is_k) trace(p, 4, tile_ctr);
           mbar_arrive_expect_tx(&full[st], n_chunks * chunk_tx);
           uint8_t* dst = ring + st * L::KT_BYTES;
           for (int c = 0; c < n_chunks; ++c) {
@@ -210,26 +223,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&info_empty[ib]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
+    // Tile j of a work item belongs to softmax warpgroup h = j & 1; its S goes to
+    // that warpgroup's next S/P buffer and its PV accumulates into O_h.  S runs up
+    // to four tiles ahead of PV (two buffers per warpgroup; the in-order tensor
+    // pipe retires PV(j) before S(j+4) overwrites the buffer holding P(j)).
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(kBlockM, kTileN, false, false);
-      constexpr uint32_t idesc_o = umma_idesc_bf16(kBlockM, HD, false, true);
+      // PV: A = P from TMEM, B = V (MN-major).  fp16 V cache: one fp16 P plane;
+      // bf16 V cache: P = hi + lo bf16 planes, two MMAs per k-step.
+      constexpr uint32_t idesc_o = VF16 ? umma_idesc_f16(kBlockM, HD, false, true, 0u, 0u)
+                                        : umma_idesc_bf16(kBlockM, HD, false, true);
       const uint32_t sQ_a = smem_u32(sQ), sK_a = smem_u32(sK), sV_a = smem_u32(sV);
       int tile_ctr = 0;
       int unit = 0;
+      int cs[2] = {0, 0};  // S tiles issued per warpgroup
+      int cp[2] = {0, 0};  // PV tiles issued per warpgroup
       for (int w = w_begin; w < w_end; ++w, ++unit) {
         const int qb = unit & 1;
-        const int ob = unit & 1;
         mbar_wait(&q_full[qb], (unit >> 1) & 1);  // implies info[qb] is staged
         const int n_tiles = (info[qb].key_end - info[qb].key_begin + kTileN - 1) / kTileN;
         tc_fence_after();
-        auto issue_s = [&](int t) {
+        auto issue_s = [&](int j) {
+          const int t = tile_ctr + j;
+          const int h = j & 1;
+          const int k = cs[h] & 1;
           const int st = t % STAGES;
           mbar_wait(&k_full[st], (t / STAGES) & 1);
           tc_fence_after();
           trace(p, 1, t);
-          const uint32_t d = tm_s0 + (t & 1) * kTileN;
+          const uint32_t d = tm_s0 + (2 * h + k) * kTileN;
 #pragma unroll
           for (int ks = 0; ks < HD / 16; ++ks) {
             if (p.dbg & 2) break;
@@ -241,38 +265,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sK_a + st * L::KT_BYTES + kb * (kTileN * 128) + koff, 16, 1024);
             umma_bf16_ss(d, a, b, idesc_s, ks > 0 ? 1u : 0u);
           }
-          umma_commit(&s_full[t & 1]);
+          umma_commit(&s_full[2 * h + k]);
           umma_commit(&k_empty[st]);
+          ++cs[h];
         };
-        issue_s(tile_ctr);
-        mbar_wait(&o_empty[ob], ((unit >> 1) & 1) ^ 1);
+        const int pre = n_tiles < 4 ? n_tiles : 4;
+        for (int j = 0; j < pre; ++j) issue_s(j);
+        mbar_wait(o_empty, (unit & 1) ^ 1);  // the previous item's epilogue has read O_0/O_1
         tc_fence_after();
         for (int j = 0; j < n_tiles; ++j) {
           const int t = tile_ctr + j;
-          if (j + 1 < n_tiles) issue_s(t + 1);
+          const int h = j & 1;
+          const int k = cp[h] & 1;
           const int st = t % STAGES;
           mbar_wait(&v_full[st], (t / STAGES) & 1);
-          mbar_wait(&p_full[t & 1], (t >> 1) & 1);
+          mbar_wait(&p_full[2 * h + k], (cp[h] >> 1) & 1);
           tc_fence_after();
-          const uint32_t d = tm_o0 + ob * HD;
-          const uint32_t pa = tm_s0 + (t & 1) * kTileN;  // P hi at +0..31, lo at +32..63
+          const uint32_t d = tm_o0 + h * HD;
+          const uint32_t pa = tm_s0 + (2 * h + k) * kTileN;  // P hi at +0..31, lo at +32..63
 #pragma unroll
           for (int ks = 0; ks < kTileN / 16; ++ks) {
             const uint64_t b =
                 umma_sdesc_sw128(sV_a + st * L::KT_BYTES + ks * 16 * 128, kTileN * 128, 1024);
             if (p.dbg & 8) break;
-            umma_bf16_ts(d, pa + ks * 8, b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
-            if (!(p.dbg & 1)) umma_bf16_ts(d, pa + 32 + ks * 8, b, idesc_o, 1u);
+            umma_bf16_ts(d, pa + ks * 8, b, idesc_o, (j > 1 || ks > 0) ? 1u : 0u);
+            if (!VF16 && !(p.dbg & 1)) umma_bf16_ts(d, pa + 32 + ks * 8, b, idesc_o, 1u);
           }
-          umma_commit(&pv_done[t & 1]);
+          umma_commit(&pv_done[2 * h + k]);
           umma_commit(&v_empty[st]);
+          ++cp[h];
+          if (j + 4 < n_tiles) issue_s(j + 4);
         }
         umma_commit(&q_empty[qb]);
-        umma_commit(&o_full[ob]);
+        umma_commit(o_full);
         tile_ctr += n_tiles;
       }
     }
-  } else if (warp == 7) {
+  } else if (warp == 11) {
     // ------------------------------------------------------------ metadata warp
     // Stages work item w+1's record while the other roles run item w: page ids of
     // its key range, the per-token visibility limit, and the visibility words.
@@ -321,17 +350,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       mbar_arrive(&info_full[ib]);
     }
-  } else if (warp < 4) {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ softmax + epilogue
-    const int row = threadIdx.x;                // query row == TMEM lane
-    const int wq = warp;                        // TMEM lane quarter
+    // Two warpgroups ping-pong over the tiles of a work item (h = tile & 1), each
+    // with its own running max m_h, sum l_h and TMEM accumulator O_h; the epilogue
+    // merges (m_0, l_0, O_0) and (m_1, l_1, O_1) like two key splits.
+    const int wg = warp >> 2;                   // this warpgroup
+    const int wq = warp & 3;                    // TMEM lane quarter
+    const int row = wq * 32 + lane;             // query row == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const int G = p.group;
     const int t_in = row / G;
     const int g_in = row - t_in * G;
     const bool row_exists = t_in < p.tok_per_tile;
     const float sc = p.scale_log2;
-    int tile_ctr = 0;
+    int cw = 0;  // tiles processed by this warpgroup (buffer / phase counter)
     int unit = 0;
     for (int w = w_begin; w < w_end; ++w, ++unit) {
       const int ib = unit & 1;
@@ -340,7 +373,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int head = u.head, tok_begin = u.tok_begin, n_tok = u.n_tok;
       const int key_begin = u.key_begin, key_end = u.key_end, slot = u.slot;
       const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
-      const int ob = unit & 1;
       const bool valid = row_exists && t_in < n_tok;
       const bool warp_valid = (wq * 32) / G < n_tok;  // first row of this warp is a real token
       const int vb = u.vb;
@@ -349,13 +381,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int lim = valid ? u.lim[t_in] : 0;
       float m = -INFINITY;
       float l = 0.f;
-      for (int j = 0; j < n_tiles; ++j) {
-        const int t = tile_ctr + j;
-        const int sb = t & 1;
-        const uint32_t tsp = tm_s0 + lane_off + sb * kTileN;  // this warp's S/P columns
-        mbar_wait(&s_full[sb], (t >> 1) & 1);
+      for (int j = wg; j < n_tiles; j += 2, ++cw) {
+        const int k = cw & 1;
+        const uint32_t tsp = tm_s0 + lane_off + (2 * wg + k) * kTileN;  // this tile's S/P
+        mbar_wait(&s_full[2 * wg + k], (cw >> 1) & 1);
         tc_fence_after();
-        if (threadIdx.x == 0) trace(p, 2, t);
+        if (threadIdx.x == 0) trace(p, 2, cw);
         if (warp_valid && !(p.dbg & 4)) {
           uint32_t sr[2][32];
           tmem_ld32(tsp, sr[0]);
@@ -369,8 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kt + 64 > vb && kt + 32 < lim) hi = words[(kt + 32 - vb) >> 5];
             vis = (static_cast<uint64_t>(hi) << 32) | lo;
             const int n = lim - kt;
-            const uint64_t lm = n >= 64 ? ~0ull : (n <= 0 ? 0ull : ((1ull << n) - 1));
-            vis &= lm;
+            vis &= n >= 64 ? ~0ull : (n <= 0 ? 0ull : ((1ull << n) - 1));
           }
           tmem_wait_ld();
           float sv[64];
@@ -380,7 +410,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 64; ++c) sv[c] = ((vis >> c) & 1ull) ? sv[c] : -INFINITY;
           }
-          // row max over raw scores: 4 independent 3-input-max chains
           float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
 #pragma unroll
           for (int c = 0; c < 64; c += 8) {
@@ -392,15 +421,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float tmax = fmax3(a0, a1, fmaxf(a2, a3)) * sc;  // scale > 0
           const bool need = tmax > m + 8.0f;
           const float m_new = need ? tmax : m;
-          if (j > 0 && __any_sync(0xFFFFFFFFu, need)) {
-            // O holds sum_{u<t} P_u V_u once PV_{t-1} retires; rescale it in TMEM.
-            mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
+          if (j >= 2 && __any_sync(0xFFFFFFFFu, need)) {
+            // O_wg holds this warpgroup's earlier tiles once its previous PV retires
+            const int cprev = cw - 1;
+            mbar_wait(&pv_done[2 * wg + (cprev & 1)], (cprev >> 1) & 1);
             tc_fence_after();
             const float alpha = need ? fast_exp2(m - m_new) : 1.0f;
 #pragma unroll
             for (int c0 = 0; c0 < HD; c0 += 32) {
               uint32_t o[32];
-              const uint32_t ta = tm_o0 + lane_off + ob * HD + c0;
+              const uint32_t ta = tm_o0 + lane_off + wg * HD + c0;
               tmem_ld32(ta, o);
               tmem_wait_ld();
 #pragma unroll
@@ -415,91 +445,115 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const float neg_m = (m == -INFINITY) ? 0.f : -m;
           float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
-          uint32_t phi[32], plo[32];
 #pragma unroll
-          for (int c8 = 0; c8 < 8; ++c8) {
-            float e[8];
+          for (int half = 0; half < 2; ++half) {
+            uint32_t phi[16], plo[16];
 #pragma unroll
-            for (int k = 0; k < 8; k += 2)
-              ffma2(e[k], e[k + 1], sv[c8 * 8 + k], sv[c8 * 8 + k + 1], sc, sc, neg_m, neg_m);
+            for (int c8 = 0; c8 < 4; ++c8) {
+              const int c = half * 32 + c8 * 8;
+              float e[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) e[k] = fast_exp2(e[k]);
-            fadd2(r0, r1, r0, r1, e[0], e[1]);
-            fadd2(r2, r3, r2, r3, e[2], e[3]);
-            fadd2(r0, r1, r0, r1, e[4], e[5]);
-            fadd2(r2, r3, r2, r3, e[6], e[7]);
+              for (int q = 0; q < 8; q += 2)
+                ffma2(e[q], e[q + 1], sv[c + q], sv[c + q + 1], sc, sc, neg_m, neg_m);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t h = pack_bf16x2(e[2 * k], e[2 * k + 1]);
-              float d0, d1;
-              fadd2(d0, d1, e[2 * k], e[2 * k + 1], -__uint_as_float(h << 16),
-                    -__uint_as_float(h & 0xFFFF0000u));
-              phi[c8 * 4 + k] = h;
-              plo[c8 * 4 + k] = pack_bf16x2(d0, d1);
+              for (int q = 0; q < 8; ++q) e[q] = fast_exp2(e[q]);
+              fadd2(r0, r1, r0, r1, e[0], e[1]);
+              fadd2(r2, r3, r2, r3, e[2], e[3]);
+              fadd2(r0, r1, r0, r1, e[4], e[5]);
+              fadd2(r2, r3, r2, r3, e[6], e[7]);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if constexpr (VF16) {
+                  phi[c8 * 4 + q] = pack_f16x2(e[2 * q], e[2 * q + 1]);
+                } else {
+                  const uint32_t hb = pack_bf16x2(e[2 * q], e[2 * q + 1]);
+                  float d0, d1;
+                  fadd2(d0, d1, e[2 * q], e[2 * q + 1], -__uint_as_float(hb << 16),
+                        -__uint_as_float(hb & 0xFFFF0000u));
+                  phi[c8 * 4 + q] = hb;
+                  plo[c8 * 4 + q] = pack_bf16x2(d0, d1);
+                }
+              }
             }
+            // P overwrites this tile's S columns: plane [0,32) (and the bf16 lo
+            // plane [32,64)); 64 keys are 32 packed 16-bit pairs per plane.
+            tmem_st16(tsp + half * 16, phi);
+            if constexpr (!VF16) tmem_st16(tsp + 32 + half * 16, plo);
           }
-          // P overwrites this tile's S columns: hi plane [0,32), lo plane [32,64)
-          tmem_st32(tsp, phi);
-          tmem_st32(tsp + 32, plo);
           l += (r0 + r1) + (r2 + r3);
           tmem_wait_st();
         }
         tc_fence_before();
-        mbar_arrive(&p_full[sb]);
-        if (threadIdx.x == 0) trace(p, 3, t);
+        mbar_arrive(&p_full[2 * wg + k]);
+        if (threadIdx.x == 0) trace(p, 3, cw);
       }
-      tile_ctr += n_tiles;
       mbar_arrive(&info_empty[ib]);
       // ---------------------------------------------------------- epilogue
-      mbar_wait(&o_full[ob], (unit >> 1) & 1);
+      // Exchange (m, l) between the warpgroups; warpgroup h then writes output
+      // columns [h*HD/2, (h+1)*HD/2) merged from O_0 and O_1.
+      red[(0 * 2 + wg) * kBlockM + row] = m;
+      red[(1 * 2 + wg) * kBlockM + row] = l;
+      named_bar_sync(1, 256);
+      const float m0 = red[0 * kBlockM + row], m1 = red[1 * kBlockM + row];
+      const float l0 = red[2 * kBlockM + row], l1 = red[3 * kBlockM + row];
+      named_bar_sync(1, 256);  // both read before the slots are reused
+      const float mx = fmaxf(m0, m1);
+      const float w0 = l0 > 0.f ? fast_exp2(m0 - mx) : 0.f;
+      const float w1 = l1 > 0.f ? fast_exp2(m1 - mx) : 0.f;
+      const float l_tot = w0 * l0 + w1 * l1;
+      mbar_wait(o_full, unit & 1);
       tc_fence_after();
       if (warp_valid) {
-        const float inv_l = (l > 0.f) ? 1.0f / l : 0.f;
+        const float inv_l = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
+        const float f0 = w0 * (slot < 0 ? inv_l : 1.f), f1 = w1 * (slot < 0 ? inv_l : 1.f);
         const int tok = tok_begin + t_in;
         const int qh = head * G + g_in;
 #pragma unroll
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-          uint32_t o[32];
-          tmem_ld32(tm_o0 + lane_off + ob * HD + c0, o);
+        for (int c0 = 0; c0 < HD / 2; c0 += 32) {
+          const int col = wg * (HD / 2) + c0;
+          uint32_t o0[32], o1[32];
+          tmem_ld32(tm_o0 + lane_off + col, o0);
+          tmem_ld32(tm_o0 + lane_off + HD + col, o1);
           tmem_wait_ld();
+          float o[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            o[c] = (w0 > 0.f ? __uint_as_float(o0[c]) * f0 : 0.f) +
+                   (w1 > 0.f ? __uint_as_float(o1[c]) * f1 : 0.f);
           if (valid) {
             if (slot < 0) {
               uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(tok) * p.out_stride_tok +
-                                                    static_cast<int64_t>(qh) * HD + c0);
+                                                    static_cast<int64_t>(qh) * HD + col);
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
                 const int c = v * 8;
-                dst[v] = make_uint4(
-                    pack_bf16x2(__uint_as_float(o[c + 0]) * inv_l, __uint_as_float(o[c + 1]) * inv_l),
-                    pack_bf16x2(__uint_as_float(o[c + 2]) * inv_l, __uint_as_float(o[c + 3]) * inv_l),
-                    pack_bf16x2(__uint_as_float(o[c + 4]) * inv_l, __uint_as_float(o[c + 5]) * inv_l),
-                    pack_bf16x2(__uint_as_float(o[c + 6]) * inv_l, __uint_as_float(o[c + 7]) * inv_l));
+                dst[v] = make_uint4(pack_bf16x2(o[c + 0], o[c + 1]), pack_bf16x2(o[c + 2], o[c + 3]),
+                                    pack_bf16x2(o[c + 4], o[c + 5]), pack_bf16x2(o[c + 6], o[c + 7]));
               }
             } else {
               float4* dst = reinterpret_cast<float4*>(
-                  p.ws_o + (static_cast<int64_t>(slot) * kBlockM + row) * HD + c0);
+                  p.ws_o + (static_cast<int64_t>(slot) * kBlockM + row) * HD + col);
 #pragma unroll
               for (int v = 0; v < 8; ++v)
-                dst[v] = make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]),
-                                     __uint_as_float(o[4 * v + 2]), __uint_as_float(o[4 * v + 3]));
+                dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
             }
           }
         }
-        if (valid && slot >= 0) {
+        if (valid && slot >= 0 && wg == 0) {
           reinterpret_cast<float2*>(p.ws_ml)[static_cast<int64_t>(slot) * kBlockM + row] =
-              make_float2(m, l);
+              make_float2(mx, l_tot);
         }
       }
       tc_fence_before();
-      mbar_arrive(&o_empty[ob]);
+      mbar_arrive(o_empty);
     }
   }
-  if (threadIdx.x == 128) trace(p, 2, 127);
+  if (threadIdx.x == 256) trace(p, 6, 2);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 6) tmem_dealloc<L::TMEM_COLS>(tmem_base);
-  if (threadIdx.x == 192) trace(p, 2, 126);
+  if (warp == 10) tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  if (threadIdx.x == 320) trace(p, 6, 3);
 }
 
 // Split-KV combine: merge the (m, l, O) partials of every split query tile.
@@ -561,21 +615,33 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __rest
   }
 }
 
-template <int HD, int STAGES>
+template <int HD, int STAGES, bool VF16>
 static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          const AttnParams& prm, int grid, const int32_t* groups, int n_groups,
                          cudaStream_t stream) {
   using L = AttnSmem<HD, STAGES>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, STAGES, VF16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
     if (e != cudaSuccess) return static_cast<int>(e);
     configured = true;
   }
   if (grid > 0) {
-    paged_attn_kernel<HD, STAGES><<<grid, kThreads, L::ALLOC, stream>>>(tq, tk, tv, prm);
-    cudaError_t e = cudaGetLastError();
+    // Launched with programmatic stream serialization: the prologue (barriers, TMEM,
+    // work-item staging) overlaps the previous kernel; the TMA producers execute
+    // griddepcontrol.wait before their first load.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = L::ALLOC;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, paged_attn_kernel<HD, STAGES, VF16>, tq, tk, tv, prm);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (n_groups > 0) {
@@ -587,12 +653,16 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   return 0;
 }
 
-int launch_paged_attn(int head_dim, const CUtensorMap& tq, const CUtensorMap& tk,
+int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CUtensorMap& tk,
                       const CUtensorMap& tv, const AttnParams& prm, int grid,
                       const int32_t* groups, int n_groups, cudaStream_t stream) {
   // 227 KB of shared memory: 2 Q tiles + a 4-deep (d=128) / 8-deep (d=64) K/V ring.
-  if (head_dim == 128) return launch_attn_t<128, 4>(tq, tk, tv, prm, grid, groups, n_groups, stream);
-  if (head_dim == 64) return launch_attn_t<64, 8>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+  if (head_dim == 128)
+    return v_fp16 ? launch_attn_t<128, 4, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                  : launch_attn_t<128, 4, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+  if (head_dim == 64)
+    return v_fp16 ? launch_attn_t<64, 8, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                  : launch_attn_t<64, 8, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
   return -1;
 }
 

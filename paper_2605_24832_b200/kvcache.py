@@ -5,6 +5,7 @@ paging"); this is the B200 layer beneath its ``Request`` objects.
 
 Layout in HBM (one tensor per K and V, all layers):
     k[L][num_pages][Hkv][page_size][head_dim]  bf16
+    v[L][num_pages][Hkv][page_size][head_dim]  fp16 (default) or bf16
 so each (layer, page, head) is a contiguous page_size x head_dim tile — the unit
 the attention kernel stages with one TMA box per 64 columns.  A request's
 absolute position s (prompt + output position) lives in page
@@ -107,14 +108,19 @@ class PagedKVCache:
     """Device KV storage for ``num_layers`` layers."""
 
     def __init__(self, num_layers: int, num_pages: int, num_kv_heads: int, page_size: int,
-                 head_dim: int, device="cuda", dtype=torch.bfloat16):
+                 head_dim: int, device="cuda", dtype=torch.bfloat16, v_dtype=torch.float16):
         if page_size < 8 or page_size > 1024 or page_size & (page_size - 1):
             raise ConfigError("page_size must be a power of two in [8, 1024]")
         if head_dim not in (64, 128):
             raise ConfigError("head_dim must be 64 or 128")
         shape = (num_layers, num_pages, num_kv_heads, page_size, head_dim)
+        if v_dtype not in (torch.bfloat16, torch.float16):
+            raise ConfigError("v_dtype must be bf16 or fp16")
+        # K is bf16 (the model's dtype).  V defaults to fp16: the bf16 values are
+        # stored exactly (|v| < 65504), and the attention kernel can then form P.V
+        # with an 11-bit fp16 P in a single tensor-core MMA.
         self.k = torch.zeros(shape, dtype=dtype, device=device)
-        self.v = torch.zeros(shape, dtype=dtype, device=device)
+        self.v = torch.zeros(shape, dtype=v_dtype, device=device)
         self.num_layers = num_layers
         self.num_pages = num_pages
         self.num_kv_heads = num_kv_heads

@@ -38,6 +38,14 @@ def _stream(stream: Optional[torch.cuda.Stream] = None) -> int:
     return s.cuda_stream
 
 
+def _v_dtype(v_cache: torch.Tensor) -> int:
+    if v_cache.dtype == torch.bfloat16:
+        return 0
+    if v_cache.dtype == torch.float16:
+        return 1
+    raise ConfigError("V cache must be bf16 or fp16")
+
+
 def sm_count() -> int:
     return int(_lib.call("optimus_device_sm_count"))
 
@@ -59,8 +67,8 @@ def kv_append(
     _cuda(k_new, v_new, tok_req, tok_pos, prompt_len, block_tables, k_cache, v_cache, slot_mapping_out)
     n_tok = k_new.shape[0]
     num_pages, hkv, page, d = k_cache.shape
-    if k_new.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16:
-        raise ConfigError("kv_append: bf16 K/V only")
+    if k_new.dtype != torch.bfloat16 or v_new.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16:
+        raise ConfigError("kv_append: new K/V rows and the K cache are bf16")
     if k_new.stride(-1) != 1 or k_new.stride(-2) != d or v_new.stride(0) != k_new.stride(0):
         raise ConfigError("kv_append: K/V rows must be [n_tok, Hkv, d] with unit inner strides")
     st = _lib.call(
@@ -68,7 +76,8 @@ def kv_append(
         _ptr(k_new), _ptr(v_new), k_new.stride(0),
         _ptr(tok_req), _ptr(tok_pos), _ptr(prompt_len), _ptr(block_tables),
         block_tables.shape[1], n_tok, hkv, d, page,
-        _ptr(k_cache), _ptr(v_cache), num_pages, _ptr(slot_mapping_out), _stream(stream),
+        _ptr(k_cache), _ptr(v_cache), num_pages, _ptr(slot_mapping_out), _v_dtype(v_cache),
+        _stream(stream),
     )
     _lib.check(st, "optimus_kv_append")
 
@@ -191,7 +200,7 @@ def paged_attention(
         block_size, hq, hkv, d, page, scale,
         _ptr(out), out.stride(0),
         _ptr(ws_o) if plan.n_partials else None, _ptr(ws_ml) if plan.n_partials else None,
-        _stream(stream),
+        _v_dtype(v_cache), _stream(stream),
     )
     _lib.check(st, "optimus_paged_attn")
     return out

@@ -31,7 +31,7 @@ def _bf16(rng, shape, scale=1.0):
 
 
 def _step(seed, n_req, chunk, block, page, hq, hkv, d, rule="in_block", prompt_range=(1, 300),
-          out_range=(2, 200), fixed_prompt=None):
+          out_range=(2, 200), fixed_prompt=None, v_dtype=torch.float16):
     rng = np.random.default_rng(seed)
     reqs = make_requests(seed, n_req, prompt_range, out_range, chunk, block, rule, fixed_prompt=fixed_prompt)
     plans = pe.plan_batch(reqs, chunk, block, rule)
@@ -40,7 +40,7 @@ def _step(seed, n_req, chunk, block, page, hq, hkv, d, rule="in_block", prompt_r
     dev = torch.device("cuda")
     dm = DeviceMeta.upload(meta, dev)
     k_cache = _bf16(rng, (num_pages, hkv, page, d))
-    v_cache = _bf16(rng, (num_pages, hkv, page, d))
+    v_cache = _bf16(rng, (num_pages, hkv, page, d)).to(v_dtype)
     n_tok = meta.n_tok
     q = _bf16(rng, (max(n_tok, 1), hq, d))
     k_new = _bf16(rng, (max(n_tok, 1), hkv, d))
@@ -60,18 +60,21 @@ def _run_append(s):
     return kc, vc, slots
 
 
+@pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("page,d,hkv", [(16, 128, 8), (64, 128, 2), (16, 64, 4), (32, 64, 2)])
-def test_kv_append_bit_exact(page, d, hkv):
-    s = _step(1, 9, 8, 32, page, hkv * 2, hkv, d)
+def test_kv_append_bit_exact(page, d, hkv, v_dtype):
+    s = _step(1, 9, 8, 32, page, hkv * 2, hkv, d, v_dtype=v_dtype)
+    # include values outside the fp16 range: the fp16 V cache saturates them
+    s["v_new"][0, 0, :4] = torch.tensor([1e6, -1e6, 70000.0, 3.0e-8], dtype=torch.bfloat16)
     kc, vc, slots = _run_append(s)
     torch.cuda.synchronize()
     m = s["meta"]
-    ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.bt if hasattr(m, "bt") else m.block_tables, page)
+    ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.block_tables, page)
     assert np.array_equal(slots.cpu().numpy()[: m.n_tok], ref_slots)
     k_ref = s["k_cache"].view(torch.int16).numpy().copy()
     v_ref = s["v_cache"].view(torch.int16).numpy().copy()
-    on.kv_append(k_ref, v_ref, s["k_new"].view(torch.int16).numpy()[: m.n_tok],
-                 s["v_new"].view(torch.int16).numpy()[: m.n_tok], ref_slots, page)
+    v_rows = on.v_storage(s["v_new"].float().numpy()[: m.n_tok], "fp16" if v_dtype == torch.float16 else "bf16")
+    on.kv_append(k_ref, v_ref, s["k_new"].view(torch.int16).numpy()[: m.n_tok], v_rows, ref_slots, page)
     assert np.array_equal(kc.cpu().view(torch.int16).numpy(), k_ref)
     assert np.array_equal(vc.cpu().view(torch.int16).numpy(), v_ref)
 
@@ -116,9 +119,10 @@ def test_paged_attention_sdar8b_shape(chunk):
     assert err <= ATTN_RTOL, err
 
 
+@pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("page,d,hq,hkv", [(64, 128, 32, 8), (16, 64, 4, 4), (16, 64, 4, 2), (32, 128, 32, 4), (128, 128, 8, 8)])
-def test_paged_attention_shapes(page, d, hq, hkv):
-    s = _step(3 + page + hq, 11, 8, 32, page, hq, hkv, d)
+def test_paged_attention_shapes(page, d, hq, hkv, v_dtype):
+    s = _step(3 + page + hq, 11, 8, 32, page, hq, hkv, d, v_dtype=v_dtype)
     plan, err, got, ref = _attn_check(s)
     assert err <= ATTN_RTOL, err
 

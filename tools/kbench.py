@@ -79,22 +79,24 @@ print(f"K1 per launch: {t_k1/L*1e3:.2f} us -> {k1b/(t_k1/L*1e-3)/1e9:.0f} GB/s ;
 
 # ---- timeline trace of one K2 launch
 from paper_2605_24832_b200 import _lib
-tr = torch.zeros((plan.grid, 1024), dtype=torch.int64, device=dev)
+tr = torch.zeros((plan.grid, 2048), dtype=torch.int64, device=dev)
 _lib.call("optimus_set_attn_trace", tr.data_ptr())
 k2(0)
 torch.cuda.synchronize()
 _lib.call("optimus_set_attn_trace", None)
 t = tr.cpu().numpy().astype(np.float64)
 np.set_printoptions(linewidth=220, precision=0, suppress=True)
+R = lambda role: slice(role * 256, role * 256 + 256)
 for c in (0, 70):
-    c0 = t[c, 3 * 128 + 126]  # clock at setup done
-    n = int((t[c, 128:256] > 0).sum())
-    print(f"CTA {c}: tiles={n} (cycles since setup, /100)")
-    for role, name in [(4, "prod_top"), (0, "prod_kfree"), (5, "prod_Kissued"), (6, "prod_vfree"), (7, "prod_Vissued"), (1, "mma_S"), (2, "smx_Sready"), (3, "smx_Pdone")]:
-        v = t[c, role * 128: role * 128 + min(n, 30)]
+    c0 = t[c, 6 * 256 + 1]
+    n = int((t[c, R(1)] > 0).sum())
+    print(f"CTA {c}: tiles={n} (cycles since setup /100)")
+    for role, name in [(0, "prod_top"), (4, "prod_free"), (5, "prod_issued"), (1, "mma_S"), (2, "smx_Sready"), (3, "smx_Pdone")]:
+        v = t[c, role * 256: role * 256 + min(n, 30)]
         print(f"  {name:12s}", ((v - c0) / 100).round(0))
-    fin = t[c, 2 * 128 + 127]
-    print("  work finished at", (fin - c0) / 1e3, "kcycles")
+    print("  producer done / CTA done (kcycles):", (t[c, 6 * 256 + 2] - c0) / 1e3, (t[c, 6 * 256 + 3] - c0) / 1e3)
+done = (t[:, 6 * 256 + 3] - t[:, 6 * 256 + 1]) / 1e3
+print("CTA done kcycles pctl:", np.percentile(done, [0, 50, 90, 100]).round(1))
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 torch.cuda._sleep(int(1e8))
 e0.record(); k2(0); e1.record(); torch.cuda.synchronize()
