@@ -158,3 +158,26 @@ def peaked_logits(rng: np.random.Generator, n_rows: int, vocab: int, tokens, con
         lse = mx + np.log(np.exp(others - mx).sum())
         x[i, k] = np.float32(lse + np.log(t / (1.0 - t)))
     return x
+
+
+def unmask_partial_ref(logits_shard, vocab_offset: int = 0):
+    """Per-row {max, sum exp(x - max), argmax + offset} of one vocabulary shard
+    (the record the unmask partials kernel writes; float64 here)."""
+    x = np.asarray(logits_shard, dtype=np.float64)
+    m = x.max(axis=1)
+    s = np.exp(x - m[:, None]).sum(axis=1)
+    idx = np.argmax(x, axis=1) + vocab_offset
+    return m, s, idx
+
+
+def unmask_merge_ref(parts):
+    """Merge shard records in the given (fixed) order: larger max wins, ties keep
+    the lower index; sums are rescaled to the merged max."""
+    M, S, I = [np.array(a, copy=True) for a in parts[0]]
+    for m2, s2, i2 in parts[1:]:
+        take = (m2 > M) | ((m2 == M) & (i2 < I))
+        newM = np.maximum(M, m2)
+        S = S * np.exp(M - newM) + s2 * np.exp(m2 - newM)
+        I = np.where(take, i2, I)
+        M = newM
+    return M, S, I

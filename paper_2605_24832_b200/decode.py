@@ -157,6 +157,8 @@ class StreamingDecoder:
         self.h2d_bytes += plan.work_host.nbytes + plan.cta_off_host.nbytes + plan.groups_host.nbytes
         dm.__dict__["attn_plan"] = plan
         dm.__dict__["slots"] = rows
+        dm.__dict__["requests"] = requests
+        dm.__dict__["plans"] = plans
         self.last_meta = dm
         self.last_plan = plan
         return dm

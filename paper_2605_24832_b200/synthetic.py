@@ -179,3 +179,61 @@ class SyntheticForward(Forward):
 
     def next_version(self):
         self.version = (self.version + 1) % self.n_versions
+
+
+class OracleDrivenForward(Forward):
+    """Stand-in model whose logits encode the reference's commit draw.
+
+    For every request with a non-empty window it consumes the request's rng exactly
+    like ``commit_step`` (commit.py:104-111: ``rng.random(n - 1)`` when n > 1) and
+    synthesizes each window row's logits with max-softmax confidence 0.97 (rank 0,
+    and rank j >= 1 when u_j < min(1, m q^j)) or 0.80 otherwise.  With tau = 0.9 the
+    B200 unmask kernel must then reproduce StochasticOracle's commit sets exactly,
+    which makes the whole device step comparable with the reference schedule.
+    """
+
+    def __init__(self, cfg: DecodeConfig, max_tokens: int, q: float, device="cuda", seed: int = 0,
+                 conf_commit: float = 0.97, conf_hold: float = 0.80):
+        self.cfg = cfg
+        self.q = q
+        self.device = torch.device(device)
+        self.t_hi, self.t_lo = conf_commit, conf_hold
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        H = cfg.num_q_heads + 2 * cfg.num_kv_heads
+        self.qkv_buf = [torch.randn((max_tokens, H, cfg.head_dim), generator=g, device=self.device,
+                                    dtype=torch.float32).to(torch.bfloat16) for _ in range(cfg.num_layers)]
+        self.gen = torch.Generator(device=self.device)
+        self.gen.manual_seed(seed + 1)
+        self.tok_rng = np.random.default_rng(seed + 2)
+
+    def qkv(self, layer: int, dm: DeviceMeta):
+        n = max(dm.host.n_tok, 1)
+        buf = self.qkv_buf[layer][:n]
+        hq, hkv = self.cfg.num_q_heads, self.cfg.num_kv_heads
+        return buf[:, :hq], buf[:, hq:hq + hkv], buf[:, hq + hkv:]
+
+    def logits(self, dm: DeviceMeta):
+        reqs = dm.__dict__["requests"]
+        plans = dm.__dict__["plans"]
+        confs = []
+        for req, plan in zip(reqs, plans):
+            n = len(plan.window)
+            if n == 0:
+                continue
+            m = float(getattr(req, "rate_multiplier", 1.0))
+            dec = [True]
+            if n > 1:
+                u = req.rng.random(n - 1)
+                dec += [bool(uj < min(1.0, m * self.q ** j)) for j, uj in enumerate(u, start=1)]
+            confs += [self.t_hi if d else self.t_lo for d in dec]
+        n_rows = len(confs)
+        V = self.cfg.vocab
+        x = torch.randn((max(n_rows, 1), V), generator=self.gen, device=self.device, dtype=torch.float32)
+        if n_rows:
+            tok = torch.as_tensor(self.tok_rng.integers(0, V, n_rows), device=self.device)
+            x.scatter_(1, tok[:, None], -float("inf"))
+            lse = torch.logsumexp(x, dim=1)
+            c = torch.as_tensor(confs, device=self.device, dtype=torch.float32)
+            x.scatter_(1, tok[:, None], (lse + torch.log(c / (1 - c)))[:, None])
+        return x.to(self.cfg.logits_dtype), None
