@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(o_empty);
     }
   }
+  grid_dep_launch();
   if (threadIdx.x == 256) trace(p, 6, 2);
   tc_fence_before();
   __syncthreads();
@@ -571,6 +572,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __rest
   const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= n_tok * group_sz) return;
+  grid_dep_wait();  // partials of the preceding attention grid are visible after this
   const float2* ml = reinterpret_cast<const float2*>(ws_ml);
   float mx = -INFINITY;
   for (int s = lane; s < n_split; s += 32) {
@@ -645,9 +647,22 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (n_groups > 0) {
-    attn_combine_kernel<HD><<<dim3(n_groups, kBlockM / 8), 256, 0, stream>>>(
-        groups, prm.ws_o, prm.ws_ml, prm.out, prm.out_stride_tok, prm.group);
-    cudaError_t e = cudaGetLastError();
+    // PDL: the combine's CTAs are resident before K2 drains; they wait on
+    // griddepcontrol.wait before reading the partials.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_groups, kBlockM / 8);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, attn_combine_kernel<HD>, groups,
+                                       static_cast<const float*>(prm.ws_o),
+                                       static_cast<const float*>(prm.ws_ml), prm.out,
+                                       prm.out_stride_tok, prm.group);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   return 0;
