@@ -133,6 +133,24 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total,
                        float* ws_o, float* ws_ml, int v_dtype, void* stream);
 
 /*
+ * Executor: K1 + K2 for n_layers layers in one call (per-layer device pointers in
+ * HOST arrays q[l], k_new[l], v_new[l], k_cache[l], v_cache[l], out[l]; metadata and
+ * work list shared).  Enqueues everything on `stream` and returns; used when the
+ * per-layer activations are already resident (no model work between the layers).
+ */
+int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k_new,
+                        const void* const* v_new, int64_t q_stride_tok, int64_t new_stride_tok,
+                        int n_tok_total, int n_tok, void* const* k_cache, void* const* v_cache,
+                        int64_t num_pages, const int32_t* tok_req, const int32_t* q_pos,
+                        const int32_t* prompt_len, const int32_t* vis_base,
+                        const int32_t* vis_off, const uint32_t* vis_words,
+                        const int32_t* block_tables, int max_pages, const int32_t* work,
+                        const int32_t* cta_off, int grid, const int32_t* groups, int n_groups,
+                        int block_size, int num_q_heads, int num_kv_heads, int head_dim,
+                        int page_size, float sm_scale, void* const* out, int64_t out_stride_tok,
+                        float* ws_o, float* ws_ml, int v_dtype, void* stream);
+
+/*
  * K3 — fused confidence-threshold unmask (replaces StochasticOracle.commits,
  * commit.py:279-280 -> commit_step commit.py:86-112, with the model rule
  * "commit tokens whose confidence exceeds the threshold"; tau=0.9
@@ -167,6 +185,30 @@ int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vs
                             uint8_t* commit_mask, int32_t* tok, float* conf,
                             const int32_t* row_pos, uint8_t* state, int32_t* token_buf,
                             int64_t state_stride, void* stream);
+
+/*
+ * Native host side of the batched step (host memory only; see csrc/host_step.cu).
+ * optimus_host_plan mirrors plan_chunk (engine.py:45-67) for every slot of the batch
+ * over packed per-slot state and emits the kernels' step metadata;
+ * optimus_host_apply mirrors apply_chunk + advance_blocks (engine.py:79-95,
+ * core.py:109-116) from the D2H commit mask.
+ */
+int optimus_host_plan(int n, const int32_t* slots, int chunk, int block, int window_rule,
+                      int8_t* states, int64_t state_stride, int32_t* queue, int qcap,
+                      int32_t* q_head, int32_t* q_len, int32_t* block_index,
+                      int32_t* cached_prefix, const int32_t* prompt, const int32_t* out_len,
+                      const int32_t* block_tables, int max_pages, int32_t* cu_seqlens,
+                      int32_t* tok_req, int32_t* tok_pos, int cap_tok, int32_t* prompt_len,
+                      int32_t* key_end, int32_t* vis_base, int32_t* vis_off,
+                      uint32_t* vis_words, int cap_words, int32_t* cu_rows, int32_t* row_tok,
+                      int32_t* row_pos, int32_t* row_req, int cap_rows,
+                      int32_t* block_tables_out, int32_t* counts_out);
+int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu_seqlens,
+                       const int32_t* tok_pos, const int32_t* cu_rows, const int32_t* row_pos,
+                       const uint8_t* commit_mask, int8_t* states, int64_t state_stride,
+                       int32_t* queue, int qcap, int32_t* q_head, int32_t* q_len,
+                       int32_t* block_index, int32_t* committed, int32_t* steps_taken,
+                       int32_t* cached_prefix, const int32_t* out_len, int32_t* commits_out);
 
 /* Recommended vocab split count for n_rows x vocab on the current device. */
 int optimus_unmask_splits(int n_rows, int vocab);

@@ -54,6 +54,17 @@ SIGNATURES = {
         [_vp, _i32, _i32, _i32, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     ),
     "optimus_unmask_splits": (_i32, [_i32, _i32]),
+    "optimus_attn_layers": (
+        _i32,
+        [_i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+         _vp, _i32, _vp, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64, _vp,
+         _vp, _i32, _vp],
+    ),
+    "optimus_host_plan": (_i32, [_i32, _vp, _i32, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
+                                 _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
+                                 _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "optimus_host_apply": (_i32, [_i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32,
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _LIB = None

@@ -259,34 +259,26 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     if (tiles > cap) s = std::min((tiles + cap - 1) / cap, std::max(1, tiles / min_split_tiles));
     return std::max(s, (tiles + hard_cap - 1) / hard_cap);
   };
+  // Pick the split granularity from a closed-form makespan estimate (LPT places
+  // items within max(largest item, mean load) + one item of slack), then run LPT
+  // once for the placement below.
   int best_cap = std::max(max_tiles, 1);
   double best_span = 1e300;
   const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16};
   for (int c : cands) {
-    int cap = std::max(min_split_tiles, (max_tiles + c - 1) / c);
-    std::vector<double> costs;
-    double sum = 0;
+    const int cap = std::max(min_split_tiles, (max_tiles + c - 1) / c);
+    double sum = 0, biggest = 0;
+    long long n_items = 0;
     for (const Unit& u : units) {
       const int s = split_count(u.tiles, cap);
-      const int base = u.tiles / s, rem = u.tiles % s;
-      for (int k = 0; k < s; ++k) {
-        const double cst = (base + (k < rem ? 1 : 0)) + kItem + (s > 1 ? kSplit : 0.0);
-        costs.push_back(cst);
-        sum += cst;
-      }
+      const double big = (u.tiles + s - 1) / s + kItem + (s > 1 ? kSplit : 0.0);
+      sum += u.tiles + s * (kItem + (s > 1 ? kSplit : 0.0));
+      biggest = std::max(biggest, big);
+      n_items += s;
     }
-    if (static_cast<long long>(costs.size()) > max_work) continue;
-    std::sort(costs.begin(), costs.end(), std::greater<double>());
-    std::priority_queue<double, std::vector<double>, std::greater<double>> heap;
-    for (int i = 0; i < grid; ++i) heap.push(0.0);
-    double span = 0;
-    for (double cst : costs) {
-      double l = heap.top();
-      heap.pop();
-      l += cst;
-      span = std::max(span, l);
-      heap.push(l);
-    }
+    if (n_items > max_work) continue;
+    const double mean = sum / grid;
+    const double span = std::max(biggest, mean + 0.5 * biggest);
     if (span < best_span - 1e-9) {
       best_span = span;
       best_cap = cap;
@@ -453,6 +445,33 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
   return cuda_status(launch_paged_attn(head_dim, v_dtype == 1, tq, tk, tv, prm, grid, groups,
                                        n_groups, static_cast<cudaStream_t>(stream)),
                      "paged_attn");
+}
+
+int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k_new,
+                        const void* const* v_new, int64_t q_stride_tok, int64_t new_stride_tok,
+                        int n_tok_total, int n_tok, void* const* k_cache, void* const* v_cache,
+                        int64_t num_pages, const int32_t* tok_req, const int32_t* q_pos,
+                        const int32_t* prompt_len, const int32_t* vis_base,
+                        const int32_t* vis_off, const uint32_t* vis_words,
+                        const int32_t* block_tables, int max_pages, const int32_t* work,
+                        const int32_t* cta_off, int grid, const int32_t* groups, int n_groups,
+                        int block_size, int hq, int hkv, int head_dim, int page_size,
+                        float sm_scale, void* const* out, int64_t out_stride_tok, float* ws_o,
+                        float* ws_ml, int v_dtype, void* stream) {
+  if (n_layers < 0 || !q || !k_new || !v_new || !k_cache || !v_cache || !out)
+    return fail("attn_layers: bad layer arrays");
+  for (int l = 0; l < n_layers; ++l) {
+    int st = optimus_kv_append(k_new[l], v_new[l], new_stride_tok, tok_req, q_pos, prompt_len,
+                               block_tables, max_pages, n_tok, hkv, head_dim, page_size,
+                               k_cache[l], v_cache[l], num_pages, nullptr, v_dtype, stream);
+    if (st) return st;
+    st = optimus_paged_attn(q[l], q_stride_tok, n_tok_total, k_cache[l], v_cache[l], num_pages, q_pos,
+                            prompt_len, vis_base, vis_off, vis_words, block_tables, max_pages, work,
+                            cta_off, grid, groups, n_groups, block_size, hq, hkv, head_dim,
+                            page_size, sm_scale, out[l], out_stride_tok, ws_o, ws_ml, v_dtype, stream);
+    if (st) return st;
+  }
+  return 0;
 }
 
 int optimus_unmask_splits(int n_rows, int vocab) {

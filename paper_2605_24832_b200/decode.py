@@ -60,6 +60,8 @@ class DecodeConfig:
     num_pages: int = 16384
     min_split_tiles: int = 4
     logits_dtype: torch.dtype = torch.bfloat16
+    max_output_tokens: int = 4096   # per-request capacity of the packed native state
+    max_chunk: int = 64
 
     def __post_init__(self):
         if self.num_q_heads % self.num_kv_heads:
@@ -113,6 +115,10 @@ class StreamingDecoder:
         self.d2h_bytes = 0
         # multi-GPU: a TensorParallelUnmask merges vocab-shard partials across ranks
         self.unmask_impl = None
+        # native (C++) batched host step over packed request state; the Python path
+        # (step_python) stays for foreign callers and as the readable specification
+        self.use_native = True
+        self._native = None
 
     # ------------------------------------------------------------------ admission
     def admit(self, request) -> int:
@@ -121,12 +127,23 @@ class StreamingDecoder:
         return self.tables.admit(request.id, request.prompt_tokens + first)
 
     def release(self, request) -> None:
-        self.tables.release(request.id)
+        if self._native is not None and getattr(request, "_bs", None) is self._native.bs:
+            self._native.release(request)
+        else:
+            self.tables.release(request.id)
 
     def release_all(self, requests) -> None:
         for r in requests:
             if self.tables.slot(r.id) is not None:
-                self.tables.release(r.id)
+                self.release(r)
+
+    def native(self):
+        if self._native is None:
+            from .native_step import NativeStepper
+
+            self._native = NativeStepper(self, max_out=self.cfg.max_output_tokens,
+                                         max_chunk=self.cfg.max_chunk)
+        return self._native
 
     def _ensure_pages(self, requests, plans) -> np.ndarray:
         rows = np.empty(len(requests), dtype=np.int64)
@@ -183,6 +200,11 @@ class StreamingDecoder:
         m = dm.host
         plan = dm.__dict__["attn_plan"]
         out = self._workspaces(plan, m.n_tok)
+        if getattr(self.forward, "resident_layers", False) and m.n_tok:
+            # activations already resident for every layer: one native call enqueues
+            # all K1/K2 launches (csrc/capi.cu optimus_attn_layers)
+            self._run_layers_native(dm, plan, out)
+            return
         self.forward.begin_step(dm)
         for layer in range(cfg.num_layers):
             q, k, v = self.forward.qkv(layer, dm)
@@ -193,6 +215,42 @@ class StreamingDecoder:
                                     dm.vis_words, dm.block_tables, plan, cfg.block_size,
                                     out=out[: m.n_tok], ws_o=self._ws_o, ws_ml=self._ws_ml)
             self.forward.post_attn(layer, out[: m.n_tok], dm)
+
+    def _run_layers_native(self, dm, plan, out) -> None:
+        import ctypes as C
+
+        from . import _lib
+
+        cfg = self.cfg
+        m = dm.host
+        L = cfg.num_layers
+        ptrs = self.__dict__.get("_layer_ptrs")
+        if ptrs is None:
+            q_l, k_l, v_l, kc_l, vc_l = [], [], [], [], []
+            for layer in range(L):
+                q, k, v = self.forward.qkv(layer, dm)
+                kc, vc = self.cache.layer(layer)
+                q_l.append(q.data_ptr()); k_l.append(k.data_ptr()); v_l.append(v.data_ptr())
+                kc_l.append(kc.data_ptr()); vc_l.append(vc.data_ptr())
+                strides = (q.stride(0), k.stride(0), self.forward.qkv_capacity)
+            arr = lambda xs: (C.c_void_p * L)(*xs)
+            ptrs = (arr(q_l), arr(k_l), arr(v_l), arr(kc_l), arr(vc_l), strides)
+            self._layer_ptrs = ptrs
+        q_a, k_a, v_a, kc_a, vc_a, (q_stride, kv_stride, cap) = ptrs
+        out_a = (C.c_void_p * L)(*([out.data_ptr()] * L))
+        kc0 = self.cache.k[0]
+        st = _lib.call(
+            "optimus_attn_layers", L, q_a, k_a, v_a, q_stride, kv_stride, cap, m.n_tok, kc_a, vc_a,
+            kc0.shape[0], dm.tok_req.data_ptr(), dm.tok_pos.data_ptr(), dm.prompt_len.data_ptr(),
+            dm.vis_base.data_ptr(), dm.vis_off.data_ptr(), dm.vis_words.data_ptr(),
+            dm.block_tables.data_ptr(), dm.block_tables.shape[1], plan.work.data_ptr(),
+            plan.cta_off.data_ptr(), plan.grid if plan.n_work else 0, plan.groups.data_ptr(),
+            plan.n_groups, cfg.block_size, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+            cfg.page_size, 1.0 / float(cfg.head_dim) ** 0.5, out_a, out.stride(0),
+            self._ws_o.data_ptr() if plan.n_partials else None,
+            self._ws_ml.data_ptr() if plan.n_partials else None,
+            ops._v_dtype(self.cache.v), torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "optimus_attn_layers")
 
     def run_unmask(self, dm: DeviceMeta) -> ops.UnmaskResult:
         m = dm.host
@@ -226,6 +284,15 @@ class StreamingDecoder:
     # ------------------------------------------------------------------ the call
     def step(self, requests: Sequence, chunk_size: int) -> list:
         """One streaming decode iteration for the whole batch (sim.py:269-305)."""
+        if self.use_native:
+            nat = self.native()
+            out = nat.step(requests, chunk_size)
+            self.h2d_bytes, self.d2h_bytes = nat.h2d_bytes, nat.d2h_bytes
+            return out
+        return self.step_python(requests, chunk_size)
+
+    def step_python(self, requests: Sequence, chunk_size: int) -> list:
+        """The same iteration with the host half in Python (plan_batch / apply_batch)."""
         cfg = self.cfg
         plans = plan_batch(requests, chunk_size, cfg.block_size, cfg.window_rule)
         dm = self.prepare(requests, plans)

@@ -1,0 +1,231 @@
+"""Native batched host step: plan, pack, launch, apply with no per-request Python.
+
+``NativeStepper.step(requests, chunk)`` is the same decode iteration as
+``StreamingDecoder.step_python`` (plan_batch -> build_step_meta -> device step ->
+apply_batch), but the control half runs in C++ over the packed ``BatchState``
+(csrc/host_step.cu: ``optimus_host_plan`` / ``optimus_host_apply``), the step
+metadata and the attention work list are written straight into one fixed-capacity
+pinned arena, and that arena goes to the device in ONE H2D copy.  The commit mask
+comes back in ONE D2H copy.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from types import SimpleNamespace
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .batch_state import BatchState
+from .core import rule_value
+from .engine import StepSummary
+from .errors import ConfigError
+
+
+class Arena:
+    """Fixed offsets for every per-step array in one pinned int32 buffer + device mirror."""
+
+    def __init__(self, device, caps: dict):
+        self.caps = dict(caps)
+        self.offs = {}
+        total = 0
+        for name, n in caps.items():
+            self.offs[name] = total
+            total += ((int(n) + 3) // 4) * 4  # 16-byte aligned fields
+        self.total = total
+        self.host_t = torch.empty(total, dtype=torch.int32, pin_memory=True)
+        self.host = self.host_t.numpy()
+        self.dev = torch.empty(total, dtype=torch.int32, device=device)
+
+    def h(self, name, n=None):
+        o = self.offs[name]
+        return self.host[o:o + (self.caps[name] if n is None else n)]
+
+    def d(self, name, n=None):
+        o = self.offs[name]
+        return self.dev[o:o + (self.caps[name] if n is None else n)]
+
+    def hptr(self, name):
+        return self.host.ctypes.data + 4 * self.offs[name]
+
+
+class NativeStepper:
+    def __init__(self, decoder, max_out: int = 4096, qcap: int = 512, max_chunk: int = 64):
+        cfg = decoder.cfg
+        self.dec = decoder
+        self.cfg = cfg
+        self.max_chunk = max_chunk
+        B = cfg.max_batch
+        self.bs = BatchState(B, max_out, qcap)
+        T = B * max_chunk
+        R = B * min(max_chunk, cfg.block_size)
+        W = B * (max_out // 32 + 4)
+        MP = cfg.max_pages_per_req
+        G = cfg.num_q_heads // cfg.num_kv_heads
+        mtiles = max(1, -(-max_chunk // max(1, 128 // G)))
+        self.max_work = B * cfg.num_kv_heads * mtiles * 8
+        self.max_groups = B * cfg.num_kv_heads * mtiles
+        self.grid = decoder.grid
+        # device-read fields first; the sparse tails (vis_words, work, groups) are
+        # uploaded up to their used length only
+        caps = dict(cu_seqlens=B + 1, tok_req=T, tok_pos=T, prompt_len=B, key_end=B, vis_base=B,
+                    vis_off=B + 1, cu_rows=B + 1, row_tok=R, row_pos=R, row_req=R, row_src=R,
+                    block_tables=B * MP, cta_off=self.grid + 1, vis_words=W,
+                    work=self.max_work * 8, groups=self.max_groups * 8, slots=B, counts=4, commits=B)
+        self.arena = Arena(decoder.device, caps)
+        self.mask_host = torch.empty(max(R, 1), dtype=torch.uint8, pin_memory=True)
+        self.lib = _lib.load()
+        self._view_cache = {}
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def _views(self, n: int) -> dict:
+        """Device views of the arena (capacity-sized; batch-sized where a kernel
+        reads the length from the shape), cached per batch size."""
+        v = self._view_cache.get(n)
+        if v is None:
+            A, MP = self.arena, self.cfg.max_pages_per_req
+            v = {k: A.d(k) for k in ("tok_req", "tok_pos", "prompt_len", "vis_base", "vis_off", "vis_words",
+                                     "row_pos", "row_src", "cta_off")}
+            v["work"] = A.d("work").view(-1, 8)
+            v["groups"] = A.d("groups").view(-1, 8)
+            v["block_tables"] = A.d("block_tables", n * MP).view(n, MP)
+            v["cu_rows"] = A.d("cu_rows", n + 1)
+            self._view_cache[n] = v
+        return v
+
+    # ------------------------------------------------------------------ admission
+    def _slot(self, req) -> int:
+        tables = self.dec.tables
+        s = tables.slot(req.id)
+        if s is None:
+            s = self.dec.admit(req)
+            self.bs.bind(req, s)
+        return s
+
+    def release(self, req) -> None:
+        s = self.dec.tables.slot(req.id)
+        if s is None:
+            return
+        self.bs.unbind(s)
+        self.dec.tables.release(req.id)
+
+    # ------------------------------------------------------------------ the step
+    def plan(self, requests, chunk: int):
+        cfg = self.cfg
+        if chunk > self.max_chunk:
+            raise ConfigError(f"chunk {chunk} > native stepper max_chunk {self.max_chunk}")
+        n = len(requests)
+        A = self.arena
+        slots = A.h("slots", n)
+        for i, req in enumerate(requests):
+            slots[i] = self._slot(req)
+        bs = self.bs
+        # pages for every position this step can touch (current block, +2 for OUT_BLOCK)
+        ahead = 3 if rule_value(cfg.window_rule) == "out_block" else 1
+        sl = slots.astype(np.int64)
+        reach = np.minimum(bs.out_len[sl], (bs.block_index[sl] + ahead) * cfg.block_size)
+        need = (bs.prompt[sl] + reach + cfg.page_size - 1) // cfg.page_size
+        tables = self.dec.tables
+        for i in np.flatnonzero(need > tables.n_pages[sl]):
+            tables.ensure(int(sl[i]), int(bs.prompt[sl[i]] + reach[i]))
+        MP = cfg.max_pages_per_req
+        L = self.lib
+        st = L.optimus_host_plan(
+            n, A.hptr("slots"), chunk, cfg.block_size, 0 if rule_value(cfg.window_rule) == "in_block" else 1,
+            bs.states.ctypes.data, bs.states.shape[1], bs.queue.ctypes.data, bs.qcap,
+            bs.q_head.ctypes.data, bs.q_len.ctypes.data, bs.block_index.ctypes.data,
+            bs.cached_prefix.ctypes.data, bs.prompt.ctypes.data, bs.out_len.ctypes.data,
+            tables.table.ctypes.data, MP, A.hptr("cu_seqlens"), A.hptr("tok_req"), A.hptr("tok_pos"),
+            A.caps["tok_pos"], A.hptr("prompt_len"), A.hptr("key_end"), A.hptr("vis_base"),
+            A.hptr("vis_off"), A.hptr("vis_words"), A.caps["vis_words"], A.hptr("cu_rows"),
+            A.hptr("row_tok"), A.hptr("row_pos"), A.hptr("row_req"), A.caps["row_pos"],
+            A.hptr("block_tables"), A.hptr("counts"))
+        _lib.check(st, "optimus_host_plan")
+        n_tok, n_rows, n_words = (int(x) for x in A.h("counts", 3))
+        # attention work list straight into the arena
+        ng, npart = C.c_int(0), C.c_int(0)
+        mw, mg = C.c_int(0), C.c_int(0)
+        _lib.check(L.optimus_attn_plan_bounds(n, A.hptr("cu_seqlens"), A.hptr("key_end"), cfg.num_q_heads,
+                                              cfg.num_kv_heads, cfg.min_split_tiles, cfg.page_size,
+                                              C.byref(mw), C.byref(mg)), "optimus_attn_plan_bounds")
+        if mw.value > self.max_work or mg.value > self.max_groups:
+            raise ConfigError(f"attention work list ({mw.value} items) exceeds the arena capacity "
+                              f"({self.max_work}); raise DecodeConfig.max_batch headroom")
+        nw = L.optimus_attn_plan(n, A.hptr("cu_seqlens"), A.hptr("key_end"), cfg.num_q_heads,
+                                 cfg.num_kv_heads, self.grid, cfg.min_split_tiles, cfg.page_size,
+                                 A.hptr("work"), self.max_work, A.hptr("cta_off"), A.hptr("groups"),
+                                 self.max_groups, C.byref(ng), C.byref(npart))
+        if nw < 0:
+            _lib.check(nw, "optimus_attn_plan")
+        host = SimpleNamespace(
+            n_req=n, n_tok=n_tok, n_rows=n_rows, cu_seqlens=A.h("cu_seqlens", n + 1),
+            cu_rows=A.h("cu_rows", n + 1), row_req=A.h("row_req", n_rows), row_pos=A.h("row_pos", n_rows),
+            row_tok=A.h("row_tok", n_rows), tok_pos=A.h("tok_pos", n_tok), key_end=A.h("key_end", n),
+            vis_base=A.h("vis_base", n), vis_off=A.h("vis_off", n + 1), vis_words=A.h("vis_words", n_words).view(np.uint32),
+            prompt_len=A.h("prompt_len", n), block_tables=A.h("block_tables", n * MP).reshape(n, MP))
+        V = self._views(n)
+        plan = ops.AttnPlan(self.grid, nw, ng.value, npart.value, V["work"], V["cta_off"], V["groups"],
+                            A.h("work", nw * 8).reshape(-1, 8), A.h("cta_off"), A.h("groups", ng.value * 8).reshape(-1, 8))
+        dm = SimpleNamespace(host=host, tok_req=V["tok_req"], tok_pos=V["tok_pos"],
+                             prompt_len=V["prompt_len"], vis_base=V["vis_base"], vis_off=V["vis_off"],
+                             vis_words=V["vis_words"], block_tables=V["block_tables"],
+                             cu_rows=V["cu_rows"], row_pos=V["row_pos"], row_src=V["row_src"])
+        dm.__dict__.update(attn_plan=plan, slots=slots.astype(np.int64), requests=requests, plans=None,
+                           row_src_host=A.h("row_src"))
+        return dm
+
+    def upload(self, dm) -> None:
+        A = self.arena
+        plan = dm.__dict__["attn_plan"]
+        n_words = int(A.h("counts", 3)[2])
+        spans = [(0, A.offs["vis_words"]), (A.offs["vis_words"], max(n_words, 1)),
+                 (A.offs["work"], max(plan.n_work, 1) * 8), (A.offs["groups"], max(plan.n_groups, 1) * 8)]
+        nbytes = 0
+        for o, n in spans:
+            A.dev[o:o + n].copy_(A.host_t[o:o + n], non_blocking=True)
+            nbytes += 4 * n
+        self.h2d_bytes = nbytes
+
+    def fetch_and_apply(self, dm, res) -> np.ndarray:
+        n, n_rows = dm.host.n_req, dm.host.n_rows
+        A = self.arena
+        if n_rows:
+            self.mask_host[:n_rows].copy_(res.commit_mask[:n_rows], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        self.d2h_bytes = n_rows
+        bs = self.bs
+        st = self.lib.optimus_host_apply(
+            n, A.hptr("slots"), self.cfg.block_size, A.hptr("cu_seqlens"), A.hptr("tok_pos"),
+            A.hptr("cu_rows"), A.hptr("row_pos"), self.mask_host.data_ptr(), bs.states.ctypes.data,
+            bs.states.shape[1], bs.queue.ctypes.data, bs.qcap, bs.q_head.ctypes.data, bs.q_len.ctypes.data,
+            bs.block_index.ctypes.data, bs.committed.ctypes.data, bs.steps_taken.ctypes.data,
+            bs.cached_prefix.ctypes.data, bs.out_len.ctypes.data, A.hptr("commits"))
+        _lib.check(st, "optimus_host_apply")
+        return A.h("commits", n)
+
+    def step(self, requests, chunk: int, summaries: bool = True):
+        dm = self.plan(requests, chunk)
+        if hasattr(self.dec.forward, "fill_row_src"):
+            self.dec.forward.fill_row_src(dm)
+        self.upload(dm)
+        res = self.dec.device_step(dm)
+        mask_rows = dm.host.n_rows
+        counts = self.fetch_and_apply(dm, res)
+        out = None
+        if summaries:
+            cu_t, cu_r = dm.host.cu_seqlens, dm.host.cu_rows
+            mask = self.mask_host.numpy()[:mask_rows].astype(bool)
+            pos = dm.host.row_pos
+            out = []
+            for r in range(dm.host.n_req):
+                a, b = int(cu_r[r]), int(cu_r[r + 1])
+                out.append(StepSummary(computed=int(cu_t[r + 1] - cu_t[r]),
+                                       commits=frozenset(pos[a:b][mask[a:b]].tolist())))
+        for req in requests:
+            if req.finished:
+                self.release(req)
+        return out if summaries else int(counts.sum())

@@ -106,6 +106,10 @@ class SyntheticForward(Forward):
         n_buf = cfg.num_layers if per_layer_qkv else 1
         self.qkv_buf = [torch.randn((max_tokens, H, cfg.head_dim), generator=g, device=self.device,
                                     dtype=torch.float32).to(torch.bfloat16) for _ in range(n_buf)]
+        # per-layer activations are resident: the decoder may enqueue every layer's
+        # K1/K2 in one native call (no model work between the layers)
+        self.resident_layers = True
+        self.qkv_capacity = max_tokens
         self.max_slots = max_slots
         self.rows_per_slot = cfg.block_size
         self.n_versions = n_versions
@@ -161,6 +165,13 @@ class SyntheticForward(Forward):
         base = self.version * self.max_slots * self.rows_per_slot
         return (base + slot * self.rows_per_slot + np.minimum(rank, self.rows_per_slot - 1)).astype(np.int32)
 
+    def fill_row_src(self, dm) -> None:
+        """Native path: write the logits-row map into the step arena before its H2D."""
+        src = self.row_src_host(dm, dm.__dict__.get("slots"))
+        dm.__dict__["row_src_host"][: src.size] = src
+        dm.__dict__["row_src_dev"] = dm.row_src[: max(src.size, 1)]
+        dm.__dict__["row_src_version"] = self.version
+
     def logits(self, dm: DeviceMeta):
         cached = dm.__dict__.get("row_src_dev")
         if cached is not None and dm.__dict__.get("row_src_version") == self.version:
@@ -203,6 +214,8 @@ class OracleDrivenForward(Forward):
         H = cfg.num_q_heads + 2 * cfg.num_kv_heads
         self.qkv_buf = [torch.randn((max_tokens, H, cfg.head_dim), generator=g, device=self.device,
                                     dtype=torch.float32).to(torch.bfloat16) for _ in range(cfg.num_layers)]
+        self.resident_layers = True
+        self.qkv_capacity = max_tokens
         self.gen = torch.Generator(device=self.device)
         self.gen.manual_seed(seed + 1)
         self.tok_rng = np.random.default_rng(seed + 2)
@@ -215,10 +228,10 @@ class OracleDrivenForward(Forward):
 
     def logits(self, dm: DeviceMeta):
         reqs = dm.__dict__["requests"]
-        plans = dm.__dict__["plans"]
+        cu_rows = dm.host.cu_rows
         confs = []
-        for req, plan in zip(reqs, plans):
-            n = len(plan.window)
+        for r, req in enumerate(reqs):
+            n = int(cu_rows[r + 1] - cu_rows[r])  # window rows of request r (ChunkPlan.window)
             if n == 0:
                 continue
             m = float(getattr(req, "rate_multiplier", 1.0))
