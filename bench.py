@@ -38,6 +38,28 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 SDAR8B = dict(num_layers=36, num_q_heads=32, num_kv_heads=8, head_dim=128, vocab=151936)
+# LLaDA2.0-16B-MoE-shaped attention (config 4): GQA 16/4, d=128, 20 layers, 157K vocab.
+# Model dims are not in /root/reference ([external, assumed]); BASELINE.json fixes the
+# 157K vocabulary, batch 128 and mixed per-request chunks.
+LLADA16B = dict(num_layers=20, num_q_heads=16, num_kv_heads=4, head_dim=128, vocab=157184)
+# commit profiles (calibrated_profile, tests/golden/commits.json and SURVEY §8d)
+Q_SHAREGPT_DENSE = 0.7758267092770552
+Q_LONGBENCH_DENSE = 0.835508
+Q_SHAREGPT_MOE = 0.6015936600147661
+
+
+def workload_spec(name):
+    from paper_2605_24832_b200.synthetic import LONGBENCH, SHAREGPT
+    return {
+        "sharegpt": dict(model=SDAR8B, batch=64, lengths=SHAREGPT, q=Q_SHAREGPT_DENSE, prompt=None, clip=None,
+                         mixed=None),
+        "ctx4096": dict(model=SDAR8B, batch=64, lengths=SHAREGPT, q=Q_SHAREGPT_DENSE, prompt=4096, clip=None,
+                        mixed=None),
+        "longbench": dict(model=SDAR8B, batch=64, lengths=LONGBENCH, q=Q_LONGBENCH_DENSE, prompt=None,
+                          clip=(4096, 16384), mixed=None),
+        "llada": dict(model=LLADA16B, batch=128, lengths=SHAREGPT, q=Q_SHAREGPT_MOE, prompt=None, clip=None,
+                      mixed=(8, 16, 24, 32)),
+    }[name]
 
 
 def parse():
@@ -47,13 +69,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--chunk", type=int, default=32)
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--page", type=int, default=64)
-    ap.add_argument("--workload", choices=["sharegpt", "ctx4096"], default="sharegpt")
+    ap.add_argument("--workload", choices=["sharegpt", "ctx4096", "longbench", "llada"], default="sharegpt")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.batch is None:
+        a.batch = workload_spec(a.workload)["batch"]
+    return a
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -113,13 +138,21 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- workload
-def workload_requests(args, seed_offset=0):
-    from paper_2605_24832_b200.synthetic import SHAREGPT, make_batch
-    if args.workload == "sharegpt":
-        return make_batch(args.seed + seed_offset, args.batch, args.chunk, lengths=SHAREGPT,
-                          first_id=seed_offset * 100000)
-    return make_batch(args.seed + seed_offset, args.batch, args.chunk, lengths=SHAREGPT,
-                      fixed_prompt=4096, first_id=seed_offset * 100000)
+def workload_requests(args, seed_offset=0, n=None):
+    from paper_2605_24832_b200.synthetic import make_batch
+    w = workload_spec(args.workload)
+    return make_batch(args.seed + seed_offset, n or args.batch, args.chunk, lengths=w["lengths"], q=w["q"],
+                      fixed_prompt=w["prompt"], prompt_clip=w["clip"], first_id=seed_offset * 100000)
+
+
+def step_chunks(args, reqs):
+    """One global chunk (the reference's FixedChunk/ElasticChunk iteration) or, for
+    the mixed-chunk workload, one seeded chunk per request from the elastic set."""
+    w = workload_spec(args.workload)
+    if not w["mixed"]:
+        return args.chunk
+    rng = np.random.default_rng(args.seed + 7)
+    return [int(c) for c in rng.choice(w["mixed"], len(reqs))]
 
 
 def pages_needed(reqs, page):
@@ -197,17 +230,18 @@ def run_reference(args):
     from paper_2605_24832_b200.decode import DecodeConfig
     from paper_2605_24832_b200.engine import plan_batch
     from paper_2605_24832_b200.meta import build_step_meta
-    cfg = DecodeConfig(**SDAR8B, page_size=args.page, max_batch=args.batch)
+    M = workload_spec(args.workload)["model"]
+    cfg = DecodeConfig(**M, page_size=args.page, max_batch=args.batch)
     reqs = workload_requests(args)
-    plans = plan_batch(reqs, args.chunk, cfg.block_size, cfg.window_rule)
+    plans = plan_batch(reqs, step_chunks(args, reqs), cfg.block_size, cfg.window_rule)
     bt = np.zeros((len(reqs), 1), dtype=np.int32)
     P = args.page
     maxp = max((r.prompt_tokens + r.output_tokens + P - 1) // P for r in reqs)
     bt = np.zeros((len(reqs), maxp), dtype=np.int32)
     m = build_step_meta(reqs, plans, cfg.block_size, bt)
     # commits per step as the device path would take them (same synthetic profile)
-    from paper_2605_24832_b200.synthetic import SHAREGPT_DENSE8B_Q
-    commits = sum(min(1, len(p.window)) + sum(SHAREGPT_DENSE8B_Q ** j for j in range(1, len(p.window))) for p in plans)
+    q = workload_spec(args.workload)["q"]
+    commits = sum(min(1, len(p.window)) + sum(q ** j for j in range(1, len(p.window))) for p in plans)
     times = []
     # each step: one layer (of 36) of K1+K2 for the whole batch + 1/36 of the unmask rows
     for i in range(args.warmup + args.steps):
@@ -222,8 +256,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": f"sdar8b-attn-unmask-{args.workload}", "batch": args.batch,
-                   "chunk": args.chunk, "layers": cfg.num_layers, "page_size": P},
+        "config": {"workload": workload_name(args), "batch": args.batch,
+                   "chunk": chunk_label(args), "layers": cfg.num_layers, "page_size": P},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                          "sample": "per step: K1+K2 of 1 of 36 layers for the whole batch + unmask of 1/36 "
                                    "of the window rows (numpy oracle), scaled x36"},
@@ -258,20 +292,28 @@ def main():
     from paper_2605_24832_b200.parallel import TensorParallelUnmask
     from paper_2605_24832_b200.synthetic import SyntheticForward
 
-    if SDAR8B["num_kv_heads"] % world:
-        sys.exit("world size must divide the 8 KV heads")
+    M = workload_spec(args.workload)["model"]
+    if M["num_kv_heads"] % world:
+        sys.exit(f"world size must divide the {M['num_kv_heads']} KV heads")
     reqs = workload_requests(args)
     P = args.page
-    e2e_pool = [workload_requests(args, seed_offset=k + 1) for k in range(2)]
+    long_ctx = args.workload in ("longbench", "ctx4096")
+    # closed-loop e2e: a second batch plus a spare pool for respawns (smaller for the
+    # long-context workloads so three batches of KV fit next to each other in HBM)
+    e2e_pool = [workload_requests(args, seed_offset=1),
+                workload_requests(args, seed_offset=2, n=16 if long_ctx else None)]
     n_pages = pages_needed(reqs, P) + sum(pages_needed(b, P) for b in e2e_pool) + 64
     maxp = max((r.prompt_tokens + r.output_tokens + P - 1) // P for b in [reqs] + e2e_pool for r in b) + 1
-    cfg = DecodeConfig(num_layers=SDAR8B["num_layers"], num_q_heads=SDAR8B["num_q_heads"] // world,
-                       num_kv_heads=SDAR8B["num_kv_heads"] // world, head_dim=SDAR8B["head_dim"],
-                       vocab=SDAR8B["vocab"], page_size=P, max_batch=args.batch,
+    cfg = DecodeConfig(num_layers=M["num_layers"], num_q_heads=M["num_q_heads"] // world,
+                       num_kv_heads=M["num_kv_heads"] // world, head_dim=M["head_dim"],
+                       vocab=M["vocab"], page_size=P, max_batch=args.batch,
                        num_pages=n_pages, max_pages_per_req=maxp)
     vshard = (rank * cfg.vocab // world, (rank + 1) * cfg.vocab // world)
-    max_tok = args.batch * max(args.chunk, 2)
-    fwd = SyntheticForward(cfg, max_tok, args.batch, device=dev, seed=args.seed, vocab_shard=vshard)
+    wl = workload_spec(args.workload)
+    max_chunk = max(wl["mixed"]) if wl["mixed"] else args.chunk
+    max_tok = args.batch * max(max_chunk, 2)
+    fwd = SyntheticForward(cfg, max_tok, args.batch, device=dev, seed=args.seed, vocab_shard=vshard,
+                           q=wl["q"])
     dec = StreamingDecoder(cfg, fwd, device=dev)
     if world > 1:
         dec.unmask_impl = TensorParallelUnmask(world, rank, vshard[0])
@@ -282,7 +324,7 @@ def main():
         dec.cache.k[l].normal_(generator=g)
         dec.cache.v[l].normal_(generator=g)
 
-    plans = plan_batch(reqs, args.chunk, cfg.block_size, cfg.window_rule)
+    plans = plan_batch(reqs, step_chunks(args, reqs), cfg.block_size, cfg.window_rule)
     dm = dec.prepare(reqs, plans)
     res = dec.device_step(dm)  # warm + lazy init
     torch.cuda.synchronize()
@@ -377,9 +419,9 @@ def main():
         "metric": "decoded_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"sdar8b-attn-unmask-{args.workload}", "batch": args.batch,
-                   "chunk": args.chunk, "layers": cfg.num_layers, "q_heads": SDAR8B["num_q_heads"],
-                   "kv_heads": SDAR8B["num_kv_heads"], "head_dim": cfg.head_dim, "block": cfg.block_size,
+        "config": {"workload": workload_name(args), "batch": args.batch,
+                   "chunk": chunk_label(args), "layers": cfg.num_layers, "q_heads": M["num_q_heads"],
+                   "kv_heads": M["num_kv_heads"], "head_dim": cfg.head_dim, "block": cfg.block_size,
                    "page_size": P, "vocab": cfg.vocab, "tp": world,
                    "tokens_per_step": int(dm.host.n_tok), "window_rows": int(dm.host.n_rows),
                    "commits_per_step": commits_per_step, "visible_keys": vis_keys,
@@ -431,7 +473,17 @@ def graph_time(fn, dev, reps=10):
 
 def cfg_full(args):
     from paper_2605_24832_b200.decode import DecodeConfig
-    return DecodeConfig(**SDAR8B, page_size=args.page, max_batch=args.batch)
+    return DecodeConfig(**workload_spec(args.workload)["model"], page_size=args.page, max_batch=args.batch)
+
+
+def workload_name(args):
+    base = "llada16b" if args.workload == "llada" else "sdar8b"
+    return f"{base}-attn-unmask-{args.workload}"
+
+
+def chunk_label(args):
+    w = workload_spec(args.workload)
+    return f"mixed{list(w['mixed'])}" if w["mixed"] else args.chunk
 
 
 def run_e2e(args, dec, fwd, pool, world, dev):
@@ -447,7 +499,7 @@ def run_e2e(args, dec, fwd, pool, world, dev):
 
     def one():
         nonlocal batch
-        summ = dec.step(batch, args.chunk)
+        summ = dec.step(batch, step_chunks(args, batch))
         fwd.next_version()
         done = [r for r in batch if r.finished]
         if done:

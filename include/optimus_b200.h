@@ -190,10 +190,12 @@ int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vs
  * Native host side of the batched step (host memory only; see csrc/host_step.cu).
  * optimus_host_plan mirrors plan_chunk (engine.py:45-67) for every slot of the batch
  * over packed per-slot state and emits the kernels' step metadata;
+ * chunk_per_req (optional, [n]) gives each request its own chunk size (mixed chunks).
  * optimus_host_apply mirrors apply_chunk + advance_blocks (engine.py:79-95,
  * core.py:109-116) from the D2H commit mask.
  */
-int optimus_host_plan(int n, const int32_t* slots, int chunk, int block, int window_rule,
+int optimus_host_plan(int n, const int32_t* slots, int chunk, const int32_t* chunk_per_req,
+                      int block, int window_rule,
                       int8_t* states, int64_t state_stride, int32_t* queue, int qcap,
                       int32_t* q_head, int32_t* q_len, int32_t* block_index,
                       int32_t* cached_prefix, const int32_t* prompt, const int32_t* out_len,

@@ -60,7 +60,7 @@ SIGNATURES = {
          _vp, _i32, _vp, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64, _vp,
          _vp, _i32, _vp],
     ),
-    "optimus_host_plan": (_i32, [_i32, _vp, _i32, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
+    "optimus_host_plan": (_i32, [_i32, _vp, _i32, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
     "optimus_host_apply": (_i32, [_i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32,

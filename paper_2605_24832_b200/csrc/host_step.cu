@@ -56,7 +56,8 @@ extern "C" {
 //   row_pos[cap_rows], row_req[cap_rows], block_tables_out[n][max_pages]
 //   (gathered from block_tables[slot][max_pages]).
 // counts_out[0..3) = {n_tok, n_rows, n_words}.  Returns 0 or OPTIMUS_EINVAL.
-int optimus_host_plan(int n, const int32_t* slots, int chunk, int block, int window_rule,
+int optimus_host_plan(int n, const int32_t* slots, int chunk, const int32_t* chunk_per_req,
+                      int block, int window_rule,
                       int8_t* states, int64_t state_stride, int32_t* queue, int qcap,
                       int32_t* q_head, int32_t* q_len, int32_t* block_index,
                       int32_t* cached_prefix, const int32_t* prompt, const int32_t* out_len,
@@ -66,7 +67,7 @@ int optimus_host_plan(int n, const int32_t* slots, int chunk, int block, int win
                       uint32_t* vis_words, int cap_words, int32_t* cu_rows, int32_t* row_tok,
                       int32_t* row_pos, int32_t* row_req, int cap_rows,
                       int32_t* block_tables_out, int32_t* counts_out) {
-  if (chunk < 2 || block < 1 || n < 0 || (window_rule != 0 && window_rule != 1)) return OPTIMUS_EINVAL;
+  if (block < 1 || n < 0 || (window_rule != 0 && window_rule != 1)) return OPTIMUS_EINVAL;
   Packed P{states, state_stride, queue, qcap, q_head, q_len, block_index,
            nullptr, nullptr, cached_prefix, prompt, out_len};
   int nt = 0, nr = 0, nw = 0;
@@ -77,14 +78,16 @@ int optimus_host_plan(int n, const int32_t* slots, int chunk, int block, int win
     const int s = slots[r];
     const int out = out_len[s];
     const int8_t* st = states + static_cast<int64_t>(s) * state_stride;
-    const int nkv = std::min(q_len[s], chunk);
-    if (nt + chunk > cap_tok) return OPTIMUS_EINVAL;
+    const int chunk_r = chunk_per_req ? chunk_per_req[r] : chunk;  // mixed chunks (elastic)
+    if (chunk_r < 2) return OPTIMUS_EINVAL;                        // ChunkTooSmall, engine.py:56
+    const int nkv = std::min(q_len[s], chunk_r);
+    if (nt + chunk_r > cap_tok) return OPTIMUS_EINVAL;
     const int t0 = nt;
     for (int i = 0; i < nkv; ++i) {
       tok_req[nt] = r;
       tok_pos[nt++] = qget(P, s, i);
     }
-    int room = chunk - nkv;
+    int room = chunk_r - nkv;
     const int r0 = nr;
     int lo = block_index[s] * block;
     int hi = std::min(lo + block, out);

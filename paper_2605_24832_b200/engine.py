@@ -114,13 +114,17 @@ def apply_chunk(request, plan: ChunkPlan, commits, block_size: int) -> StepSumma
     return StepSummary(computed=plan.computed, commits=frozenset(ordered))
 
 
-def plan_batch(requests, chunk_size: int, block_size: int, window_rule="in_block") -> list:
-    """``plan_chunk`` for every request of a batch (identical plans)."""
-    if chunk_size < 2:
-        raise ChunkTooSmall(f"chunk_size must be >= 2, got {chunk_size}")
+def plan_batch(requests, chunk_size, block_size: int, window_rule="in_block") -> list:
+    """``plan_chunk`` for every request of a batch (identical plans).
+
+    ``chunk_size`` is one size for the batch (the reference's global chunk,
+    sim.py:270-274) or a sequence with one size per request (mixed chunks)."""
+    sizes = list(chunk_size) if np.ndim(chunk_size) else [chunk_size] * len(requests)
+    if any(c < 2 for c in sizes):
+        raise ChunkTooSmall(f"chunk_size must be >= 2, got {min(sizes)}")
     in_block = rule_value(window_rule) == "in_block"
     plans = []
-    for req in requests:
+    for req, chunk_size in zip(requests, sizes):
         queue = req.uncached_queue
         n_kv = min(len(queue), chunk_size)
         kv = tuple(queue[i] for i in range(n_kv)) if n_kv else ()

@@ -74,13 +74,33 @@ class NativeStepper:
         caps = dict(cu_seqlens=B + 1, tok_req=T, tok_pos=T, prompt_len=B, key_end=B, vis_base=B,
                     vis_off=B + 1, cu_rows=B + 1, row_tok=R, row_pos=R, row_req=R, row_src=R,
                     block_tables=B * MP, cta_off=self.grid + 1, vis_words=W,
-                    work=self.max_work * 8, groups=self.max_groups * 8, slots=B, counts=4, commits=B)
+                    work=self.max_work * 8, groups=self.max_groups * 8, slots=B, counts=4, commits=B, chunks=B)
         self.arena = Arena(decoder.device, caps)
         self.mask_host = torch.empty(max(R, 1), dtype=torch.uint8, pin_memory=True)
         self.lib = _lib.load()
         self._view_cache = {}
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+
+    def _grow(self, max_work: int, max_groups: int) -> None:
+        """Re-lay the arena with room for a larger attention work list (long contexts
+        split into many key ranges).  Per-step fields are rebuilt every step, so
+        nothing needs copying; the host-side plan fields are re-planned below."""
+        old = self.arena
+        caps = dict(old.caps)
+        caps["work"] = max_work * 8
+        caps["groups"] = max_groups * 8
+        self.max_work, self.max_groups = max_work, max_groups
+        new = Arena(self.dec.device, caps)
+        # keep this step's already-planned prefix (everything before vis_words + counts)
+        new.host[: old.offs["vis_words"]] = old.host[: old.offs["vis_words"]]
+        nw = int(old.h("counts", 3)[2])
+        new.h("vis_words", nw)[:] = old.h("vis_words", nw)
+        new.h("slots")[:] = old.h("slots")
+        new.h("counts")[:] = old.h("counts")
+        new.h("chunks")[:] = old.h("chunks")
+        self.arena = new
+        self._view_cache = {}
 
     def _views(self, n: int) -> dict:
         """Device views of the arena (capacity-sized; batch-sized where a kernel
@@ -114,12 +134,20 @@ class NativeStepper:
         self.dec.tables.release(req.id)
 
     # ------------------------------------------------------------------ the step
-    def plan(self, requests, chunk: int):
+    def plan(self, requests, chunk):
+        """``chunk``: one chunk size for the batch, or one per request (mixed chunks)."""
         cfg = self.cfg
-        if chunk > self.max_chunk:
-            raise ConfigError(f"chunk {chunk} > native stepper max_chunk {self.max_chunk}")
         n = len(requests)
         A = self.arena
+        if np.ndim(chunk):
+            per = A.h("chunks", n)
+            per[:] = np.asarray(chunk, dtype=np.int32)
+            chunk_ptr, chunk0 = A.hptr("chunks"), 0
+            cmax = int(per.max()) if n else 0
+        else:
+            chunk_ptr, chunk0, cmax = None, int(chunk), int(chunk)
+        if cmax > self.max_chunk:
+            raise ConfigError(f"chunk {cmax} > native stepper max_chunk {self.max_chunk}")
         slots = A.h("slots", n)
         for i, req in enumerate(requests):
             slots[i] = self._slot(req)
@@ -135,7 +163,8 @@ class NativeStepper:
         MP = cfg.max_pages_per_req
         L = self.lib
         st = L.optimus_host_plan(
-            n, A.hptr("slots"), chunk, cfg.block_size, 0 if rule_value(cfg.window_rule) == "in_block" else 1,
+            n, A.hptr("slots"), chunk0, chunk_ptr, cfg.block_size,
+            0 if rule_value(cfg.window_rule) == "in_block" else 1,
             bs.states.ctypes.data, bs.states.shape[1], bs.queue.ctypes.data, bs.qcap,
             bs.q_head.ctypes.data, bs.q_len.ctypes.data, bs.block_index.ctypes.data,
             bs.cached_prefix.ctypes.data, bs.prompt.ctypes.data, bs.out_len.ctypes.data,
@@ -153,8 +182,8 @@ class NativeStepper:
                                               cfg.num_kv_heads, cfg.min_split_tiles, cfg.page_size,
                                               C.byref(mw), C.byref(mg)), "optimus_attn_plan_bounds")
         if mw.value > self.max_work or mg.value > self.max_groups:
-            raise ConfigError(f"attention work list ({mw.value} items) exceeds the arena capacity "
-                              f"({self.max_work}); raise DecodeConfig.max_batch headroom")
+            self._grow(max(mw.value, self.max_work), max(mg.value, self.max_groups))
+            A = self.arena
         nw = L.optimus_attn_plan(n, A.hptr("cu_seqlens"), A.hptr("key_end"), cfg.num_q_heads,
                                  cfg.num_kv_heads, self.grid, cfg.min_split_tiles, cfg.page_size,
                                  A.hptr("work"), self.max_work, A.hptr("cta_off"), A.hptr("groups"),

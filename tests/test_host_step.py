@@ -25,7 +25,9 @@ def _native_plan(bs, slots, chunk, block, rule, tables, caps=4096):
     counts = np.zeros(4, np.int32)
     L = _lib.load()
     st = L.optimus_host_plan(
-        n, sl.ctypes.data, chunk, block, 0 if rule == "in_block" else 1,
+        n, sl.ctypes.data, chunk if np.ndim(chunk) == 0 else 0,
+        None if np.ndim(chunk) == 0 else np.ascontiguousarray(chunk, dtype=np.int32).ctypes.data,
+        block, 0 if rule == "in_block" else 1,
         bs.states.ctypes.data, bs.states.shape[1], bs.queue.ctypes.data, bs.qcap,
         bs.q_head.ctypes.data, bs.q_len.ctypes.data, bs.block_index.ctypes.data,
         bs.cached_prefix.ctypes.data, bs.prompt.ctypes.data, bs.out_len.ctypes.data,
@@ -54,10 +56,10 @@ def _native_apply(bs, slots, block, out, mask):
 
 
 @pytest.mark.parametrize("rule,chunk,block", [("in_block", 8, 32), ("in_block", 32, 32), ("out_block", 8, 16),
-                                              ("in_block", 2, 8), ("out_block", 16, 8)])
+                                              ("in_block", 2, 8), ("out_block", 16, 8), ("in_block", "mixed", 32)])
 def test_native_plan_and_apply_match_python_over_whole_decodes(rule, chunk, block):
-    rng = np.random.default_rng(chunk + block)
-    ref = make_requests(11 + chunk, 10, (1, 200), (3, 120), chunk, block, rule)
+    rng = np.random.default_rng(block + (7 if chunk == "mixed" else chunk))
+    ref = make_requests(11 + block, 10, (1, 200), (3, 120), 8, block, rule)
     nat = copy.deepcopy(ref)
     bs = BatchState(16, 256, qcap=64)
     for i, r in enumerate(nat):
@@ -67,9 +69,10 @@ def test_native_plan_and_apply_match_python_over_whole_decodes(rule, chunk, bloc
     while not all(r.finished for r in ref):
         idx = [i for i, r in enumerate(ref) if not r.finished]
         batch_ref = [ref[i] for i in idx]
-        plans = pe.plan_batch(batch_ref, chunk, block, rule)
+        c = rng.choice([2, 4, 8, 16, 24, 32], len(idx)) if chunk == "mixed" else chunk
+        plans = pe.plan_batch(batch_ref, c, block, rule)
         meta = build_step_meta(batch_ref, plans, block, tables[idx])
-        out, counts = _native_plan(bs, idx, chunk, block, rule, tables)
+        out, counts = _native_plan(bs, idx, c, block, rule, tables)
         n_tok, n_rows, n_words = counts[:3]
         assert n_tok == meta.n_tok and n_rows == meta.n_rows
         for k in ("cu_seqlens", "prompt_len", "key_end", "vis_base", "vis_off", "cu_rows"):
