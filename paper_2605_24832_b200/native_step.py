@@ -77,6 +77,7 @@ class NativeStepper:
                     work=self.max_work * 8, groups=self.max_groups * 8, slots=B, counts=4, commits=B, chunks=B)
         self.arena = Arena(decoder.device, caps)
         self.mask_host = torch.empty(max(R, 1), dtype=torch.uint8, pin_memory=True)
+        self.tok_host = torch.empty(max(R, 1), dtype=torch.int32, pin_memory=True)
         self.lib = _lib.load()
         self._view_cache = {}
         self.h2d_bytes = 0
@@ -123,6 +124,7 @@ class NativeStepper:
         s = tables.slot(req.id)
         if s is None:
             s = self.dec.admit(req)
+        if self.bs._req.get(s) is not req:  # admitted elsewhere (e.g. prefill): bind now
             self.bs.bind(req, s)
         return s
 
@@ -222,10 +224,16 @@ class NativeStepper:
     def fetch_and_apply(self, dm, res) -> np.ndarray:
         n, n_rows = dm.host.n_req, dm.host.n_rows
         A = self.arena
+        fwd = self.dec.forward
+        want_tok = getattr(fwd, "needs_tokens", False)
         if n_rows:
             self.mask_host[:n_rows].copy_(res.commit_mask[:n_rows], non_blocking=True)
+            if want_tok:
+                self.tok_host[:n_rows].copy_(res.tokens[:n_rows], non_blocking=True)
             torch.cuda.current_stream().synchronize()
-        self.d2h_bytes = n_rows
+        self.d2h_bytes = n_rows * (5 if want_tok else 1)
+        if want_tok and n_rows:
+            fwd.on_commit(dm, self.mask_host.numpy()[:n_rows].astype(bool), self.tok_host.numpy()[:n_rows])
         bs = self.bs
         st = self.lib.optimus_host_apply(
             n, A.hptr("slots"), self.cfg.block_size, A.hptr("cu_seqlens"), A.hptr("tok_pos"),
