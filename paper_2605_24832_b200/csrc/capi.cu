@@ -236,8 +236,7 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     int req, head, tok_begin, n_tok, tiles;
   };
   std::vector<Unit> units;
-  long long total = 0;
-  int max_tiles = 0;
+  units.reserve(static_cast<size_t>(n_req) * hkv * 2);
   for (int r = 0; r < n_req; ++r) {
     const int nq = cu[r + 1] - cu[r];
     if (nq <= 0) continue;
@@ -246,122 +245,164 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     for (int h = 0; h < hkv; ++h)
       for (int t0 = 0; t0 < nq; t0 += T) {
         units.push_back({r, h, cu[r] + t0, std::min(T, nq - t0), nt});
-        total += nt;
-        max_tiles = std::max(max_tiles, nt);
       }
   }
-  // Cost model (in 64-key tile units): every item pays a fixed prologue/epilogue
-  // (Q load, O drain) and a split item also pays its partial write + combine read.
-  const double kItem = 2.0, kSplit = 3.0;
+  // Cost model (in 64-key tile units; a tile is ~1100 SM cycles in the steady
+  // state): every item pays a fixed prologue/epilogue (Q load, O drain, pipeline
+  // refill, measured ~2.5 tiles) and a cut item also pays its partial write and
+  // the combine read.
+  const double kItem = 2.5, kSplit = 1.5;
   const int hard_cap = item_tile_cap(page_size);
-  auto split_count = [&](int tiles, int cap) {
-    int s = 1;
-    if (tiles > cap) s = std::min((tiles + cap - 1) / cap, std::max(1, tiles / min_split_tiles));
-    return std::max(s, (tiles + hard_cap - 1) / hard_cap);
+  const int nu = static_cast<int>(units.size());
+  std::vector<int> order(nu);
+  for (int i = 0; i < nu; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return units[a].tiles > units[b].tiles; });
+  struct Piece {
+    int unit, t0, nt, cta;
   };
-  // Pick the split granularity from a closed-form makespan estimate (LPT places
-  // items within max(largest item, mean load) + one item of slack), then run LPT
-  // once for the placement below.
-  int best_cap = std::max(max_tiles, 1);
-  double best_span = 1e300;
-  const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16};
-  for (int c : cands) {
-    const int cap = std::max(min_split_tiles, (max_tiles + c - 1) / c);
-    double sum = 0, biggest = 0;
-    long long n_items = 0;
-    for (const Unit& u : units) {
-      const int s = split_count(u.tiles, cap);
-      const double big = (u.tiles + s - 1) / s + kItem + (s > 1 ? kSplit : 0.0);
-      sum += u.tiles + s * (kItem + (s > 1 ? kSplit : 0.0));
-      biggest = std::max(biggest, big);
-      n_items += s;
-    }
-    if (n_items > max_work) continue;
-    const double mean = sum / grid;
-    const double span = std::max(biggest, mean + 0.5 * biggest);
-    if (span < best_span - 1e-9) {
-      best_span = span;
-      best_cap = cap;
+
+  // ---- candidate A: whole units (cut only at the per-item page cap), placed
+  // longest-first on the least-loaded CTA.
+  std::vector<Piece> pa;
+  pa.reserve(nu + 16);
+  double span_a = 0;
+  {
+    typedef std::pair<double, int> LoadCta;
+    std::vector<LoadCta> heap;
+    heap.reserve(grid);
+    for (int c = 0; c < grid; ++c) heap.push_back(LoadCta(0.0, c));
+    auto cmp = [](const LoadCta& a, const LoadCta& b) { return a > b; };  // min-heap
+    for (int ui : order) {
+      const int tiles = units[ui].tiles;
+      const int sc = (tiles + hard_cap - 1) / hard_cap;
+      const int base = tiles / sc, rem = tiles % sc;
+      int t0 = 0;
+      for (int k = 0; k < sc; ++k) {
+        const int nt = base + (k < rem ? 1 : 0);
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        LoadCta& lc = heap.back();
+        pa.push_back({ui, t0, nt, lc.second});
+        lc.first += nt + kItem + (sc > 1 ? kSplit : 0.0);
+        span_a = std::max(span_a, lc.first);
+        std::push_heap(heap.begin(), heap.end(), cmp);
+        t0 += nt;
+      }
     }
   }
-  // Materialise items with the chosen cap.
-  struct Item {
-    int req, head, tok_begin, n_tok, key_begin, key_end, slot;
-    double cost;
-  };
-  std::vector<Item> items;
+
+  // ---- candidate B: LPT with cutting.  Pieces are placed largest first on the
+  // least-loaded CTA; a piece that would push that CTA past the balanced budget
+  // (mean load + one item) is cut to fit and its remainder re-queued, so only the
+  // units that do not pack are split, and each only as far as needed.
+  std::vector<Piece> pb;
+  pb.reserve(nu + 2 * grid + 16);
+  double span_b = 0;
+  {
+    double total_cost = 0;
+    for (const Unit& u : units) total_cost += u.tiles + kItem;
+    const double budget = total_cost / grid + kItem;
+    typedef std::pair<double, int> LoadCta;
+    std::vector<LoadCta> heap;
+    heap.reserve(grid);
+    for (int c = 0; c < grid; ++c) heap.push_back(LoadCta(0.0, c));
+    auto cmin = [](const LoadCta& a, const LoadCta& b) { return a > b; };
+    struct Pend {
+      int tiles, unit, t0;
+      bool operator<(const Pend& o) const {  // max-heap on size, then unit order
+        return tiles != o.tiles ? tiles < o.tiles : (unit != o.unit ? unit > o.unit : t0 > o.t0);
+      }
+    };
+    std::vector<Pend> pend;
+    pend.reserve(nu + grid);
+    for (int ui = 0; ui < nu; ++ui) pend.push_back({units[ui].tiles, ui, 0});
+    std::make_heap(pend.begin(), pend.end());
+    std::vector<char> cut(nu, 0);
+    while (!pend.empty()) {
+      std::pop_heap(pend.begin(), pend.end());
+      Pend pc = pend.back();
+      pend.pop_back();
+      std::pop_heap(heap.begin(), heap.end(), cmin);
+      LoadCta& lc = heap.back();
+      int take = std::min(pc.tiles, hard_cap);
+      if (lc.first + take + kItem + (cut[pc.unit] ? kSplit : 0.0) > budget) {
+        const int fit = static_cast<int>(budget - lc.first - kItem - kSplit);
+        if (fit >= min_split_tiles && pc.tiles - fit >= min_split_tiles) take = std::min(fit, take);
+      }
+      if (take < pc.tiles) cut[pc.unit] = 1;
+      pb.push_back({pc.unit, pc.t0, take, lc.second});
+      lc.first += take + kItem + (cut[pc.unit] ? kSplit : 0.0);
+      std::push_heap(heap.begin(), heap.end(), cmin);
+      if (take < pc.tiles) {
+        pend.push_back({pc.tiles - take, pc.unit, pc.t0 + take});
+        std::push_heap(pend.begin(), pend.end());
+      }
+    }
+    // a unit's first piece was charged before it was known to be cut
+    std::vector<double> loads(grid, 0.0);
+    for (const Piece& pc : pb) loads[pc.cta] += pc.nt + kItem + (cut[pc.unit] ? kSplit : 0.0);
+    for (double l : loads) span_b = std::max(span_b, l);
+  }
+
+  // Prefer whole units unless cutting buys >3% of the makespan, net of the split
+  // combine launch it brings (~5 us ~ 7 tiles, measured).
+  const double kCombine = 7.0;
+  bool use_b = span_b + kCombine < 0.97 * span_a && static_cast<int>(pb.size()) <= max_work;
+  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE"))  // diagnostics: "whole" | "cut"
+    use_b = std::strcmp(f, "cut") == 0 && static_cast<int>(pb.size()) <= max_work;
+  const std::vector<Piece>& P = use_b ? pb : pa;
+  if (static_cast<int>(P.size()) > max_work) return fail("attn_plan: work buffer too small");
+  if (std::getenv("OPTIMUS_PLAN_DEBUG"))
+    std::fprintf(stderr, "attn_plan: whole-unit LPT span %.1f (%zu items), cutting LPT %.1f (%zu items) -> %s\n",
+                 span_a, pa.size(), span_b, pb.size(), use_b ? "cut" : "whole");
+  // Split groups: the pieces of a unit, in key order, get consecutive partial slots.
+  std::vector<int> byu(P.size());
+  for (size_t x = 0; x < P.size(); ++x) byu[x] = static_cast<int>(x);
+  std::sort(byu.begin(), byu.end(), [&](int a, int b) {
+    return P[a].unit != P[b].unit ? P[a].unit < P[b].unit : P[a].t0 < P[b].t0;
+  });
+  std::vector<int> slot(P.size(), -1);
   int n_groups = 0, n_partials = 0;
-  for (const Unit& u : units) {
-    const int s = split_count(u.tiles, best_cap);
-    const int base = u.tiles / s, rem = u.tiles % s;
-    const int kend = key_end[u.req];
-    int t0 = 0;
-    if (s > 1) {
+  for (size_t i = 0; i < byu.size();) {
+    size_t k = i + 1;
+    while (k < byu.size() && P[byu[k]].unit == P[byu[i]].unit) ++k;
+    if (k - i > 1) {
       if (n_groups >= max_groups) return fail("attn_plan: groups buffer too small");
-      int32_t* g = groups + 8 * n_groups;
+      const Unit& u = units[P[byu[i]].unit];
+      int32_t* g = groups + 8 * n_groups++;
       g[0] = u.req;
       g[1] = u.head;
       g[2] = u.tok_begin;
       g[3] = u.n_tok;
       g[4] = n_partials;
-      g[5] = s;
+      g[5] = static_cast<int>(k - i);
       g[6] = 0;
       g[7] = 0;
-      ++n_groups;
+      for (size_t x = i; x < k; ++x) slot[byu[x]] = n_partials++;
     }
-    for (int k = 0; k < s; ++k) {
-      const int nt = base + (k < rem ? 1 : 0);
-      Item it;
-      it.req = u.req;
-      it.head = u.head;
-      it.tok_begin = u.tok_begin;
-      it.n_tok = u.n_tok;
-      it.key_begin = t0 * 64;
-      it.key_end = std::min(kend, (t0 + nt) * 64);
-      it.slot = s > 1 ? n_partials++ : -1;
-      it.cost = nt + kItem + (s > 1 ? kSplit : 0.0);
-      items.push_back(it);
-      t0 += nt;
-    }
+    i = k;
   }
-  if (static_cast<int>(items.size()) > max_work) return fail("attn_plan: work buffer too small");
-  // Longest-processing-time-first assignment to persistent CTAs.
-  std::vector<int> order(items.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return items[a].cost > items[b].cost; });
-  typedef std::pair<double, int> LoadCta;
-  std::priority_queue<LoadCta, std::vector<LoadCta>, std::greater<LoadCta>> heap;
-  for (int i = 0; i < grid; ++i) heap.push(LoadCta(0.0, i));
-  std::vector<std::vector<int>> per(grid);
-  for (int idx : order) {
-    LoadCta lc = heap.top();
-    heap.pop();
-    per[lc.second].push_back(idx);
-    lc.first += items[idx].cost;
-    heap.push(lc);
+  // Work list in CTA order (stable: a CTA runs its pieces in placement order).
+  std::vector<int> cnt(grid + 1, 0);
+  for (const Piece& pc : P) ++cnt[pc.cta + 1];
+  for (int c = 0; c < grid; ++c) cnt[c + 1] += cnt[c];
+  for (int c = 0; c <= grid; ++c) cta_off[c] = cnt[c];
+  for (size_t x = 0; x < P.size(); ++x) {
+    const Piece& pc = P[x];
+    const Unit& u = units[pc.unit];
+    int32_t* w = work + 8 * cnt[pc.cta]++;
+    w[0] = u.req;
+    w[1] = u.head;
+    w[2] = u.tok_begin;
+    w[3] = u.n_tok;
+    w[4] = pc.t0 * 64;
+    w[5] = std::min(key_end[u.req], (pc.t0 + pc.nt) * 64);
+    w[6] = slot[x];
+    w[7] = 0;
   }
-  int pos = 0;
-  for (int c = 0; c < grid; ++c) {
-    cta_off[c] = pos;
-    for (int idx : per[c]) {
-      const Item& it = items[idx];
-      int32_t* w = work + 8 * pos;
-      w[0] = it.req;
-      w[1] = it.head;
-      w[2] = it.tok_begin;
-      w[3] = it.n_tok;
-      w[4] = it.key_begin;
-      w[5] = it.key_end;
-      w[6] = it.slot;
-      w[7] = 0;
-      ++pos;
-    }
-  }
-  cta_off[grid] = pos;
   *n_groups_out = n_groups;
   *n_partials_out = n_partials;
-  return pos;
+  return static_cast<int>(P.size());
 }
 
 int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, const void* k_cache,

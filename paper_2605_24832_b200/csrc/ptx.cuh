@@ -197,6 +197,20 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync).  Issue tcgen05.mma / TMA from the lane
+// this returns while the whole warp computes the (warp-uniform) operands, so they
+// live in uniform registers: from a lane-divergent region the compiler has to
+// funnel every operand through an R2UR waterfall loop, ~100 cycles per instruction.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: wait until the preceding grid's memory is visible /
 // allow the next grid to start its prologue.

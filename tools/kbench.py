@@ -17,6 +17,9 @@ ap.add_argument("--page", type=int, default=64)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--layers", type=int, default=36)
 ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--dump", default="")
+ap.add_argument("--ab", action="store_true")
+ap.add_argument("--dbgs", default="0,16")
 a = ap.parse_args()
 a.steps = 1
 dev = torch.device("cuda")
@@ -68,6 +71,52 @@ def timed(fn, reps=10, label=""):
     return ms
 
 L = cfg.num_layers
+if a.ab:
+    # A/B in one process, interleaved rounds (power capping drifts the clocks):
+    # planner choice x epilogue overlap
+    import os
+    from paper_2605_24832_b200 import _lib
+    variants = []
+    for force in ("whole", "cut"):
+        os.environ["OPTIMUS_PLAN_FORCE"] = force
+        pl = ops.plan_attention(m.cu_seqlens, m.key_end, cfg.num_q_heads, cfg.num_kv_heads, grid=dec.grid,
+                                min_split_tiles=cfg.min_split_tiles, device=dev, page_size=cfg.page_size)
+        for dbg in a.dbgs.split(","):
+            variants.append((f"plan={force} dbg={dbg} groups={pl.n_groups}", pl, dbg))
+    os.environ.pop("OPTIMUS_PLAN_FORCE")
+    graphs = []
+    for name, pl, dbg in variants:
+        os.environ["OPTIMUS_DBG"] = dbg
+        plan = pl
+        out = dec._workspaces(pl, m.n_tok)
+        s_ = torch.cuda.Stream(); s_.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s_):
+            k2(0); s_.synchronize()
+            with torch.cuda.graph(g, stream=s_):
+                for l in range(L):
+                    k2(l)
+        torch.cuda.synchronize()
+        # per-variant CTA timeline (clock64 cycles)
+        tr = torch.zeros((pl.grid, 4096), dtype=torch.int64, device=dev)
+        _lib.call("optimus_set_attn_trace", tr.data_ptr()); k2(0); torch.cuda.synchronize()
+        _lib.call("optimus_set_attn_trace", None)
+        t = tr.cpu().numpy().astype(np.float64)
+        done = (t[:, 6 * 256 + 3] - t[:, 6 * 256 + 1]) / 1e3
+        ghz = np.median((t[:, 6 * 256 + 3] - t[:, 6 * 256 + 1]) / (t[:, 6 * 256 + 4] - t[:, 6 * 256 + 0]))
+        print(f"{name}: SM clock during the traced launch ~{ghz:.2f} GHz (cycles/ns, setup excluded)")
+        graphs.append((name, g, np.percentile(done, [0, 50, 90, 100]).round(1)))
+    os.environ.pop("OPTIMUS_DBG")
+    res = {name: [] for name, _, _ in graphs}
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    for rnd in range(12):
+        for name, g, _ in graphs:
+            e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+            res[name].append(e0.elapsed_time(e1) * 1e3 / L)
+    for name, g, done in graphs:
+        v = np.array(res[name][2:])
+        print(f"{name:40s} K2 us/launch median {np.median(v):7.1f} min {v.min():7.1f}  CTA kcycles {done}")
+    sys.exit(0)
 t_k2_same = timed(lambda: [k2(0) for _ in range(L)], label="K2 x L same layer")
 t_k2 = timed(lambda: [k2(l) for l in range(L)], label="K2 x L layers")
 t_k1 = timed(lambda: [k1(l) for l in range(L)], label="K1 x L layers")
@@ -79,20 +128,27 @@ print(f"K1 per launch: {t_k1/L*1e3:.2f} us -> {k1b/(t_k1/L*1e-3)/1e9:.0f} GB/s ;
 
 # ---- timeline trace of one K2 launch
 from paper_2605_24832_b200 import _lib
-tr = torch.zeros((plan.grid, 2048), dtype=torch.int64, device=dev)
+tr = torch.zeros((plan.grid, 4096), dtype=torch.int64, device=dev)
 _lib.call("optimus_set_attn_trace", tr.data_ptr())
 k2(0)
 torch.cuda.synchronize()
 _lib.call("optimus_set_attn_trace", None)
 t = tr.cpu().numpy().astype(np.float64)
+if a.dump:
+    np.save(a.dump, t)
+    np.save(a.dump.replace(".npy", "_work.npy"), plan.work.cpu().numpy())
+    np.save(a.dump.replace(".npy", "_ctaoff.npy"), plan.cta_off.cpu().numpy())
 np.set_printoptions(linewidth=220, precision=0, suppress=True)
 R = lambda role: slice(role * 256, role * 256 + 256)
 for c in (0, 70):
     c0 = t[c, 6 * 256 + 1]
     n = int((t[c, R(1)] > 0).sum())
     print(f"CTA {c}: tiles={n} (cycles since setup /100)")
-    for role, name in [(0, "prod_top"), (4, "prod_free"), (5, "prod_issued"), (1, "mma_S"), (2, "smx_Sready"), (3, "smx_Pdone")]:
-        v = t[c, role * 256: role * 256 + min(n, 30)]
+    for role, name in [(0, "prod_top"), (4, "prod_free"), (5, "prod_issued"), (10, "vprod_free"), (11, "vprod_issued"),
+                       (12, "mma_reachS"), (1, "mma_S"), (8, "mma_reachPV"), (9, "mma_Vlanded"), (7, "mma_PV"),
+                       (2, "smx_Sready"), (3, "smx_Pdone")]:
+        a0 = 20 if role in (2, 3) else 40  # softmax stamps are warpgroup 0's (every other tile)
+        v = t[c, role * 256 + a0: role * 256 + a0 + 16]
         print(f"  {name:12s}", ((v - c0) / 100).round(0))
     print("  producer done / CTA done (kcycles):", (t[c, 6 * 256 + 2] - c0) / 1e3, (t[c, 6 * 256 + 3] - c0) / 1e3)
 done = (t[:, 6 * 256 + 3] - t[:, 6 * 256 + 1]) / 1e3

@@ -15,7 +15,12 @@
 #include "../paper_2605_24832_b200/csrc/ptx.cuh"
 using namespace optimus;
 
-constexpr int STAGES = 6;
+#ifndef STAGES
+#define STAGES 6
+#endif
+#ifndef HOLD
+#define HOLD 0
+#endif
 constexpr int TILE = 32768;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -67,6 +72,7 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ 
       const int st = t % STAGES;
       mbar_wait(&full[st], (t / STAGES) & 1);
       acc += *(volatile float*)(sm + st * TILE + lane * 4);
+      if (HOLD) { const long long t0 = clock64(); while (clock64() - t0 < HOLD) {} }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
