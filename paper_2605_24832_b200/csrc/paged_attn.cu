@@ -8,30 +8,32 @@
 // arrives as a per-request bitmap anchored at vis_base plus a per-query limit.
 //
 // How (sm_100a, one persistent CTA per SM, warp-specialised):
-//   warp 8   TMA producer (Q + K ring; warp 10 lane 0 drives the V ring): per work item one Q tile (the G query heads of a KV
-//            head folded into 128 MMA rows, row = token*G + head) and a ring of
-//            64-key K and V tiles gathered page by page through the block table
-//            (4-D tensor maps, SWIZZLE_128B boxes of 64 columns).  K and V slots
-//            have separate full/empty barriers: a K slot is refilled as soon as
-//            its S = Q K^T MMA retires, without waiting for the PV MMA.
-//   warp 9   MMA issuer (one thread): S = Q K^T into TMEM (double buffered),
-//            O += P V with P read from TMEM (double buffered O across work items).
-//   warp 10  TMEM allocator, then V producer.
+//   warp 8   TMA producer: per work item one Q tile (the G query heads of a KV head
+//            folded into 128 MMA rows, row = token*G + head) and the K ring of
+//            64-key tiles gathered page by page through the block table (4-D tensor
+//            maps, SWIZZLE_128B boxes of 64 columns).  warp 10: TMEM allocator,
+//            then the V ring.  K and V slots have separate full/empty barriers: a K
+//            slot is refilled as soon as its S = Q K^T retires.
+//   warp 9   MMA issuer: one stream of tiles across the CTA's work items.  The
+//            item's Q tile is copied smem -> TMEM (tcgen05.cp) and is the A operand
+//            of S = Q K^T (only K is read from shared memory); S goes to one of three
+//            rotating S/P buffers in TMEM, three tiles ahead of PV and across item
+//            boundaries; O += P V with P read from TMEM (TS-MMA).
 //   warp 11  metadata: stages the next work item's page ids / limits in smem.
-//   (control roles sit on the HIGH warp ids: the SMSP issue arbiter favours the
-//   highest warp id, so the softmax warps must not starve them.)
 //   warps 0-7  softmax + epilogue, two warpgroups ping-ponging over the tiles of
-//            a work item (each SMSP interleaves two softmax warps): thread i owns
-//            query row i (= TMEM lane i), so the row max/sum need no shuffles;
-//            each warpgroup keeps its own (m, l, O) and the epilogue merges them; online softmax in the exp2 domain
-//            with a lazy rescale (O in TMEM is only rescaled when the running max
-//            grows by more than 2^8).  P overwrites S in TMEM as two bf16 planes
-//            P = hi + lo, so the PV product carries ~16 mantissa bits of P (the
-//            tensor pipe has the headroom: this kernel is HBM-bound); keeping P
-//            out of shared memory frees it for a deeper K/V ring.  The epilogue
-//            normalises O and stores bf16, or writes fp32 split-KV partials.
-// Work items are planned on the host (optimus_attn_plan): long contexts are split
-// into key ranges and items are distributed longest-first over the CTAs.
+//            a work item: thread i owns query row i (= TMEM lane i), so the row
+//            max/sum need no shuffles; each warpgroup keeps its own (m, l, O) and
+//            the epilogue merges them.  Online softmax in the exp2 domain with a
+//            lazy rescale (O in TMEM is only rescaled when the running max grows by
+//            more than 2^8).  P overwrites S in TMEM: one fp16 plane with the fp16 V
+//            cache, or two bf16 planes P = hi + lo with a bf16 V cache.  An item's
+//            epilogue (normalise O, store bf16 or fp32 split-KV partials) runs
+//            after the warpgroup's first tile of the next item.
+//   Control roles issue from a converged warp with one elected lane, so their
+//   operands sit in uniform registers (no per-instruction R2UR loop).
+// Work items are planned on the host (optimus_attn_plan): whole (request, KV head,
+// token group) units placed longest-first, cut at tile boundaries when that balances
+// the CTAs; cut pieces are merged by the split-KV combine kernel below.
 #include "attn.cuh"
 
 namespace optimus {
@@ -39,6 +41,8 @@ namespace optimus {
 constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
 constexpr int kThreads = 384;  // 12 warps: 8 softmax, 4 control
+constexpr int kSBuf = 3;       // S/P buffers in TMEM, rotating over the CTA's tile stream
+constexpr int kEpiRing = 8;    // per-item epilogue records (outlive the staged record)
 constexpr int kTraceSlots = 4096;  // per CTA: [role*256 + i], 16 roles
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -48,8 +52,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // roles: 0 producer top, 1 MMA S issue, 2 softmax S ready, 3 softmax P done,
 // 4 producer slot free, 5 producer K issued, 6 misc (0 entry [globaltimer], 1 setup,
-// 2 producer done, 3 CTA done), 7 PV issued, 8 MMA reaches PV (v_full wait),
-// 9 V landed (p_full wait), 10 V producer slot free, 11 V producer issued, 12 MMA reaches S
+// 2 producer done, 3 CTA done, 4 CTA done [globaltimer]), 7 PV issued, 8 MMA reaches
+// PV (v_full wait), 9 V landed (p_full wait), 10 V producer slot free, 11 V producer
+// issued, 12 MMA reaches S.  Tile-indexed roles count the CTA's tile stream.
 __device__ __forceinline__ void trace(const AttnParams& p, int role, int i) {
   if (p.trace != nullptr && i < 256)
     p.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + role * 256 + i] =
@@ -67,34 +72,40 @@ struct UnitInfo {
   uint32_t words[kMaxUnitWords];
   int pages[kMaxUnitPages];
 };
+// epilogue record of item u at [u % kEpiRing]: {head, tok_begin, n_tok, slot, n_tiles}
+constexpr int kEpiInts = 8;
 
-template <int HD, int STAGES>
+template <int HD, int KST, int VST>
 struct AttnSmem {
   static constexpr int KB = HD / 64;
   static constexpr uint32_t Q_BYTES = KB * kBlockM * 128;
   static constexpr uint32_t KT_BYTES = KB * kTileN * 128;
-  static constexpr uint32_t OFF_Q = 0;
-  static constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
-  static constexpr uint32_t OFF_V = OFF_K + STAGES * KT_BYTES;
-  static constexpr uint32_t OFF_INFO = OFF_V + STAGES * KT_BYTES;
+  static constexpr uint32_t OFF_Q = 0;  // one Q tile: copied into TMEM per item
+  static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
+  static constexpr uint32_t OFF_V = OFF_K + KST * KT_BYTES;
+  static constexpr uint32_t OFF_INFO = OFF_V + VST * KT_BYTES;
   static constexpr uint32_t OFF_RED = OFF_INFO + 2 * sizeof(UnitInfo);  // float[{m,l}][wg][128]
-  static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * kBlockM * 4;  // int4[4] epilogue ring
-  static constexpr uint32_t OFF_BAR = OFF_EPI + 4 * 16;
-  static constexpr int NUM_BARS = 4 * STAGES + 2 + 2 + 4 * 3 + 2 + 2 + 2;
+  static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * kBlockM * 4;
+  static constexpr uint32_t OFF_BAR = OFF_EPI + kEpiRing * kEpiInts * 4;
+  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 2 + 4;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
-  // TMEM columns: four S/P buffers [0,256) (warpgroup h, buffer k at (2h+k)*64), then
-  // the two warpgroups' O accumulators O_0 = [256,256+HD), O_1 = [256+HD,256+2HD)
+  // TMEM columns: three S/P buffers [0,192), the item's Q tile (A operand of
+  // S = Q K^T) [192, 192+HD/2), then the warpgroups' O accumulators
+  // O_0 = [256,256+HD), O_1 = [256+HD,256+2HD).
   static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t TM_Q = kSBuf * kTileN;
+  static constexpr uint32_t TM_O = 256;
+  static_assert(TM_Q + HD / 2 <= TM_O && TM_O + 2 * HD <= TMEM_COLS, "TMEM budget");
 };
 
-template <int HD, int STAGES, bool VF16>
+template <int HD, int KST, int VST, bool VF16>
 __global__ void __launch_bounds__(kThreads, 1)
     paged_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
-  using L = AttnSmem<HD, STAGES>;
+  using L = AttnSmem<HD, KST, VST>;
   constexpr int KB = L::KB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -103,24 +114,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = smem + L::OFF_V;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* k_full = bars;
-  uint64_t* k_empty = k_full + STAGES;
-  uint64_t* v_full = k_empty + STAGES;
-  uint64_t* v_empty = v_full + STAGES;
-  uint64_t* q_full = v_empty + STAGES;
-  uint64_t* q_empty = q_full + 2;
-  uint64_t* s_full = q_empty + 2;   // [warpgroup][buffer]
-  uint64_t* p_full = s_full + 4;    // [warpgroup][buffer]
-  uint64_t* pv_done = p_full + 4;   // [warpgroup][buffer]
-  uint64_t* o_full = pv_done + 4;   // [1]
-  uint64_t* o_empty = o_full + 1;   // [1]
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* q_full = v_empty + VST;  // Q tile landed in smem
+  uint64_t* q_empty = q_full + 1;    // Q tile copied into TMEM (smem free)
+  uint64_t* s_full = q_empty + 1;    // [buffer]
+  uint64_t* p_full = s_full + kSBuf;   // [buffer]
+  uint64_t* pv_done = p_full + kSBuf;  // [buffer]
+  uint64_t* o_full = pv_done + kSBuf;
+  uint64_t* o_empty = o_full + 1;
   uint64_t* info_full = o_empty + 1;
   uint64_t* info_empty = info_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + 2);
   UnitInfo* info = reinterpret_cast<UnitInfo*>(smem + L::OFF_INFO);
-  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);    // epilogue (m, l) exchange
-  // {head, tok_begin, n_tok, slot} of item u at [u & 3]: outlives the double-buffered
-  // record, because an item's epilogue runs during the next item
-  int4* epi = reinterpret_cast<int4*>(smem + L::OFF_EPI);
+  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // epilogue (m, l) exchange
+  int* epi = reinterpret_cast<int*>(smem + L::OFF_EPI);
 
   const int warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0);  // provably warp-uniform
   const int lane = threadIdx.x & 31;
@@ -132,19 +141,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tm_v);
   }
   if (warp == 9 && lane == 0) {
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < KST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VST; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
       mbar_init(&info_full[i], 32);
       mbar_init(&info_empty[i], 256 + 2);  // softmax threads + K and V producers
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kSBuf; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&pv_done[i], 1);
@@ -154,12 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_fence_init();
   }
   if (warp == 10) tmem_alloc<L::TMEM_COLS>(tmem_slot);
-  // Zero the K/V ring once: rows a partial tile never loads must hold finite values
+  // Zero the K/V rings once: rows a partial tile never loads must hold finite values
   // (their probabilities are 0, and 0 * NaN would poison O).
   {
     uint4* z = reinterpret_cast<uint4*>(sK);
     const uint4 zero = make_uint4(0, 0, 0, 0);
-    for (uint32_t i = threadIdx.x; i < 2 * STAGES * L::KT_BYTES / 16; i += kThreads) z[i] = zero;
+    for (uint32_t i = threadIdx.x; i < (KST + VST) * L::KT_BYTES / 16; i += kThreads) z[i] = zero;
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -167,162 +178,173 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace(p, 6, 1);
-  const uint32_t tm_s0 = tmem_base;        // S/P buffers
-  const uint32_t tm_o0 = tmem_base + 256;  // O accumulators
+  const uint32_t tm_s0 = tmem_base;           // S/P buffers
+  const uint32_t tm_qt = tmem_base + L::TM_Q; // Q tile (MMA A operand)
+  const uint32_t tm_o0 = tmem_base + L::TM_O; // O accumulators
 
   const int w_begin = p.cta_off[blockIdx.x];
   const int w_end = p.cta_off[blockIdx.x + 1];
 
   if (warp == 8 || warp == 10) {
     // ------------------------------------------------------------ TMA producers
-    // Two issuing threads keep the TMA engine busy (one box costs its issuer a few
-    // hundred cycles): warp 8 loads Q and the K ring, warp 10 the V ring.
-    if (lane == 0) {
-      const bool is_k = warp == 8;
-      const uint32_t q_tx = KB * 64 * p.group * p.tok_per_tile * 2;
-      const uint32_t chunk_tx = p.box_rows * 128 * KB;  // one tensor, one box-row group
-      const int chunks_per_tile = kTileN / p.box_rows;
-      const int shift = p.page_shift;
-      const int pmask = p.page_size - 1;
-      const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
-      uint8_t* ring = is_k ? sK : sV;
-      uint64_t* full = is_k ? k_full : v_full;
-      uint64_t* empty = is_k ? k_empty : v_empty;
-      int tile_ctr = 0;
-      int unit = 0;
-      for (int w = w_begin; w < w_end; ++w, ++unit) {
-        const int ib = unit & 1;
-        const uint32_t ipar = (unit >> 1) & 1;
-        mbar_wait(&info_full[ib], ipar);
-        // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
-        // everything above overlapped their tail under PDL; the loads may not.
-        if (unit == 0) grid_dep_wait();
-        const UnitInfo& u = info[ib];
-        const int head = u.head, key_begin = u.key_begin, key_end = u.key_end;
-        const int pg0 = key_begin >> shift;
-        if (is_k) {
-          mbar_wait(&q_empty[ib], ipar ^ 1);
-          mbar_arrive_expect_tx(&q_full[ib], q_tx);
+    // Warp 8 loads Q and the K ring, warp 10 the V ring.  The whole warp runs the
+    // loop (operands warp-uniform, in uniform registers); one elected lane issues.
+    const bool is_k = warp == 8;
+    const int NST = is_k ? KST : VST;
+    const uint32_t q_tx = KB * 64 * p.group * p.tok_per_tile * 2;
+    const uint32_t chunk_tx = p.box_rows * 128 * KB;  // one tensor, one box-row group
+    const int chunks_per_tile = kTileN / p.box_rows;
+    const int shift = p.page_shift;
+    const int pmask = p.page_size - 1;
+    const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+    uint8_t* ring = is_k ? sK : sV;
+    uint64_t* full = is_k ? k_full : v_full;
+    uint64_t* empty = is_k ? k_empty : v_empty;
+    int tile_ctr = 0;
+    int unit = 0;
+    for (int w = w_begin; w < w_end; ++w, ++unit) {
+      const int ib = unit & 1;
+      mbar_wait(&info_full[ib], (unit >> 1) & 1);
+      // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
+      // everything above overlapped their tail under PDL; the loads may not.
+      if (unit == 0) grid_dep_wait();
+      const UnitInfo& u = info[ib];
+      const int head = __shfl_sync(0xFFFFFFFFu, u.head, 0);
+      const int key_begin = __shfl_sync(0xFFFFFFFFu, u.key_begin, 0);
+      const int key_end = __shfl_sync(0xFFFFFFFFu, u.key_end, 0);
+      const int pg0 = key_begin >> shift;
+      if (is_k) {
+        const int tok_begin = __shfl_sync(0xFFFFFFFFu, u.tok_begin, 0);
+        mbar_wait(q_empty, (unit & 1) ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(q_full, q_tx);
           for (int kb = 0; kb < KB; ++kb)
-            tma_load_4d(sQ + ib * L::Q_BYTES + kb * (kBlockM * 128), &tm_q, &q_full[ib], kb * 64, 0,
-                        head, u.tok_begin);
+            tma_load_4d(sQ + kb * (kBlockM * 128), &tm_q, q_full, kb * 64, 0, head, tok_begin);
         }
-        for (int kt = key_begin; kt < key_end; kt += kTileN, ++tile_ctr) {
-          const int st = tile_ctr % STAGES;
-          int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
-          if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
-          if (is_k) trace(p, 0, tile_ctr);
-          mbar_wait(&empty[st], ((tile_ctr / STAGES) & 1) ^ 1);
-          trace(p, is_k ? 4 : 10, tile_ctr);
-          mbar_arrive_expect_tx(&full[st], n_chunks * chunk_tx);
-          uint8_t* dst = ring + st * L::KT_BYTES;
-          for (int c = 0; c < n_chunks; ++c) {
-            const int s0 = kt + c * p.box_rows;
-            const int page = u.pages[(s0 >> shift) - pg0];
+        __syncwarp();
+      }
+      for (int kt = key_begin; kt < key_end; kt += kTileN, ++tile_ctr) {
+        const int st = tile_ctr % NST;
+        int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
+        if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
+        if (is_k && lane == 0) trace(p, 0, tile_ctr);
+        mbar_wait(&empty[st], ((tile_ctr / NST) & 1) ^ 1);
+        if (lane == 0) trace(p, is_k ? 4 : 10, tile_ctr);
+        uint8_t* dst = ring + st * L::KT_BYTES;
+        const int pg_lane = lane < n_chunks ? u.pages[((kt + lane * p.box_rows) >> shift) - pg0] : 0;
+        if (elect_one()) mbar_arrive_expect_tx(&full[st], n_chunks * chunk_tx);
+        for (int c = 0; c < n_chunks; ++c) {
+          const int s0 = kt + c * p.box_rows;
+          const int page = __shfl_sync(0xFFFFFFFFu, pg_lane, c);
+          if (elect_one()) {
             for (int kb = 0; kb < KB; ++kb)
               tma_load_4d(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st], kb * 64,
                           s0 & pmask, head, page);
           }
-          trace(p, is_k ? 5 : 11, tile_ctr);
         }
-        mbar_arrive(&info_empty[ib]);
+        __syncwarp();
+        if (lane == 0) trace(p, is_k ? 5 : 11, tile_ctr);
       }
+      if (elect_one()) mbar_arrive(&info_empty[ib]);
+      __syncwarp();
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    // Tile j of a work item belongs to softmax warpgroup h = j & 1; its S goes to
-    // that warpgroup's next S/P buffer and its PV accumulates into O_h.  S runs up
-    // to four tiles ahead of PV (two buffers per warpgroup; the in-order tensor
-    // pipe retires PV(j) before S(j+4) overwrites the buffer holding P(j)).
-    // The whole warp runs the loop (all lanes wait on the barriers and compute the
-    // same operands, in uniform registers); one elected lane issues.
-    {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(kBlockM, kTileN, false, false);
-      // PV: A = P from TMEM, B = V (MN-major).  fp16 V cache: one fp16 P plane;
-      // bf16 V cache: P = hi + lo bf16 planes, two MMAs per k-step.
-      constexpr uint32_t idesc_o = VF16 ? umma_idesc_f16(kBlockM, HD, false, true, 0u, 0u)
-                                        : umma_idesc_bf16(kBlockM, HD, false, true);
-      const uint32_t sQ_a = smem_u32(sQ), sK_a = smem_u32(sK), sV_a = smem_u32(sV);
-      int tile_ctr = 0;
-      int unit = 0;
-      int cs[2] = {0, 0};  // S tiles issued per warpgroup
-      int cp[2] = {0, 0};  // PV tiles issued per warpgroup
-      for (int w = w_begin; w < w_end; ++w, ++unit) {
-        const int qb = unit & 1;
-        mbar_wait(&q_full[qb], (unit >> 1) & 1);  // implies info[qb] is staged
-        const int n_tiles = __shfl_sync(
-            0xFFFFFFFFu, (info[qb].key_end - info[qb].key_begin + kTileN - 1) / kTileN, 0);
+    // One stream of tiles over the CTA's work items.  S(t) = Q K^T goes to S/P buffer
+    // t % 3 with A = the item's Q tile in TMEM (copied from smem by tcgen05.cp when
+    // the S stream enters the item) and B = the K tile; PV(t) accumulates
+    // P(t) (TMEM, TS-MMA) x V into O_{j&1} of its item.  S runs three tiles ahead
+    // of PV, across item boundaries: the in-order tensor pipe retires PV(t) before
+    // S(t+3) overwrites the buffer holding P(t), and the last S of an item before the
+    // next item's Q copy overwrites the Q columns.  The whole warp runs the loop
+    // (warp-uniform operands in uniform registers); one elected lane issues.
+    constexpr uint32_t idesc_s = umma_idesc_bf16(kBlockM, kTileN, false, false);
+    // PV: A = P from TMEM, B = V (MN-major).  fp16 V cache: one fp16 P plane;
+    // bf16 V cache: P = hi + lo bf16 planes, two MMAs per k-step.
+    constexpr uint32_t idesc_o = VF16 ? umma_idesc_f16(kBlockM, HD, false, true, 0u, 0u)
+                                      : umma_idesc_bf16(kBlockM, HD, false, true);
+    const uint32_t sQ_a = smem_u32(sQ), sK_a = smem_u32(sK), sV_a = smem_u32(sV);
+    const int n_units = w_end - w_begin;
+    int s_unit = -1, s_j = 0, s_n = 0, s_cnt = 0;  // S stream cursor
+    auto s_more = [&]() { return s_j < s_n || s_unit + 1 < n_units; };
+    auto issue_s = [&]() {
+      if (s_j == s_n) {
+        // enter the next item: its record gives the tile count, its Q tile goes to TMEM
+        ++s_unit;
+        s_j = 0;
+        mbar_wait(&info_full[s_unit & 1], (s_unit >> 1) & 1);
+        s_n = __shfl_sync(0xFFFFFFFFu, epi[(s_unit % kEpiRing) * kEpiInts + 4], 0);
+        mbar_wait(q_full, s_unit & 1);
         tc_fence_after();
-        auto issue_s = [&](int j) {
-          const int t = tile_ctr + j;
-          const int h = j & 1;
-          const int k = cs[h] & 1;
-          const int st = t % STAGES;
-          if (lane == 0) trace(p, 12, t);
-          mbar_wait(&k_full[st], (t / STAGES) & 1);
-          tc_fence_after();
-          if (lane == 0) trace(p, 1, t);
-          const uint32_t d = tm_s0 + (2 * h + k) * kTileN;
-          const uint64_t a0 = umma_sdesc_sw128(sQ_a + qb * L::Q_BYTES, 16, 1024);
-          const uint64_t b0 = umma_sdesc_sw128(sK_a + st * L::KT_BYTES, 16, 1024);
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < HD / 16; ++ks) {
-              if (p.dbg & 2) break;
-              // descriptor start address is in 16 B units: +32 B per k-step inside a
-              // 128 B swizzle row, +one 64-column box per 4 k-steps
-              const uint64_t da = ((ks >> 2) * (kBlockM * 128) + (ks & 3) * 32) >> 4;
-              const uint64_t db = ((ks >> 2) * (kTileN * 128) + (ks & 3) * 32) >> 4;
-              if (p.dbg & 32)  // timing experiment only: A from TMEM (garbage operand)
-                umma_bf16_ts(d, tm_o0 + HD + ks * 8, b0 + db, idesc_s, ks > 0 ? 1u : 0u);
-              else
-                umma_bf16_ss(d, a0 + da, b0 + db, idesc_s, ks > 0 ? 1u : 0u);
-            }
-            umma_commit(&s_full[2 * h + k]);
-            umma_commit(&k_empty[st]);
-          }
-          __syncwarp();
-          ++cs[h];
-        };
-        const int pre = n_tiles < 4 ? n_tiles : 4;
-        for (int j = 0; j < pre; ++j) issue_s(j);
-        mbar_wait(o_empty, (unit & 1) ^ 1);  // the previous item's epilogue has read O_0/O_1
-        tc_fence_after();
-        for (int j = 0; j < n_tiles; ++j) {
-          const int t = tile_ctr + j;
-          const int h = j & 1;
-          const int k = cp[h] & 1;
-          const int st = t % STAGES;
-          if (lane == 0) trace(p, 8, t);
-          mbar_wait(&v_full[st], (t / STAGES) & 1);
-          if (lane == 0) trace(p, 9, t);
-          mbar_wait(&p_full[2 * h + k], (cp[h] >> 1) & 1);
-          tc_fence_after();
-          if (lane == 0) trace(p, 7, t);
-          const uint32_t d = tm_o0 + h * HD;
-          const uint32_t pa = tm_s0 + (2 * h + k) * kTileN;  // P hi at +0..31, lo at +32..63
-          const uint64_t b0 = umma_sdesc_sw128(sV_a + st * L::KT_BYTES, kTileN * 128, 1024);
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < kTileN / 16; ++ks) {
-              if (p.dbg & 8) break;
-              const uint64_t b = b0 + ((ks * 16 * 128) >> 4);  // 16 keys = 16 rows of 128 B
-              umma_bf16_ts(d, pa + ks * 8, b, idesc_o, (j > 1 || ks > 0) ? 1u : 0u);
-              if (!VF16 && !(p.dbg & 1)) umma_bf16_ts(d, pa + 32 + ks * 8, b, idesc_o, 1u);
-            }
-            umma_commit(&pv_done[2 * h + k]);
-            umma_commit(&v_empty[st]);
-          }
-          __syncwarp();
-          ++cp[h];
-          if (j + 4 < n_tiles) issue_s(j + 4);
-        }
+        const uint64_t q0 = umma_sdesc_sw128(sQ_a, 16, 1024);
         if (elect_one()) {
-          umma_commit(&q_empty[qb]);
-          umma_commit(o_full);
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks)
+            tmem_cp_128x256b(tm_qt + ks * 8, q0 + (((ks >> 2) * (kBlockM * 128) + (ks & 3) * 32) >> 4));
+          umma_commit(q_empty);  // the smem tile is free once the copies land
         }
         __syncwarp();
-        tile_ctr += n_tiles;
+      }
+      const int t = s_cnt;
+      const int b = t % kSBuf;
+      const int st = t % KST;
+      if (lane == 0) trace(p, 12, t);
+      mbar_wait(&k_full[st], (t / KST) & 1);
+      tc_fence_after();
+      if (lane == 0) trace(p, 1, t);
+      const uint32_t d = tm_s0 + b * kTileN;
+      const uint64_t b0 = umma_sdesc_sw128(sK_a + st * L::KT_BYTES, 16, 1024);
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          if (p.dbg & 2) break;
+          // +32 B per k-step inside a 128 B swizzle row, +one 64-column box per 4
+          const uint64_t db = ((ks >> 2) * (kTileN * 128) + (ks & 3) * 32) >> 4;
+          umma_bf16_ts(d, tm_qt + ks * 8, b0 + db, idesc_s, ks > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[b]);
+        umma_commit(&k_empty[st]);
+      }
+      __syncwarp();
+      ++s_cnt;
+      ++s_j;
+    };
+    for (int i = 0; i < kSBuf && s_more(); ++i) issue_s();
+    int t = 0;  // PV stream position
+    for (int u = 0; u < n_units; ++u) {
+      const int n_tiles = __shfl_sync(0xFFFFFFFFu, epi[(u % kEpiRing) * kEpiInts + 4], 0);
+      mbar_wait(o_empty, (u & 1) ^ 1);  // the previous item's epilogue has read O_0/O_1
+      tc_fence_after();
+      for (int j = 0; j < n_tiles; ++j, ++t) {
+        const int h = j & 1;
+        const int b = t % kSBuf;
+        const int st = t % VST;
+        if (lane == 0) trace(p, 8, t);
+        mbar_wait(&v_full[st], (t / VST) & 1);
+        if (lane == 0) trace(p, 9, t);
+        mbar_wait(&p_full[b], (t / kSBuf) & 1);
+        tc_fence_after();
+        if (lane == 0) trace(p, 7, t);
+        const uint32_t d = tm_o0 + h * HD;
+        const uint32_t pa = tm_s0 + b * kTileN;  // P (hi) at +0..31, bf16 lo plane at +32..63
+        const uint64_t b0 = umma_sdesc_sw128(sV_a + st * L::KT_BYTES, kTileN * 128, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < kTileN / 16; ++ks) {
+            if (p.dbg & 8) break;
+            const uint64_t bd = b0 + ((ks * 16 * 128) >> 4);  // 16 keys = 16 rows of 128 B
+            umma_bf16_ts(d, pa + ks * 8, bd, idesc_o, (j > 1 || ks > 0) ? 1u : 0u);
+            if (!VF16 && !(p.dbg & 1)) umma_bf16_ts(d, pa + 32 + ks * 8, bd, idesc_o, 1u);
+          }
+          umma_commit(&pv_done[b]);
+          umma_commit(&v_empty[st]);
+          // the item's accumulators are complete after its last PV; signal before
+          // the S stream may block on a later item's record, which the softmax
+          // warps only release after draining this item (deferred epilogue)
+          if (j == n_tiles - 1) umma_commit(o_full);
+        }
+        __syncwarp();
+        if (s_more()) issue_s();
       }
     }
   } else if (warp == 11) {
@@ -336,10 +358,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       UnitInfo& u = info[ib];
       const int f = lane < 8 ? __ldg(p.work + 8 * w + lane) : 0;
       const int req = __shfl_sync(0xFFFFFFFFu, f, 0);
+      const int head = __shfl_sync(0xFFFFFFFFu, f, 1);
       const int tok_begin = __shfl_sync(0xFFFFFFFFu, f, 2);
       const int n_tok = __shfl_sync(0xFFFFFFFFu, f, 3);
       const int key_begin = __shfl_sync(0xFFFFFFFFu, f, 4);
       const int key_end = __shfl_sync(0xFFFFFFFFu, f, 5);
+      const int slot = __shfl_sync(0xFFFFFFFFu, f, 6);
       // one round trip: request scalars, query positions, page ids
       int scal = 0;
       if (lane == 0) scal = __ldg(p.prompt_len + req);
@@ -366,8 +390,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nw = key_end > vb ? (key_end - vb + 31) / 32 : 0;
       if (nw <= kMaxUnitWords && lane < nw) u.words[lane] = __ldg(p.vis_words + voff + lane);
       if (lane < 7) (&u.req)[lane] = f;
-      const int e_head = __shfl_sync(0xFFFFFFFFu, f, 1), e_slot = __shfl_sync(0xFFFFFFFFu, f, 6);
-      if (lane == 0) epi[unit & 3] = make_int4(e_head, tok_begin, n_tok, e_slot);
+      if (lane < kEpiInts) {
+        const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
+        const int v = lane == 0 ? head : lane == 1 ? tok_begin : lane == 2 ? n_tok
+                    : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
+        epi[(unit % kEpiRing) * kEpiInts + lane] = v;
+      }
       if (lane == 0) {
         u.vb = vb;
         u.n_words = nw;
@@ -393,11 +421,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Epilogue of item `e`: exchange (m, l) between the warpgroups through `red`;
     // warpgroup h then writes output columns [h*HD/2, (h+1)*HD/2) merged from O_0
     // and O_1 and releases the accumulators to the MMA warp.  It runs after this
-    // warpgroup's first tile of item e+1, so the S/softmax of the next item
-    // overlaps the last PV and this drain instead of waiting behind them.
+    // warpgroup's first tile of item e+1, so the next item's softmax overlaps the
+    // last PV and this drain instead of waiting behind them.
     auto epilogue = [&](int e) {
-      const int4 ei = epi[e & 3];
-      const int head = ei.x, tok_begin = ei.y, n_tok = ei.z, slot = ei.w;
+      const int* er = epi + (e % kEpiRing) * kEpiInts;
+      const int head = er[0], tok_begin = er[1], n_tok = er[2], slot = er[3];
       const bool valid = row_exists && t_in < n_tok;
       const bool warp_valid = (wq * 32) / G < n_tok;
       named_bar_sync(1, 256);
@@ -454,7 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(o_empty);
     };
-    int cw = 0;  // tiles processed by this warpgroup (buffer / phase counter)
+    int cw = 0;     // tiles processed by this warpgroup (trace index)
+    int tbase = 0;  // stream index of the current item's first tile
     int unit = 0;
     for (int w = w_begin; w < w_end; ++w, ++unit) {
       const int ib = unit & 1;
@@ -472,9 +501,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY;
       float l = 0.f;
       for (int j = wg; j < n_tiles; j += 2, ++cw) {
-        const int k = cw & 1;
-        const uint32_t tsp = tm_s0 + lane_off + (2 * wg + k) * kTileN;  // this tile's S/P
-        mbar_wait(&s_full[2 * wg + k], (cw >> 1) & 1);
+        const int t = tbase + j;
+        const int b = t % kSBuf;
+        const uint32_t tsp = tm_s0 + lane_off + b * kTileN;  // this tile's S/P
+        mbar_wait(&s_full[b], (t / kSBuf) & 1);
         tc_fence_after();
         if (threadIdx.x == 0) trace(p, 2, cw);
         if (warp_valid && !(p.dbg & 4)) {
@@ -513,8 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float m_new = need ? tmax : m;
           if (j >= 2 && __any_sync(0xFFFFFFFFu, need)) {
             // O_wg holds this warpgroup's earlier tiles once its previous PV retires
-            const int cprev = cw - 1;
-            mbar_wait(&pv_done[2 * wg + (cprev & 1)], (cprev >> 1) & 1);
+            const int tp = t - 2;
+            mbar_wait(&pv_done[tp % kSBuf], (tp / kSBuf) & 1);
             tc_fence_after();
             const float alpha = need ? fast_exp2(m - m_new) : 1.0f;
 #pragma unroll
@@ -574,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_st();
         }
         tc_fence_before();
-        mbar_arrive(&p_full[2 * wg + k]);
+        mbar_arrive(&p_full[b]);
         if (threadIdx.x == 0) trace(p, 3, cw);
         if (j == wg && unit > 0 && !(p.dbg & 16)) epilogue(unit - 1);  // previous item, overlapped
       }
@@ -584,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       red[(0 * 2 + wg) * kBlockM + row] = m;  // read by this item's epilogue
       red[(1 * 2 + wg) * kBlockM + row] = l;
       if (p.dbg & 16) epilogue(unit);  // diagnostics: drain in place (no overlap)
+      tbase += n_tiles;
     }
     if (unit > 0 && !(p.dbg & 16)) epilogue(unit - 1);
   }
@@ -659,14 +690,14 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __rest
   }
 }
 
-template <int HD, int STAGES, bool VF16>
+template <int HD, int KST, int VST, bool VF16>
 static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          const AttnParams& prm, int grid, const int32_t* groups, int n_groups,
                          cudaStream_t stream) {
-  using L = AttnSmem<HD, STAGES>;
+  using L = AttnSmem<HD, KST, VST>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, STAGES, VF16>,
+    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, KST, VST, VF16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
     if (e != cudaSuccess) return static_cast<int>(e);
     configured = true;
@@ -685,7 +716,7 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, paged_attn_kernel<HD, STAGES, VF16>, tq, tk, tv, prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, paged_attn_kernel<HD, KST, VST, VF16>, tq, tk, tv, prm);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (n_groups > 0) {
@@ -713,13 +744,14 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
 int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CUtensorMap& tk,
                       const CUtensorMap& tv, const AttnParams& prm, int grid,
                       const int32_t* groups, int n_groups, cudaStream_t stream) {
-  // 227 KB of shared memory: 2 Q tiles + a 4-deep (d=128) / 8-deep (d=64) K/V ring.
+  // 227 KB of shared memory: one Q tile + the K ring + a deeper V ring (a V slot is
+  // held until its PV retires, a K slot only until its S does).
   if (head_dim == 128)
-    return v_fp16 ? launch_attn_t<128, 4, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
-                  : launch_attn_t<128, 4, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+    return v_fp16 ? launch_attn_t<128, 5, 6, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                  : launch_attn_t<128, 5, 6, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
   if (head_dim == 64)
-    return v_fp16 ? launch_attn_t<64, 8, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
-                  : launch_attn_t<64, 8, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+    return v_fp16 ? launch_attn_t<64, 10, 12, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                  : launch_attn_t<64, 10, 12, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
   return -1;
 }
 
