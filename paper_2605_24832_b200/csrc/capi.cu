@@ -433,6 +433,7 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
   if (reinterpret_cast<uintptr_t>(q) % 16 || reinterpret_cast<uintptr_t>(k_cache) % 16 ||
       reinterpret_cast<uintptr_t>(v_cache) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
     return fail("paged_attn: tensors must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(work) % 16) return fail("paged_attn: work list must be 16-byte aligned");
   if (int st = check_device()) return st;
   const int T = 128 / G;
   CUtensorMap tq, tk, tv;

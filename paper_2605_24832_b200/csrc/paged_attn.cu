@@ -42,7 +42,9 @@ constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
 constexpr int kThreads = 384;  // 12 warps: 8 softmax, 4 control
 constexpr int kSBuf = 3;       // S/P buffers in TMEM, rotating over the CTA's tile stream
+constexpr int kInfo = 4;       // staged work-item records: the metadata warp runs 3 items ahead
 constexpr int kEpiRing = 8;    // per-item epilogue records (outlive the staged record)
+static_assert(kEpiRing > kInfo + 1, "epilogue records must outlive the staging ring");
 constexpr int kTraceSlots = 4096;  // per CTA: [role*256 + i], 16 roles
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -52,23 +54,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // roles: 0 producer top, 1 MMA S issue, 2 softmax S ready, 3 softmax P done,
 // 4 producer slot free, 5 producer K issued, 6 misc (0 entry [globaltimer], 1 setup,
-// 2 producer done, 3 CTA done, 4 CTA done [globaltimer]), 7 PV issued, 8 MMA reaches
-// PV (v_full wait), 9 V landed (p_full wait), 10 V producer slot free, 11 V producer
-// issued, 12 MMA reaches S.  Tile-indexed roles count the CTA's tile stream.
+// 2 producer done, 3 CTA done, 4 CTA done [globaltimer], 5.. metadata item staged),
+// 7 PV issued, 8 MMA reaches PV (v_full wait), 9 V landed (p_full wait), 10 V producer
+// slot free, 11 V producer issued, 12 MMA reaches S, 13/14/15 epilogue of item i
+// entered / O complete / O released (warpgroup 0).  Tile-indexed roles count the
+// CTA's tile stream.
 __device__ __forceinline__ void trace(const AttnParams& p, int role, int i) {
   if (p.trace != nullptr && i < 256)
     p.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + role * 256 + i] =
         (role == 6 && (i == 0 || i == 4)) ? gtimer() : static_cast<unsigned long long>(clock64());
 }
 
-// Per-work-item record staged in shared memory by the metadata warp one item ahead,
-// so no other role touches global memory on its critical path.
+// Per-work-item record staged in shared memory by the metadata warp up to kInfo items
+// ahead (scalars by plain stores, page ids / query positions / visibility words by
+// 4-byte cp.async), so no other role touches global memory on its critical path and
+// the stager itself never waits on a load.
 constexpr int kMaxUnitPages = 256;  // the planner caps an item at 255 pages of keys
 constexpr int kMaxUnitWords = 16;   // visibility words held in smem (more: read from global)
 struct UnitInfo {
   int req, head, tok_begin, n_tok, key_begin, key_end, slot, vb;
-  int n_words, vis_off, pad0, pad1;
-  int lim[kBlockM];                 // per query token: first key it may not see
+  int n_words, vis_off, prompt, pad0;
+  int qpos[kBlockM];                // query positions of the item's tokens
   uint32_t words[kMaxUnitWords];
   int pages[kMaxUnitPages];
 };
@@ -84,10 +90,10 @@ struct AttnSmem {
   static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
   static constexpr uint32_t OFF_V = OFF_K + KST * KT_BYTES;
   static constexpr uint32_t OFF_INFO = OFF_V + VST * KT_BYTES;
-  static constexpr uint32_t OFF_RED = OFF_INFO + 2 * sizeof(UnitInfo);  // float[{m,l}][wg][128]
+  static constexpr uint32_t OFF_RED = OFF_INFO + kInfo * sizeof(UnitInfo);  // float[{m,l}][wg][128]
   static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * kBlockM * 4;
   static constexpr uint32_t OFF_BAR = OFF_EPI + kEpiRing * kEpiInts * 4;
-  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 2 + 4;
+  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 2 + 2 * kInfo;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
@@ -125,8 +131,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_full = pv_done + kSBuf;
   uint64_t* o_empty = o_full + 1;
   uint64_t* info_full = o_empty + 1;
-  uint64_t* info_empty = info_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + 2);
+  uint64_t* info_empty = info_full + kInfo;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + kInfo);
   UnitInfo* info = reinterpret_cast<UnitInfo*>(smem + L::OFF_INFO);
   float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // epilogue (m, l) exchange
   int* epi = reinterpret_cast<int*>(smem + L::OFF_EPI);
@@ -151,8 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&info_full[i], 32);
+    for (int i = 0; i < kInfo; ++i) {
+      mbar_init(&info_full[i], 33);  // 32 cp.async arrivals + lane 0's store arrival
       mbar_init(&info_empty[i], 256 + 2);  // softmax threads + K and V producers
     }
     for (int i = 0; i < kSBuf; ++i) {
@@ -200,11 +206,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* ring = is_k ? sK : sV;
     uint64_t* full = is_k ? k_full : v_full;
     uint64_t* empty = is_k ? k_empty : v_empty;
+    // K/V pages are read once per step: stream them through L2 with evict_first so
+    // the step metadata and Q stay resident
+    const uint64_t pol_stream = l2_policy_evict_first();
     int tile_ctr = 0;
     int unit = 0;
     for (int w = w_begin; w < w_end; ++w, ++unit) {
-      const int ib = unit & 1;
-      mbar_wait(&info_full[ib], (unit >> 1) & 1);
+      const int ib = unit % kInfo;
+      mbar_wait(&info_full[ib], (unit / kInfo) & 1);
       // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
       // everything above overlapped their tail under PDL; the loads may not.
       if (unit == 0) grid_dep_wait();
@@ -237,9 +246,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s0 = kt + c * p.box_rows;
           const int page = __shfl_sync(0xFFFFFFFFu, pg_lane, c);
           if (elect_one()) {
-            for (int kb = 0; kb < KB; ++kb)
-              tma_load_4d(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st], kb * 64,
-                          s0 & pmask, head, page);
+            for (int kb = 0; kb < KB; ++kb) {
+              if (p.dbg & 32)
+                tma_load_4d(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st], kb * 64,
+                            s0 & pmask, head, page);
+              else
+                tma_load_4d_hint(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st],
+                                 kb * 64, s0 & pmask, head, page, pol_stream);
+            }
           }
         }
         __syncwarp();
@@ -272,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // enter the next item: its record gives the tile count, its Q tile goes to TMEM
         ++s_unit;
         s_j = 0;
-        mbar_wait(&info_full[s_unit & 1], (s_unit >> 1) & 1);
+        mbar_wait(&info_full[s_unit % kInfo], (s_unit / kInfo) & 1);
         s_n = __shfl_sync(0xFFFFFFFFu, epi[(s_unit % kEpiRing) * kEpiInts + 4], 0);
         mbar_wait(q_full, s_unit & 1);
         tc_fence_after();
@@ -338,9 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma_commit(&pv_done[b]);
           umma_commit(&v_empty[st]);
-          // the item's accumulators are complete after its last PV; signal before
-          // the S stream may block on a later item's record, which the softmax
-          // warps only release after draining this item (deferred epilogue)
+          // the item's accumulator is complete after its last PV
           if (j == n_tiles - 1) umma_commit(o_full);
         }
         __syncwarp();
@@ -349,60 +361,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 11) {
     // ------------------------------------------------------------ metadata warp
-    // Stages work item w+1's record while the other roles run item w: page ids of
-    // its key range, the per-token visibility limit, and the visibility words.
-    int unit = 0;
-    for (int w = w_begin; w < w_end; ++w, ++unit) {
-      const int ib = unit & 1;
-      mbar_wait(&info_empty[ib], ((unit >> 1) & 1) ^ 1);
-      UnitInfo& u = info[ib];
-      const int f = lane < 8 ? __ldg(p.work + 8 * w + lane) : 0;
-      const int req = __shfl_sync(0xFFFFFFFFu, f, 0);
-      const int head = __shfl_sync(0xFFFFFFFFu, f, 1);
-      const int tok_begin = __shfl_sync(0xFFFFFFFFu, f, 2);
-      const int n_tok = __shfl_sync(0xFFFFFFFFu, f, 3);
-      const int key_begin = __shfl_sync(0xFFFFFFFFu, f, 4);
-      const int key_end = __shfl_sync(0xFFFFFFFFu, f, 5);
-      const int slot = __shfl_sync(0xFFFFFFFFu, f, 6);
-      // one round trip: request scalars, query positions, page ids
-      int scal = 0;
-      if (lane == 0) scal = __ldg(p.prompt_len + req);
-      if (lane == 1) scal = __ldg(p.vis_base + req);
-      if (lane == 2) scal = __ldg(p.vis_off + req);
-      int qp[kBlockM / 32];
+    // Stages work items into the kInfo-deep record ring.  The work records and the
+    // per-request scalars of up to 32 items are fetched once per batch (lane k holds
+    // item k); per item the warp then only issues asynchronous 4-byte copies of the
+    // page ids, query positions and visibility words, so several items' copies are
+    // in flight at once and the ring fills at the memory system's throughput, not
+    // one dependent round trip chain per item.
+    for (int base = w_begin; base < w_end; base += 32) {
+      const int nb = min(32, w_end - base);
+      int f[8];
+      if (lane < nb) {
+        const int4* wp = reinterpret_cast<const int4*>(p.work + 8 * (base + lane));
+        const int4 a = __ldg(wp), b = __ldg(wp + 1);
+        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < kBlockM / 32; ++i) {
-        const int t = lane + 32 * i;
-        qp[i] = t < n_tok ? __ldg(p.q_pos + tok_begin + t) : 0;
+        for (int i = 0; i < 8; ++i) f[i] = 0;
       }
-      const int pg0 = key_begin / p.page_size;
-      const int npg = (key_end - 1) / p.page_size - pg0 + 1;
-      const int32_t* bt = p.block_tables + static_cast<int64_t>(req) * p.max_pages + pg0;
-      for (int i = lane; i < npg && i < kMaxUnitPages; i += 32) u.pages[i] = __ldg(bt + i);
-      const int prompt = __shfl_sync(0xFFFFFFFFu, scal, 0);
-      const int vb = __shfl_sync(0xFFFFFFFFu, scal, 1);
-      const int voff = __shfl_sync(0xFFFFFFFFu, scal, 2);
-#pragma unroll
-      for (int i = 0; i < kBlockM / 32; ++i) {
-        const int t = lane + 32 * i;
-        if (t < n_tok) u.lim[t] = min(prompt + (qp[i] / p.block_size + 1) * p.block_size, key_end);
+      int prompt_l = 0, vb_l = 0, voff_l = 0;
+      if (lane < nb) {
+        prompt_l = __ldg(p.prompt_len + f[0]);
+        vb_l = __ldg(p.vis_base + f[0]);
+        voff_l = __ldg(p.vis_off + f[0]);
       }
-      const int nw = key_end > vb ? (key_end - vb + 31) / 32 : 0;
-      if (nw <= kMaxUnitWords && lane < nw) u.words[lane] = __ldg(p.vis_words + voff + lane);
-      if (lane < 7) (&u.req)[lane] = f;
-      if (lane < kEpiInts) {
-        const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
-        const int v = lane == 0 ? head : lane == 1 ? tok_begin : lane == 2 ? n_tok
-                    : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
-        epi[(unit % kEpiRing) * kEpiInts + lane] = v;
+      for (int k = 0; k < nb; ++k) {
+        const int unit = base - w_begin + k;
+        const int ib = unit % kInfo;
+        const int req = __shfl_sync(0xFFFFFFFFu, f[0], k);
+        const int head = __shfl_sync(0xFFFFFFFFu, f[1], k);
+        const int tok_begin = __shfl_sync(0xFFFFFFFFu, f[2], k);
+        const int n_tok = __shfl_sync(0xFFFFFFFFu, f[3], k);
+        const int key_begin = __shfl_sync(0xFFFFFFFFu, f[4], k);
+        const int key_end = __shfl_sync(0xFFFFFFFFu, f[5], k);
+        const int slot = __shfl_sync(0xFFFFFFFFu, f[6], k);
+        const int prompt = __shfl_sync(0xFFFFFFFFu, prompt_l, k);
+        const int vb = __shfl_sync(0xFFFFFFFFu, vb_l, k);
+        const int voff = __shfl_sync(0xFFFFFFFFu, voff_l, k);
+        mbar_wait(&info_empty[ib], ((unit / kInfo) & 1) ^ 1);
+        UnitInfo& u = info[ib];
+        const int pg0 = key_begin >> p.page_shift;
+        const int npg = min(((key_end - 1) >> p.page_shift) - pg0 + 1, kMaxUnitPages);
+        const int32_t* bt = p.block_tables + static_cast<int64_t>(req) * p.max_pages + pg0;
+        for (int i = lane; i < npg; i += 32) cp_async_4(&u.pages[i], bt + i);
+        for (int i = lane; i < n_tok; i += 32) cp_async_4(&u.qpos[i], p.q_pos + tok_begin + i);
+        const int nw = key_end > vb ? (key_end - vb + 31) / 32 : 0;
+        if (nw <= kMaxUnitWords && lane < nw) cp_async_4(&u.words[lane], p.vis_words + voff + lane);
+        cp_async_arrive_noinc(&info_full[ib]);
+        if (lane < kEpiInts) {
+          const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
+          const int v = lane == 0 ? head : lane == 1 ? tok_begin : lane == 2 ? n_tok
+                      : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
+          epi[(unit % kEpiRing) * kEpiInts + lane] = v;
+        }
+        if (lane < 11) {
+          const int v = lane == 0 ? req : lane == 1 ? head : lane == 2 ? tok_begin : lane == 3 ? n_tok
+                      : lane == 4 ? key_begin : lane == 5 ? key_end : lane == 6 ? slot : lane == 7 ? vb
+                      : lane == 8 ? nw : lane == 9 ? voff : prompt;
+          (&u.req)[lane] = v;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          trace(p, 6, 5 + unit);
+          mbar_arrive(&info_full[ib]);
+        }
       }
-      if (lane == 0) {
-        u.vb = vb;
-        u.n_words = nw;
-        u.vis_off = voff;
-      }
-      __syncwarp();
-      mbar_arrive(&info_full[ib]);
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax + epilogue
@@ -428,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int head = er[0], tok_begin = er[1], n_tok = er[2], slot = er[3];
       const bool valid = row_exists && t_in < n_tok;
       const bool warp_valid = (wq * 32) / G < n_tok;
+      if (threadIdx.x == 0) trace(p, 13, e);
       named_bar_sync(1, 256);
       const float m0 = red[0 * kBlockM + row], m1 = red[1 * kBlockM + row];
       const float l0 = red[2 * kBlockM + row], l1 = red[3 * kBlockM + row];
@@ -436,58 +459,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float w0 = l0 > 0.f ? fast_exp2(m0 - mx) : 0.f;
       const float w1 = l1 > 0.f ? fast_exp2(m1 - mx) : 0.f;
       const float l_tot = w0 * l0 + w1 * l1;
+      const float inv_l = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
+      const float f0 = w0 * (slot < 0 ? inv_l : 1.f), f1 = w1 * (slot < 0 ? inv_l : 1.f);
       mbar_wait(o_full, e & 1);
       tc_fence_after();
+      if (threadIdx.x == 0) trace(p, 14, e);
+      // Drain this warpgroup's half of the merged O (packed to bf16 in registers, or
+      // stored as fp32 split-KV partials), then hand the accumulators back to the MMA
+      // warp before the bf16 output stores.
+      const int tok = tok_begin + t_in;
+      const int qh = head * G + g_in;
+      uint32_t pk[HD / 4] = {};
       if (warp_valid) {
-        const float inv_l = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
-        const float f0 = w0 * (slot < 0 ? inv_l : 1.f), f1 = w1 * (slot < 0 ? inv_l : 1.f);
-        const int tok = tok_begin + t_in;
-        const int qh = head * G + g_in;
 #pragma unroll
-        for (int c0 = 0; c0 < HD / 2; c0 += 32) {
+        for (int c0 = 0; c0 < HD / 2; c0 += 16) {
           const int col = wg * (HD / 2) + c0;
-          uint32_t o0[32], o1[32];
-          tmem_ld32(tm_o0 + lane_off + col, o0);
-          tmem_ld32(tm_o0 + lane_off + HD + col, o1);
+          uint32_t o0[16], o1[16];
+          tmem_ld16(tm_o0 + lane_off + col, o0);
+          tmem_ld16(tm_o0 + lane_off + HD + col, o1);
           tmem_wait_ld();
-          float o[32];
+          float o[16];
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
+          for (int c = 0; c < 16; ++c)
             o[c] = (w0 > 0.f ? __uint_as_float(o0[c]) * f0 : 0.f) +
                    (w1 > 0.f ? __uint_as_float(o1[c]) * f1 : 0.f);
-          if (valid) {
-            if (slot < 0) {
-              uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(tok) * p.out_stride_tok +
-                                                    static_cast<int64_t>(qh) * HD + col);
+          if (slot < 0) {
 #pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                const int c = v * 8;
-                dst[v] = make_uint4(pack_bf16x2(o[c + 0], o[c + 1]), pack_bf16x2(o[c + 2], o[c + 3]),
-                                    pack_bf16x2(o[c + 4], o[c + 5]), pack_bf16x2(o[c + 6], o[c + 7]));
-              }
-            } else {
-              float4* dst = reinterpret_cast<float4*>(
-                  p.ws_o + (static_cast<int64_t>(slot) * kBlockM + row) * HD + col);
+            for (int c = 0; c < 8; ++c) pk[c0 / 2 + c] = pack_bf16x2(o[2 * c], o[2 * c + 1]);
+          } else if (valid) {
+            float4* dst = reinterpret_cast<float4*>(
+                p.ws_o + (static_cast<int64_t>(slot) * kBlockM + row) * HD + col);
 #pragma unroll
-              for (int v = 0; v < 8; ++v)
-                dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
-            }
+            for (int v = 0; v < 4; ++v)
+              dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
           }
-        }
-        if (valid && slot >= 0 && wg == 0) {
-          reinterpret_cast<float2*>(p.ws_ml)[static_cast<int64_t>(slot) * kBlockM + row] =
-              make_float2(mx, l_tot);
         }
       }
       tc_fence_before();
       mbar_arrive(o_empty);
+      if (threadIdx.x == 0) trace(p, 15, e);
+      if (valid) {
+        if (slot < 0) {
+          uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(tok) * p.out_stride_tok +
+                                                static_cast<int64_t>(qh) * HD + wg * (HD / 2));
+#pragma unroll
+          for (int v = 0; v < HD / 16; ++v)
+            dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+        } else if (wg == 0) {
+          reinterpret_cast<float2*>(p.ws_ml)[static_cast<int64_t>(slot) * kBlockM + row] =
+              make_float2(mx, l_tot);
+        }
+      }
     };
     int cw = 0;     // tiles processed by this warpgroup (trace index)
     int tbase = 0;  // stream index of the current item's first tile
     int unit = 0;
     for (int w = w_begin; w < w_end; ++w, ++unit) {
-      const int ib = unit & 1;
-      mbar_wait(&info_full[ib], (unit >> 1) & 1);
+      const int ib = unit % kInfo;
+      mbar_wait(&info_full[ib], (unit / kInfo) & 1);
       const UnitInfo& u = info[ib];
       const int n_tok = u.n_tok;
       const int key_begin = u.key_begin, key_end = u.key_end;
@@ -497,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int vb = u.vb;
       const bool words_smem = u.n_words <= kMaxUnitWords;
       const uint32_t* words = words_smem ? u.words : p.vis_words + u.vis_off;
-      const int lim = valid ? u.lim[t_in] : 0;
+      const int lim = valid ? min(u.prompt + (u.qpos[t_in] / p.block_size + 1) * p.block_size, key_end) : 0;
       float m = -INFINITY;
       float l = 0.f;
       for (int j = wg; j < n_tiles; j += 2, ++cw) {
@@ -746,12 +775,25 @@ int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CU
                       const int32_t* groups, int n_groups, cudaStream_t stream) {
   // 227 KB of shared memory: one Q tile + the K ring + a deeper V ring (a V slot is
   // held until its PV retires, a K slot only until its S does).
-  if (head_dim == 128)
-    return v_fp16 ? launch_attn_t<128, 5, 6, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
-                  : launch_attn_t<128, 5, 6, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+  if (head_dim == 128) {
+    // Shallow rings measured fastest (3/3 vs 5/6: -10% on the ShareGPT batch, -4% at
+    // 4K): every CTA keeps ~96 KB in flight, enough to cover the unloaded HBM latency
+    // at its bandwidth share, while deeper rings only lengthen the DRAM queues that
+    // every dependent step (item start, first tile, tail) waits behind.
+    const char* e = getenv("OPTIMUS_K2_RINGS");  // diagnostics: ring-depth variants
+    const int rings = e ? atoi(e) : 33;
+    if (rings == 44)
+      return v_fp16 ? launch_attn_t<128, 4, 4, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                    : launch_attn_t<128, 4, 4, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+    if (rings == 56)
+      return v_fp16 ? launch_attn_t<128, 5, 6, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                    : launch_attn_t<128, 5, 6, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+    return v_fp16 ? launch_attn_t<128, 3, 3, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                  : launch_attn_t<128, 3, 3, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+  }
   if (head_dim == 64)
-    return v_fp16 ? launch_attn_t<64, 10, 12, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
-                  : launch_attn_t<64, 10, 12, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
+    return v_fp16 ? launch_attn_t<64, 6, 6, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
+                  : launch_attn_t<64, 6, 6, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
   return -1;
 }
 

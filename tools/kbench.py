@@ -19,7 +19,8 @@ ap.add_argument("--layers", type=int, default=36)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--dump", default="")
 ap.add_argument("--ab", action="store_true")
-ap.add_argument("--dbgs", default="0,16")
+ap.add_argument("--dbgs", default="0,16")  # OPTIMUS_DBG[:OPTIMUS_K2_RINGS] per variant
+ap.add_argument("--plans", default="both")
 a = ap.parse_args()
 a.steps = 1
 dev = torch.device("cuda")
@@ -83,10 +84,16 @@ if a.ab:
                                 min_split_tiles=cfg.min_split_tiles, device=dev, page_size=cfg.page_size)
         for dbg in a.dbgs.split(","):
             variants.append((f"plan={force} dbg={dbg} groups={pl.n_groups}", pl, dbg))
+        if a.plans == "whole":
+            break
     os.environ.pop("OPTIMUS_PLAN_FORCE")
     graphs = []
     for name, pl, dbg in variants:
-        os.environ["OPTIMUS_DBG"] = dbg
+        os.environ["OPTIMUS_DBG"] = dbg.split(":")[0]
+        if ":" in dbg:
+            os.environ["OPTIMUS_K2_RINGS"] = dbg.split(":")[1]
+        else:
+            os.environ.pop("OPTIMUS_K2_RINGS", None)
         plan = pl
         out = dec._workspaces(pl, m.n_tok)
         s_ = torch.cuda.Stream(); s_.wait_stream(torch.cuda.current_stream())
