@@ -133,10 +133,58 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total,
                        float* ws_o, float* ws_ml, int v_dtype, void* stream);
 
 /*
+ * K1 folded into K2: the same attention, with the step's new K/V rows (k_new /
+ * v_new [n_tok][Hkv][head_dim] bf16, token stride new_stride_tok elements) scattered
+ * into the pages by rule S inside the attention kernel (no separate append launch).
+ * Requires every (request, KV head) to be a single query tile (max chunk tokens x
+ * Hq/Hkv <= 128), so that the CTA covering a key position is the only reader of the
+ * row it writes.  slot_mapping_out (optional, int64 [n_tok]) as optimus_kv_append.
+ * slot_abs (optional): the step's optimus_slot_mapping output; without it every
+ * launch re-derives positions and slots from q_pos / prompt_len / block_tables.
+ */
+int optimus_paged_attn_append(const void* q, int64_t q_stride_tok, int n_tok_total,
+                              const void* k_new, const void* v_new, int64_t new_stride_tok,
+                              void* k_cache, void* v_cache, int64_t num_pages,
+                              const int32_t* q_pos, const int32_t* prompt_len,
+                              const int32_t* vis_base, const int32_t* vis_off,
+                              const uint32_t* vis_words, const int32_t* block_tables,
+                              int max_pages, const int32_t* work, const int32_t* cta_off, int grid,
+                              const int32_t* groups, int n_groups,
+                              int block_size, int num_q_heads, int num_kv_heads, int head_dim,
+                              int page_size, float sm_scale, void* out, int64_t out_stride_tok,
+                              float* ws_o, float* ws_ml, int v_dtype, int64_t* slot_mapping_out,
+                              const int32_t* slot_abs, void* stream);
+
+/*
+ * The step's slot map for the fused append, computed once per step (rule S):
+ * int32 [n_tok][2]: slot_abs_out[2t] = s = prompt_len[tok_req[t]] + tok_pos[t]
+ * (absolute position), slot_abs_out[2t + 1] = block_tables[r][s / P] * P + s % P.
+ */
+int optimus_slot_mapping(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                         const int32_t* block_tables, int max_pages, int n_tok, int page_size,
+                         int32_t* slot_abs_out, void* stream);
+
+/*
+ * K1 over the step's slot map (optimus_slot_mapping output slot_abs): the same page
+ * writes as optimus_kv_append with one round trip per row (the slot is read, not
+ * derived through tok_req -> prompt_len -> block_tables).  Requires a power-of-two
+ * page_size.
+ */
+int optimus_kv_append_slots(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                            const int32_t* slot_abs, int n_tok, int num_kv_heads, int head_dim,
+                            int page_size, void* k_cache, void* v_cache, int64_t num_pages,
+                            int v_dtype, void* stream);
+
+/*
  * Executor: K1 + K2 for n_layers layers in one call (per-layer device pointers in
  * HOST arrays q[l], k_new[l], v_new[l], k_cache[l], v_cache[l], out[l]; metadata and
  * work list shared).  Enqueues everything on `stream` and returns; used when the
  * per-layer activations are already resident (no model work between the layers).
+ * append_mode: 0 = optimus_kv_append + optimus_paged_attn per layer; 1 = the step's
+ * optimus_slot_mapping once into slot_ws (int32 [n_tok][2], 8-byte aligned), then per
+ * layer an append over that slot map + optimus_paged_attn;
+ * 2 = slot map once, then one optimus_paged_attn_append launch per layer (K1 folded
+ * into K2; same precondition as that call).
  */
 int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k_new,
                         const void* const* v_new, int64_t q_stride_tok, int64_t new_stride_tok,
@@ -148,7 +196,8 @@ int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k
                         const int32_t* cta_off, int grid, const int32_t* groups, int n_groups,
                         int block_size, int num_q_heads, int num_kv_heads, int head_dim,
                         int page_size, float sm_scale, void* const* out, int64_t out_stride_tok,
-                        float* ws_o, float* ws_ml, int v_dtype, void* stream);
+                        float* ws_o, float* ws_ml, int v_dtype, int append_mode, int32_t* slot_ws,
+                        void* stream);
 
 /*
  * K3 — fused confidence-threshold unmask (replaces StochasticOracle.commits,

@@ -48,6 +48,21 @@ SIGNATURES = {
             _vp, _vp, _i32, _vp,        # ws_o, ws_ml, v_dtype, stream
         ],
     ),
+    "optimus_paged_attn_append": (
+        _i32,
+        [
+            _vp, _i64, _i32,            # q, q_stride_tok, n_tok_total
+            _vp, _vp, _i64,             # k_new, v_new, new_stride_tok
+            _vp, _vp, _i64,             # k_cache, v_cache, num_pages
+            _vp, _vp, _vp, _vp, _vp,    # q_pos, prompt_len, vis_base, vis_off, vis_words
+            _vp, _i32,                  # block_tables, max_pages
+            _vp, _vp, _i32,             # work, cta_off, grid
+            _vp, _i32,                  # groups, n_groups
+            _i32, _i32, _i32, _i32, _i32, _f32,  # block_size, Hq, Hkv, head_dim, page_size, sm_scale
+            _vp, _i64,                  # out, out_stride_tok
+            _vp, _vp, _i32, _vp, _vp, _vp,  # ws_o, ws_ml, v_dtype, slot_mapping_out, slot_abs, stream
+        ],
+    ),
     "optimus_unmask_partials": (_i32, [_vp, _i32, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "optimus_unmask_finalize": (
         _i32,
@@ -58,8 +73,10 @@ SIGNATURES = {
         _i32,
         [_i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
          _vp, _i32, _vp, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64, _vp,
-         _vp, _i32, _vp],
+         _vp, _i32, _i32, _vp, _vp],
     ),
+    "optimus_kv_append_slots": (_i32, [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _i32, _vp]),
+    "optimus_slot_mapping": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "optimus_host_plan": (_i32, [_i32, _vp, _i32, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),

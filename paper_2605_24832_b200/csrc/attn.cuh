@@ -27,6 +27,18 @@ struct AttnParams {
   int page_shift;  // log2(page_size)
   int box_rows;    // min(page_size, 64)
   float scale_log2;
+  // fused KV append (K1 folded into K2): the new K/V rows of every query token are
+  // scattered into the pages by the CTA whose work item covers their position
+  // (valid when each (request, KV head) is a single query tile); nullptr = off
+  const void* k_new;
+  const void* v_new;
+  int64_t new_stride_tok;  // elements between tokens in k_new / v_new
+  int64_t* slot_out;       // optional slot mapping output (rule S)
+  const int32_t* slot_abs; // optional per-step {abs pos, slot} per token (else computed)
+  void* k_cache_w;         // the caches the append writes (the K2 inputs k_cache / v_cache)
+  void* v_cache_w;
+  int num_kv_heads;
+  int v_fp16;              // V cache is fp16: convert on the way
   unsigned long long* trace;
   int dbg;  // diagnostics: bit0 skip lo-plane PV, bit1 skip S MMA, bit2 skip softmax math, bit3 skip PV  // optional per-CTA timeline (diagnostics), nullptr in production
 };

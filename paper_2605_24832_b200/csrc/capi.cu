@@ -17,6 +17,10 @@
 
 namespace optimus {
 
+int launch_kv_append_slots(const void*, const void*, int64_t, const int32_t*, int, int, int, int,
+                           void*, void*, int, cudaStream_t);
+int launch_slot_map(const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int,
+                    int32_t*, cudaStream_t);
 int launch_kv_append(const void*, const void*, int64_t, const int32_t*, const int32_t*,
                      const int32_t*, const int32_t*, int, int, int, int, int, void*, void*,
                      int64_t*, int, cudaStream_t);
@@ -188,6 +192,39 @@ int optimus_kv_append(const void* k_new, const void* v_new, int64_t new_stride_t
                        max_pages, n_tok, num_kv_heads, head_dim, page_size, k_cache, v_cache,
                        slot_mapping_out, v_dtype, static_cast<cudaStream_t>(stream)),
       "kv_append");
+}
+
+int optimus_kv_append_slots(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                            const int32_t* slot_abs, int n_tok, int num_kv_heads, int head_dim,
+                            int page_size, void* k_cache, void* v_cache, int64_t num_pages,
+                            int v_dtype, void* stream) {
+  if (v_dtype != 0 && v_dtype != 1) return fail("kv_append_slots: v_dtype must be 0 (bf16) or 1 (fp16)");
+  if (n_tok < 0 || num_kv_heads < 1 || num_pages < 1) return fail("kv_append_slots: bad sizes");
+  if (head_dim % 8 || head_dim < 8) return fail("kv_append_slots: head_dim must be a multiple of 8");
+  if (new_stride_tok < static_cast<int64_t>(num_kv_heads) * head_dim || new_stride_tok % 8)
+    return fail("kv_append_slots: new_stride_tok must be >= Hkv*head_dim and a multiple of 8");
+  if (!page_ok(page_size)) return fail("kv_append_slots: page_size must be a power of two in [8, 1024]");
+  if (n_tok == 0) return 0;
+  if (!k_new || !v_new || !slot_abs || !k_cache || !v_cache) return fail("kv_append_slots: null pointer");
+  if (reinterpret_cast<uintptr_t>(slot_abs) % 8) return fail("kv_append_slots: slot_abs must be 8-byte aligned");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_kv_append_slots(k_new, v_new, new_stride_tok, slot_abs, n_tok, num_kv_heads,
+                                            head_dim, page_size, k_cache, v_cache, v_dtype,
+                                            static_cast<cudaStream_t>(stream)),
+                     "kv_append_slots");
+}
+
+int optimus_slot_mapping(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                         const int32_t* block_tables, int max_pages, int n_tok, int page_size,
+                         int32_t* slot_abs_out, void* stream) {
+  if (n_tok < 0 || max_pages < 1 || page_size < 1) return fail("slot_mapping: bad sizes");
+  if (n_tok == 0) return 0;
+  if (!tok_req || !tok_pos || !prompt_len || !block_tables || !slot_abs_out)
+    return fail("slot_mapping: null pointer");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_slot_map(tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok,
+                                     page_size, slot_abs_out, static_cast<cudaStream_t>(stream)),
+                     "slot_mapping");
 }
 
 namespace {
@@ -405,15 +442,20 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
   return static_cast<int>(P.size());
 }
 
-int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, const void* k_cache,
-                       const void* v_cache, int64_t num_pages, const int32_t* q_pos,
-                       const int32_t* prompt_len, const int32_t* vis_base, const int32_t* vis_off,
-                       const uint32_t* vis_words, const int32_t* block_tables, int max_pages,
-                       const int32_t* work, const int32_t* cta_off, int grid,
-                       const int32_t* groups, int n_groups, int block_size, int hq, int hkv,
-                       int head_dim, int page_size, float sm_scale, void* out,
-                       int64_t out_stride_tok, float* ws_o, float* ws_ml, int v_dtype,
-                       void* stream) {
+}  // extern "C"
+
+// Shared body of optimus_paged_attn and optimus_paged_attn_append (k_new == nullptr:
+// attention only).
+static int paged_attn_impl(const void* q, int64_t q_stride_tok, int n_tok_total, const void* k_cache,
+                           const void* v_cache, int64_t num_pages, const int32_t* q_pos,
+                           const int32_t* prompt_len, const int32_t* vis_base, const int32_t* vis_off,
+                           const uint32_t* vis_words, const int32_t* block_tables, int max_pages,
+                           const int32_t* work, const int32_t* cta_off, int grid,
+                           const int32_t* groups, int n_groups, int block_size, int hq, int hkv,
+                           int head_dim, int page_size, float sm_scale, void* out,
+                           int64_t out_stride_tok, float* ws_o, float* ws_ml, int v_dtype,
+                           const void* k_new, const void* v_new, int64_t new_stride_tok,
+                           int64_t* slot_out, const int32_t* slot_abs, void* stream) {
   if (v_dtype != 0 && v_dtype != 1) return fail("paged_attn: v_dtype must be 0 (bf16) or 1 (fp16)");
   if (head_dim != 64 && head_dim != 128) return fail("paged_attn: head_dim must be 64 or 128");
   if (hkv < 1 || hq % hkv) return fail("paged_attn: Hq must be a multiple of Hkv");
@@ -457,7 +499,23 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
     if (int st = get_map(k_cache, dims, strides, box, &tk)) return st;
     if (int st = get_map(v_cache, dims, strides, box, &tv, v_dtype == 1)) return st;
   }
-  AttnParams prm;
+  if (k_new != nullptr) {
+    if (!v_new) return fail("paged_attn_append: v_new is null");
+    if (new_stride_tok % 8 || new_stride_tok < static_cast<int64_t>(hkv) * head_dim)
+      return fail("paged_attn_append: new_stride_tok must be >= Hkv*head_dim and a multiple of 8");
+    if (reinterpret_cast<uintptr_t>(k_new) % 16 || reinterpret_cast<uintptr_t>(v_new) % 16)
+      return fail("paged_attn_append: k_new / v_new must be 16-byte aligned");
+  }
+  AttnParams prm{};
+  prm.k_new = k_new;
+  prm.v_new = v_new;
+  prm.new_stride_tok = new_stride_tok;
+  prm.slot_out = slot_out;
+  prm.slot_abs = slot_abs;
+  prm.num_kv_heads = hkv;
+  prm.v_fp16 = v_dtype == 1;
+  prm.k_cache_w = const_cast<void*>(k_cache);
+  prm.v_cache_w = const_cast<void*>(v_cache);
   prm.q_pos = q_pos;
   prm.prompt_len = prompt_len;
   prm.vis_base = vis_base;
@@ -489,6 +547,43 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
                      "paged_attn");
 }
 
+extern "C" {
+
+int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, const void* k_cache,
+                       const void* v_cache, int64_t num_pages, const int32_t* q_pos,
+                       const int32_t* prompt_len, const int32_t* vis_base, const int32_t* vis_off,
+                       const uint32_t* vis_words, const int32_t* block_tables, int max_pages,
+                       const int32_t* work, const int32_t* cta_off, int grid,
+                       const int32_t* groups, int n_groups, int block_size, int hq, int hkv,
+                       int head_dim, int page_size, float sm_scale, void* out,
+                       int64_t out_stride_tok, float* ws_o, float* ws_ml, int v_dtype,
+                       void* stream) {
+  return paged_attn_impl(q, q_stride_tok, n_tok_total, k_cache, v_cache, num_pages, q_pos, prompt_len,
+                         vis_base, vis_off, vis_words, block_tables, max_pages, work, cta_off, grid,
+                         groups, n_groups, block_size, hq, hkv, head_dim, page_size, sm_scale, out,
+                         out_stride_tok, ws_o, ws_ml, v_dtype, nullptr, nullptr, 0, nullptr, nullptr,
+                         stream);
+}
+
+int optimus_paged_attn_append(const void* q, int64_t q_stride_tok, int n_tok_total,
+                              const void* k_new, const void* v_new, int64_t new_stride_tok,
+                              void* k_cache, void* v_cache, int64_t num_pages,
+                              const int32_t* q_pos, const int32_t* prompt_len,
+                              const int32_t* vis_base, const int32_t* vis_off,
+                              const uint32_t* vis_words, const int32_t* block_tables,
+                              int max_pages, const int32_t* work, const int32_t* cta_off, int grid,
+                              const int32_t* groups, int n_groups, int block_size, int hq, int hkv,
+                              int head_dim, int page_size, float sm_scale, void* out,
+                              int64_t out_stride_tok, float* ws_o, float* ws_ml, int v_dtype,
+                              int64_t* slot_mapping_out, const int32_t* slot_abs, void* stream) {
+  if (!k_new) return fail("paged_attn_append: k_new is null");
+  return paged_attn_impl(q, q_stride_tok, n_tok_total, k_cache, v_cache, num_pages, q_pos, prompt_len,
+                         vis_base, vis_off, vis_words, block_tables, max_pages, work, cta_off, grid,
+                         groups, n_groups, block_size, hq, hkv, head_dim, page_size, sm_scale, out,
+                         out_stride_tok, ws_o, ws_ml, v_dtype, k_new, v_new, new_stride_tok,
+                         slot_mapping_out, slot_abs, stream);
+}
+
 int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k_new,
                         const void* const* v_new, int64_t q_stride_tok, int64_t new_stride_tok,
                         int n_tok_total, int n_tok, void* const* k_cache, void* const* v_cache,
@@ -499,10 +594,42 @@ int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k
                         const int32_t* cta_off, int grid, const int32_t* groups, int n_groups,
                         int block_size, int hq, int hkv, int head_dim, int page_size,
                         float sm_scale, void* const* out, int64_t out_stride_tok, float* ws_o,
-                        float* ws_ml, int v_dtype, void* stream) {
+                        float* ws_ml, int v_dtype, int append_mode, int32_t* slot_ws,
+                        void* stream) {
   if (n_layers < 0 || !q || !k_new || !v_new || !k_cache || !v_cache || !out)
     return fail("attn_layers: bad layer arrays");
+  if (append_mode < 0 || append_mode > 2) return fail("attn_layers: append_mode must be 0, 1 or 2");
+  if (append_mode != 0 && slot_ws == nullptr) return fail("attn_layers: append_mode 1/2 needs slot_ws");
+  if (append_mode != 0 && n_tok > 0) {
+    // the step's slot map once (rule S), shared by every layer's append
+    const int st = optimus_slot_mapping(tok_req, q_pos, prompt_len, block_tables, max_pages, n_tok,
+                                        page_size, slot_ws, stream);
+    if (st) return st;
+  }
   for (int l = 0; l < n_layers; ++l) {
+    if (append_mode == 1) {
+      int st = cuda_status(launch_kv_append_slots(k_new[l], v_new[l], new_stride_tok, slot_ws, n_tok,
+                                                  hkv, head_dim, page_size, k_cache[l], v_cache[l],
+                                                  v_dtype == 1, static_cast<cudaStream_t>(stream)),
+                           "kv_append_slots");
+      if (st) return st;
+      st = optimus_paged_attn(q[l], q_stride_tok, n_tok_total, k_cache[l], v_cache[l], num_pages, q_pos,
+                              prompt_len, vis_base, vis_off, vis_words, block_tables, max_pages, work,
+                              cta_off, grid, groups, n_groups, block_size, hq, hkv, head_dim,
+                              page_size, sm_scale, out[l], out_stride_tok, ws_o, ws_ml, v_dtype, stream);
+      if (st) return st;
+      continue;
+    }
+    if (append_mode == 2) {
+      // K1 folded into K2 (caller guarantees one query tile per (request, KV head))
+      const int st = optimus_paged_attn_append(
+          q[l], q_stride_tok, n_tok_total, k_new[l], v_new[l], new_stride_tok, k_cache[l], v_cache[l],
+          num_pages, q_pos, prompt_len, vis_base, vis_off, vis_words, block_tables, max_pages, work,
+          cta_off, grid, groups, n_groups, block_size, hq, hkv, head_dim, page_size, sm_scale, out[l],
+          out_stride_tok, ws_o, ws_ml, v_dtype, nullptr, slot_ws, stream);
+      if (st) return st;
+      continue;
+    }
     int st = optimus_kv_append(k_new[l], v_new[l], new_stride_tok, tok_req, q_pos, prompt_len,
                                block_tables, max_pages, n_tok, hkv, head_dim, page_size,
                                k_cache[l], v_cache[l], num_pages, nullptr, v_dtype, stream);

@@ -79,4 +79,77 @@ int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_to
   return static_cast<int>(cudaGetLastError());
 }
 
+// K1 over a precomputed per-step slot map (optimus_slot_mapping): one round trip
+// (slot + row loads in parallel) instead of the tok_req -> prompt -> block-table chain.
+__global__ void __launch_bounds__(256) kv_append_slots_kernel(
+    const uint4* __restrict__ k_new, const uint4* __restrict__ v_new, int64_t new_stride_vec,
+    const int2* __restrict__ slot_abs, int n_tok, int hkv, int vec_per_head, int page_size,
+    int page_shift, uint4* __restrict__ k_cache, uint4* __restrict__ v_cache, int v_fp16) {
+  grid_dep_launch();
+  const int per_tok = hkv * vec_per_head;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= static_cast<int64_t>(n_tok) * per_tok) return;
+  const int t = static_cast<int>(gid / per_tok);
+  const int i = static_cast<int>(gid - static_cast<int64_t>(t) * per_tok);
+  const int h = i / vec_per_head;
+  const int c = i - h * vec_per_head;
+  const int slot = __ldg(slot_abs + t).y;
+  const int64_t src = static_cast<int64_t>(t) * new_stride_vec + i;
+  const uint4 kv = __ldg(k_new + src);
+  const uint4 vv = __ldg(v_new + src);
+  const int64_t dst = ((static_cast<int64_t>(slot >> page_shift) * hkv + h) * page_size +
+                       (slot & (page_size - 1))) * vec_per_head + c;
+  k_cache[dst] = kv;
+  if (v_fp16) {
+    const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+    uint32_t hh[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float lo = __uint_as_float(w[k] << 16), hi = __uint_as_float(w[k] & 0xFFFF0000u);
+      asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(hh[k]) : "f"(hi), "f"(lo));
+    }
+    v_cache[dst] = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+  } else {
+    v_cache[dst] = vv;
+  }
+}
+
+int launch_kv_append_slots(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                           const int32_t* slot_abs, int n_tok, int hkv, int head_dim, int page_size,
+                           void* k_cache, void* v_cache, int v_fp16, cudaStream_t stream) {
+  if (n_tok == 0) return 0;
+  const int vec_per_head = head_dim / 8;
+  const int64_t total = static_cast<int64_t>(n_tok) * hkv * vec_per_head;
+  const int blocks = static_cast<int>((total + 255) / 256);
+  kv_append_slots_kernel<<<blocks, 256, 0, stream>>>(
+      static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
+      reinterpret_cast<const int2*>(slot_abs), n_tok, hkv, vec_per_head, page_size,
+      __builtin_ctz(static_cast<unsigned>(page_size)), static_cast<uint4*>(k_cache),
+      static_cast<uint4*>(v_cache), v_fp16);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Per-step slot map for the fused append (K2 with k_new): out[t] = {prompt + pos,
+// slot} (rule S), computed once per step instead of in every layer's kernel.
+__global__ void __launch_bounds__(256) slot_map_kernel(
+    const int32_t* __restrict__ tok_req, const int32_t* __restrict__ tok_pos,
+    const int32_t* __restrict__ prompt_len, const int32_t* __restrict__ block_tables, int max_pages,
+    int n_tok, int page_size, int32_t* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tok) return;
+  const int r = __ldg(tok_req + t);
+  const int s = __ldg(prompt_len + r) + __ldg(tok_pos + t);
+  const int page = __ldg(block_tables + static_cast<int64_t>(r) * max_pages + s / page_size);
+  reinterpret_cast<int2*>(out)[t] = make_int2(s, page * page_size + s % page_size);
+}
+
+int launch_slot_map(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                    const int32_t* block_tables, int max_pages, int n_tok, int page_size,
+                    int32_t* out, cudaStream_t stream) {
+  if (n_tok == 0) return 0;
+  slot_map_kernel<<<(n_tok + 255) / 256, 256, 0, stream>>>(tok_req, tok_pos, prompt_len, block_tables,
+                                                           max_pages, n_tok, page_size, out);
+  return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace optimus

@@ -45,7 +45,8 @@ constexpr int kSBuf = 3;       // S/P buffers in TMEM, rotating over the CTA's t
 constexpr int kInfo = 4;       // staged work-item records: the metadata warp runs 3 items ahead
 constexpr int kEpiRing = 8;    // per-item epilogue records (outlive the staged record)
 static_assert(kEpiRing > kInfo + 1, "epilogue records must outlive the staging ring");
-constexpr int kTraceSlots = 4096;  // per CTA: [role*256 + i], 16 roles
+constexpr int kTraceSlots = 4096;
+constexpr int kAppItems = 64;  // work records per fused-append batch  // per CTA: [role*256 + i], 16 roles
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -92,8 +93,9 @@ struct AttnSmem {
   static constexpr uint32_t OFF_INFO = OFF_V + VST * KT_BYTES;
   static constexpr uint32_t OFF_RED = OFF_INFO + kInfo * sizeof(UnitInfo);  // float[{m,l}][wg][128]
   static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * kBlockM * 4;
-  static constexpr uint32_t OFF_BAR = OFF_EPI + kEpiRing * kEpiInts * 4;
-  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 2 + 2 * kInfo;
+  static constexpr uint32_t OFF_APP = OFF_EPI + kEpiRing * kEpiInts * 4;  // fused-append scratch
+  static constexpr uint32_t OFF_BAR = (OFF_APP + (kAppItems * 9 + 1) * 4 + 15) / 16 * 16;
+  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 2 + 2 * kInfo + 2;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
@@ -132,7 +134,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_empty = o_full + 1;
   uint64_t* info_full = o_empty + 1;
   uint64_t* info_empty = info_full + kInfo;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(info_empty + kInfo);
+  uint64_t* append_done = info_empty + kInfo;  // fused KV append of this CTA's items landed
+  uint64_t* append_issued = append_done + 1;   // ... and its first loads are in flight
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(append_issued + 1);
   UnitInfo* info = reinterpret_cast<UnitInfo*>(smem + L::OFF_INFO);
   float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // epilogue (m, l) exchange
   int* epi = reinterpret_cast<int*>(smem + L::OFF_EPI);
@@ -168,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(o_full, 1);
     mbar_init(o_empty, 256);
+    mbar_init(append_done, 256);
+    mbar_init(append_issued, 256);
     mbar_fence_init();
   }
   if (warp == 10) tmem_alloc<L::TMEM_COLS>(tmem_slot);
@@ -211,6 +217,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_stream = l2_policy_evict_first();
     int tile_ctr = 0;
     int unit = 0;
+    bool need_append = p.k_new != nullptr;  // output-region tiles wait for the fused append
+    if (need_append) {
+      // the append's loads go first; (diagnostics, dbg 64: no load before it landed)
+      mbar_wait((p.dbg & 64) ? append_done : append_issued, 0);
+      if (p.dbg & 64) need_append = false;
+    }
     for (int w = w_begin; w < w_end; ++w, ++unit) {
       const int ib = unit % kInfo;
       mbar_wait(&info_full[ib], (unit / kInfo) & 1);
@@ -222,6 +234,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int key_begin = __shfl_sync(0xFFFFFFFFu, u.key_begin, 0);
       const int key_end = __shfl_sync(0xFFFFFFFFu, u.key_end, 0);
       const int pg0 = key_begin >> shift;
+      // first key this step appends in this item's range: tiles below it never wait
+      // for the fused append (new rows are the recomputed kv positions + the window)
+      int first_new = 0x7FFFFFFF;
+      if (need_append) {
+        const int n_tok_u = __shfl_sync(0xFFFFFFFFu, u.n_tok, 0);
+        for (int i = lane; i < n_tok_u; i += 32) first_new = min(first_new, u.qpos[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) first_new = min(first_new, __shfl_xor_sync(0xFFFFFFFFu, first_new, o));
+        first_new += __shfl_sync(0xFFFFFFFFu, u.prompt, 0);
+      }
       if (is_k) {
         const int tok_begin = __shfl_sync(0xFFFFFFFFu, u.tok_begin, 0);
         mbar_wait(q_empty, (unit & 1) ^ 1);
@@ -237,6 +259,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
         if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
         if (is_k && lane == 0) trace(p, 0, tile_ctr);
+        if (need_append && kt + kTileN > first_new) {
+          // this tile holds rows appended in this step: wait for the append once
+          mbar_wait(append_done, 0);
+          need_append = false;
+        }
         mbar_wait(&empty[st], ((tile_ctr / NST) & 1) ^ 1);
         if (lane == 0) trace(p, is_k ? 4 : 10, tile_ctr);
         uint8_t* dst = ring + st * L::KT_BYTES;
@@ -511,6 +538,114 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
+    if (p.k_new != nullptr) {
+      // Fused KV append (K1): while the first tiles are in flight, the softmax
+      // threads scatter the new K/V rows of this CTA's items into the pages.  Item i
+      // appends token t for its head iff s = prompt + q_pos[t] lies in its key
+      // range: the pieces of a (request, head) partition its keys, so every appended
+      // row is read only by the CTA that wrote it.  One warp per (item, token) pair,
+      // lanes [0, HD/8) copy K and [HD/8, HD/4) copy V in 16-byte vectors.
+      grid_dep_wait();  // k_new / v_new are written by the preceding kernel
+      if (threadIdx.x == 0) trace(p, 6, 250);
+      int* app = reinterpret_cast<int*>(smem + L::OFF_APP);  // [kAppItems][8] + prefix
+      int* pre = app + kAppItems * 8;
+      constexpr int VPH = HD / 8;
+      const int hkv = p.num_kv_heads;
+      bool issued = false;
+      for (int base = w_begin; base < w_end; base += kAppItems) {
+        const int nb = min(kAppItems, w_end - base);
+        if (threadIdx.x < nb) {
+          const int4* wp = reinterpret_cast<const int4*>(p.work + 8 * (base + threadIdx.x));
+          const int4 a = __ldg(wp), b = __ldg(wp + 1);
+          int* r = app + 8 * threadIdx.x;
+          r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y;
+          r[6] = p.slot_abs != nullptr ? 0 : __ldg(p.prompt_len + a.x);
+        }
+        named_bar_sync(1, 256);
+        if (threadIdx.x == 0) {
+          int acc = 0;
+          for (int i = 0; i < nb; ++i) {
+            pre[i] = acc;
+            acc += app[8 * i + 3];
+          }
+          pre[nb] = acc;
+        }
+        named_bar_sync(1, 256);
+        const int total = pre[nb];
+        const int kind = lane / VPH;  // 0: K row, 1: V row, else idle
+        const int c = lane - kind * VPH;
+        // B pairs per warp per pass: all of a pass's loads are issued before any
+        // store, and the first pass's issue releases the TMA producers (so these
+        // loads sit ahead of the page stream in the DRAM queues)
+        constexpr int B = 12;
+        for (int q0 = warp; q0 < total; q0 += 8 * B) {
+          uint4 val[B];
+          int2 sa[B];  // {absolute position, slot}; x = -1: nothing to write
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            const int q = q0 + 8 * k;
+            sa[k] = make_int2(-1, 0);
+            if (q < total && kind < 2) {
+              int it = 0;
+              while (it + 1 < nb && pre[it + 1] <= q) ++it;
+              const int* r = app + 8 * it;
+              const int tok = r[2] + (q - pre[it]);
+              const void* src = kind == 0 ? p.k_new : p.v_new;
+              val[k] = __ldg(reinterpret_cast<const uint4*>(src) +
+                             (static_cast<int64_t>(tok) * p.new_stride_tok + r[1] * HD) / 8 + c);
+              if (p.slot_abs != nullptr) {
+                // per-step slot map: one round trip, in parallel with the row load
+                sa[k] = __ldg(reinterpret_cast<const int2*>(p.slot_abs) + tok);
+              } else {
+                const int s_abs = r[6] + __ldg(p.q_pos + tok);
+                const int page = __ldg(p.block_tables + static_cast<int64_t>(r[0]) * p.max_pages +
+                                       (s_abs >> p.page_shift));
+                sa[k] = make_int2(s_abs, page * p.page_size + (s_abs & (p.page_size - 1)));
+              }
+            }
+          }
+          if (!issued) {
+            mbar_arrive(append_issued);
+            issued = true;
+          }
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            const int q = q0 + 8 * k;
+            if (sa[k].x < 0) continue;
+            int it = 0;
+            while (it + 1 < nb && pre[it + 1] <= q) ++it;
+            const int* r = app + 8 * it;
+            if (sa[k].x < r[4] || sa[k].x >= r[5]) continue;  // another piece's key range
+            const int tok = r[2] + (q - pre[it]);
+            const int head = r[1];
+            const int slot = sa[k].y;
+            const int64_t page = slot >> p.page_shift;
+            const int off = slot & (p.page_size - 1);
+            const int64_t dst = ((page * hkv + head) * p.page_size + off) * VPH + c;
+            if (kind == 0) {
+              reinterpret_cast<uint4*>(p.k_cache_w)[dst] = val[k];
+              if (head == 0 && c == 0 && p.slot_out != nullptr) p.slot_out[tok] = slot;
+            } else if (p.v_fp16) {
+              const uint32_t w4[4] = {val[k].x, val[k].y, val[k].z, val[k].w};
+              uint32_t hv[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float lo = __uint_as_float(w4[i] << 16), hi = __uint_as_float(w4[i] & 0xFFFF0000u);
+                asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(hv[i]) : "f"(hi), "f"(lo));
+              }
+              reinterpret_cast<uint4*>(p.v_cache_w)[dst] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            } else {
+              reinterpret_cast<uint4*>(p.v_cache_w)[dst] = val[k];
+            }
+          }
+        }
+        named_bar_sync(1, 256);  // scratch reused by the next batch
+      }
+      if (!issued) mbar_arrive(append_issued);
+      fence_proxy_async_global();
+      mbar_arrive(append_done);
+      if (threadIdx.x == 0) trace(p, 6, 251);
+    }
     int cw = 0;     // tiles processed by this warpgroup (trace index)
     int tbase = 0;  // stream index of the current item's first tile
     int unit = 0;

@@ -70,6 +70,11 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- fences
+// Order this thread's generic-proxy global writes before later async-proxy (TMA)
+// reads of the same memory (published to other threads through an mbarrier).
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

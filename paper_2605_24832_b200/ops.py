@@ -62,8 +62,11 @@ def kv_append(
     v_cache: torch.Tensor,
     slot_mapping_out: Optional[torch.Tensor] = None,
     stream=None,
+    slot_abs: Optional[torch.Tensor] = None,
 ) -> None:
-    """Scatter ``k_new``/``v_new`` ``[n_tok, Hkv, d]`` into ``[num_pages, Hkv, P, d]`` caches."""
+    """Scatter ``k_new``/``v_new`` ``[n_tok, Hkv, d]`` into ``[num_pages, Hkv, P, d]`` caches.
+    With ``slot_abs`` (the step's :func:`slot_mapping`) the slots are read, not
+    re-derived (``optimus_kv_append_slots``)."""
     _cuda(k_new, v_new, tok_req, tok_pos, prompt_len, block_tables, k_cache, v_cache, slot_mapping_out)
     n_tok = k_new.shape[0]
     num_pages, hkv, page, d = k_cache.shape
@@ -71,6 +74,15 @@ def kv_append(
         raise ConfigError("kv_append: new K/V rows and the K cache are bf16")
     if k_new.stride(-1) != 1 or k_new.stride(-2) != d or v_new.stride(0) != k_new.stride(0):
         raise ConfigError("kv_append: K/V rows must be [n_tok, Hkv, d] with unit inner strides")
+    if slot_abs is not None:
+        _cuda(slot_abs)
+        if slot_mapping_out is not None:
+            raise ConfigError("kv_append: slot_mapping_out is the slot map itself with slot_abs")
+        st = _lib.call("optimus_kv_append_slots", _ptr(k_new), _ptr(v_new), k_new.stride(0), _ptr(slot_abs),
+                       n_tok, hkv, d, page, _ptr(k_cache), _ptr(v_cache), num_pages, _v_dtype(v_cache),
+                       _stream(stream))
+        _lib.check(st, "optimus_kv_append_slots")
+        return
     st = _lib.call(
         "optimus_kv_append",
         _ptr(k_new), _ptr(v_new), k_new.stride(0),
@@ -80,6 +92,30 @@ def kv_append(
         _stream(stream),
     )
     _lib.check(st, "optimus_kv_append")
+
+
+def slot_mapping(
+    tok_req: torch.Tensor,
+    tok_pos: torch.Tensor,
+    prompt_len: torch.Tensor,
+    block_tables: torch.Tensor,
+    page_size: int,
+    n_tok: Optional[int] = None,
+    out: Optional[torch.Tensor] = None,
+    stream=None,
+) -> torch.Tensor:
+    """Rule S once per step: int32 ``[n_tok, 2]`` = (absolute position, slot) for the
+    first ``n_tok`` tokens (default: all of ``tok_req``)."""
+    _cuda(tok_req, tok_pos, prompt_len, block_tables, out)
+    n_tok = tok_req.shape[0] if n_tok is None else int(n_tok)
+    if n_tok > tok_req.shape[0] or n_tok > tok_pos.shape[0]:
+        raise ConfigError("slot_mapping: n_tok exceeds the token arrays")
+    if out is None:
+        out = torch.empty((max(n_tok, 1), 2), dtype=torch.int32, device=tok_req.device)
+    st = _lib.call("optimus_slot_mapping", _ptr(tok_req), _ptr(tok_pos), _ptr(prompt_len),
+                   _ptr(block_tables), block_tables.shape[1], n_tok, page_size, _ptr(out), _stream(stream))
+    _lib.check(st, "optimus_slot_mapping")
+    return out
 
 
 # --------------------------------------------------------------------------- K2 plan
@@ -97,6 +133,16 @@ class AttnPlan:
     work_host: np.ndarray
     cta_off_host: np.ndarray
     groups_host: np.ndarray
+    single_tile: bool = False  # every (request, KV head) is one query tile: K1 may fold into K2
+
+
+def single_query_tile(work_host: np.ndarray) -> bool:
+    """True when no request's query tokens span two tiles (one tok_begin per request),
+    the precondition of the fused append (optimus_paged_attn_append)."""
+    if len(work_host) == 0:
+        return True
+    pairs = np.unique(work_host[:, [0, 2]], axis=0)
+    return len(pairs) == len(np.unique(pairs[:, 0]))
 
 
 def plan_attention(
@@ -145,7 +191,8 @@ def plan_attention(
         dev_work = torch.from_numpy(work).to(device)
         dev_off = torch.from_numpy(cta_off).to(device)
         dev_groups = torch.from_numpy(groups).to(device)
-    return AttnPlan(grid, n, ng.value, npart.value, dev_work, dev_off, dev_groups, work, cta_off, groups)
+    return AttnPlan(grid, n, ng.value, npart.value, dev_work, dev_off, dev_groups, work, cta_off, groups,
+                    single_query_tile(work))
 
 
 # --------------------------------------------------------------------------- K2
@@ -203,6 +250,79 @@ def paged_attention(
         _v_dtype(v_cache), _stream(stream),
     )
     _lib.check(st, "optimus_paged_attn")
+    return out
+
+
+def paged_attention_append(
+    q: torch.Tensor,
+    k_new: torch.Tensor,
+    v_new: torch.Tensor,
+    k_cache: torch.Tensor,
+    v_cache: torch.Tensor,
+    q_pos: torch.Tensor,
+    prompt_len: torch.Tensor,
+    vis_base: torch.Tensor,
+    vis_off: torch.Tensor,
+    vis_words: torch.Tensor,
+    block_tables: torch.Tensor,
+    plan: AttnPlan,
+    block_size: int,
+    sm_scale: Optional[float] = None,
+    out: Optional[torch.Tensor] = None,
+    ws_o: Optional[torch.Tensor] = None,
+    ws_ml: Optional[torch.Tensor] = None,
+    slot_mapping_out: Optional[torch.Tensor] = None,
+    slot_abs: Optional[torch.Tensor] = None,
+    stream=None,
+) -> torch.Tensor:
+    """K1 folded into K2 (``optimus_paged_attn_append``): append ``k_new``/``v_new``
+    ``[n_tok, Hkv, d]`` into the pages (rule S) and attend, in one launch.  Same
+    result as :func:`kv_append` followed by :func:`paged_attention`; requires
+    ``plan.single_tile`` (no request's query tokens span two MMA tiles).  ``slot_abs``:
+    the step's :func:`slot_mapping` (else every launch re-derives the slots)."""
+    _cuda(q, k_new, v_new, k_cache, v_cache, q_pos, prompt_len, vis_base, vis_off, vis_words,
+          block_tables, out, slot_mapping_out)
+    if not plan.single_tile:
+        raise ConfigError("paged_attention_append: a request's query tokens span two query tiles "
+                          "(chunk x Hq/Hkv > 128); use kv_append + paged_attention")
+    n_tok, hq, d = q.shape
+    num_pages, hkv, page, d2 = k_cache.shape
+    if d2 != d or k_new.shape[-1] != d or k_new.shape[-2] != hkv:
+        raise ConfigError("paged_attention_append: head_dim / kv-head mismatch")
+    if q.stride(-1) != 1 or q.stride(-2) != d:
+        raise ConfigError("paged_attention_append: q must be [n_tok, Hq, d] with unit inner strides")
+    if k_new.stride() != v_new.stride() or k_new.stride(-1) != 1 or k_new.stride(-2) != d:
+        raise ConfigError("paged_attention_append: k_new/v_new must be [n_tok, Hkv, d] with equal strides")
+    if k_new.dtype != torch.bfloat16 or v_new.dtype != torch.bfloat16:
+        raise ConfigError("paged_attention_append: k_new/v_new must be bf16")
+    if slot_mapping_out is not None and (slot_mapping_out.dtype != torch.int64 or slot_mapping_out.numel() < n_tok):
+        raise ConfigError("paged_attention_append: slot_mapping_out must be int64 [n_tok]")
+    if out is None:
+        out = torch.empty((n_tok, hq, d), dtype=torch.bfloat16, device=q.device)
+    if plan.n_partials > 0:
+        need_o = plan.n_partials * 128 * d
+        need_ml = plan.n_partials * 128 * 2
+        if ws_o is None or ws_o.numel() < need_o:
+            ws_o = torch.empty(need_o, dtype=torch.float32, device=q.device)
+        if ws_ml is None or ws_ml.numel() < need_ml:
+            ws_ml = torch.empty(need_ml, dtype=torch.float32, device=q.device)
+    scale = float(sm_scale) if sm_scale is not None else 1.0 / float(d) ** 0.5
+    st = _lib.call(
+        "optimus_paged_attn_append",
+        _ptr(q), q.stride(0), n_tok,
+        _ptr(k_new), _ptr(v_new), k_new.stride(0),
+        _ptr(k_cache), _ptr(v_cache), num_pages,
+        _ptr(q_pos), _ptr(prompt_len), _ptr(vis_base), _ptr(vis_off), _ptr(vis_words),
+        _ptr(block_tables), block_tables.shape[1],
+        _ptr(plan.work), _ptr(plan.cta_off), plan.grid if plan.n_work else 0,
+        _ptr(plan.groups), plan.n_groups,
+        block_size, hq, hkv, d, page, scale,
+        _ptr(out), out.stride(0),
+        _ptr(ws_o) if plan.n_partials else None, _ptr(ws_ml) if plan.n_partials else None,
+        _v_dtype(v_cache), _ptr(slot_mapping_out) if slot_mapping_out is not None else None,
+        _ptr(slot_abs), _stream(stream),
+    )
+    _lib.check(st, "optimus_paged_attn_append")
     return out
 
 

@@ -60,16 +60,27 @@ def _run_append(s):
     return kc, vc, slots
 
 
+@pytest.mark.parametrize("slot_map", [False, True])
 @pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("page,d,hkv", [(16, 128, 8), (64, 128, 2), (16, 64, 4), (32, 64, 2)])
-def test_kv_append_bit_exact(page, d, hkv, v_dtype):
+def test_kv_append_bit_exact(page, d, hkv, v_dtype, slot_map):
     s = _step(1, 9, 8, 32, page, hkv * 2, hkv, d, v_dtype=v_dtype)
     # include values outside the fp16 range: the fp16 V cache saturates them
     s["v_new"][0, 0, :4] = torch.tensor([1e6, -1e6, 70000.0, 3.0e-8], dtype=torch.bfloat16)
-    kc, vc, slots = _run_append(s)
-    torch.cuda.synchronize()
     m = s["meta"]
     ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.block_tables, page)
+    if slot_map:
+        # K1 over the step's slot map (optimus_slot_mapping + optimus_kv_append_slots)
+        dev = torch.device("cuda")
+        dm = s["dm"]
+        sa = ops.slot_mapping(dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, page, n_tok=m.n_tok)
+        kc, vc = s["k_cache"].to(dev), s["v_cache"].to(dev)
+        ops.kv_append(s["k_new"].to(dev)[: m.n_tok], s["v_new"].to(dev)[: m.n_tok], dm.tok_req, dm.tok_pos,
+                      dm.prompt_len, dm.block_tables, kc, vc, slot_abs=sa)
+        slots = sa[:, 1].long()
+    else:
+        kc, vc, slots = _run_append(s)
+    torch.cuda.synchronize()
     assert np.array_equal(slots.cpu().numpy()[: m.n_tok], ref_slots)
     k_ref = s["k_cache"].view(torch.int16).numpy().copy()
     v_ref = s["v_cache"].view(torch.int16).numpy().copy()
@@ -201,3 +212,68 @@ def test_unmask_vocab_parallel_merge_equals_single():
     sharded = ops.unmask_finalize(torch.stack([p0, p1]), 2, n, 2, cu, 0.9)
     assert torch.equal(full.tokens[:n], sharded.tokens[:n])
     torch.testing.assert_close(full.conf[:n], sharded.conf[:n], rtol=1e-5, atol=0)
+
+
+@pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("case", ["sdar8b", "d64_g1", "d64_g2", "page128", "split_kv", "one_cta", "out_block"])
+def test_fused_append_equals_k1_then_k2(case, v_dtype):
+    """K1 folded into K2 (optimus_paged_attn_append) writes exactly K1's pages and slot
+    mapping and returns bit-identical attention outputs, including cut (split-KV)
+    items, where only the piece covering a position appends it."""
+    cfg = {
+        "sdar8b": dict(seed=31, n_req=14, chunk=32, page=64, hq=32, hkv=8, d=128),
+        "d64_g1": dict(seed=32, n_req=9, chunk=8, page=16, hq=4, hkv=4, d=64),
+        "d64_g2": dict(seed=33, n_req=9, chunk=16, page=16, hq=4, hkv=2, d=64),
+        "page128": dict(seed=34, n_req=7, chunk=16, page=128, hq=8, hkv=8, d=128),
+        "split_kv": dict(seed=35, n_req=5, chunk=8, page=64, hq=32, hkv=8, d=128, prompt_range=(4096, 9000),
+                         out_range=(20, 120)),
+        "one_cta": dict(seed=36, n_req=10, chunk=8, page=16, hq=32, hkv=8, d=128, grid=1),
+        "out_block": dict(seed=37, n_req=12, chunk=16, page=16, hq=32, hkv=8, d=128, rule="out_block"),
+    }[case]
+    grid = cfg.pop("grid", None)
+    seed, n_req, chunk, page, hq, hkv, d = (cfg.pop(k) for k in ("seed", "n_req", "chunk", "page", "hq", "hkv", "d"))
+    s = _step(seed, n_req, chunk, 32, page, hq, hkv, d, v_dtype=v_dtype, **cfg)
+    dev = torch.device("cuda")
+    m = s["meta"]
+    plan = ops.plan_attention(m.cu_seqlens, m.key_end, hq, hkv, grid=grid, min_split_tiles=4, device=dev,
+                              page_size=page)
+    assert plan.single_tile
+    if case == "split_kv":
+        assert plan.n_groups > 0
+    q = s["q"].to(dev)[: m.n_tok]
+    dm = s["dm"]
+    kc1, vc1, slots1 = _run_append(s)
+    out1 = ops.paged_attention(q, kc1, vc1, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off,
+                               dm.vis_words, dm.block_tables, plan, s["block"])
+    kc2, vc2 = s["k_cache"].to(dev), s["v_cache"].to(dev)
+    slots2 = torch.full_like(slots1, -1)
+    slot_abs = None
+    if case in ("sdar8b", "split_kv", "one_cta", "d64_g2"):
+        # the per-step slot map (optimus_slot_mapping) instead of in-kernel derivation
+        slot_abs = ops.slot_mapping(dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, page, n_tok=m.n_tok)
+        ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.block_tables, page)
+        assert np.array_equal(slot_abs[:, 1].cpu().numpy()[: m.n_tok], ref_slots)
+        assert np.array_equal(slot_abs[:, 0].cpu().numpy()[: m.n_tok], m.prompt_len[m.tok_req] + m.tok_pos)
+    out2 = ops.paged_attention_append(q, s["k_new"].to(dev)[: m.n_tok], s["v_new"].to(dev)[: m.n_tok], kc2, vc2,
+                                      dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off, dm.vis_words,
+                                      dm.block_tables, plan, s["block"], slot_mapping_out=slots2,
+                                      slot_abs=slot_abs)
+    torch.cuda.synchronize()
+    assert torch.equal(kc1.view(torch.int16), kc2.view(torch.int16))
+    assert torch.equal(vc1.view(torch.int16), vc2.view(torch.int16))
+    assert torch.equal(slots1[: m.n_tok], slots2[: m.n_tok])
+    assert torch.equal(out1.view(torch.int16), out2.view(torch.int16))
+
+
+def test_fused_append_rejects_multi_tile_requests():
+    # G = 8 and 32-token chunks: a request's 256 query rows span two MMA tiles
+    s = _step(41, 4, 32, 32, 16, 64, 8, 128)
+    dev = torch.device("cuda")
+    m = s["meta"]
+    plan = ops.plan_attention(m.cu_seqlens, m.key_end, 64, 8, device=dev, page_size=16)
+    assert not plan.single_tile
+    with pytest.raises(Exception):
+        ops.paged_attention_append(s["q"].to(dev)[: m.n_tok], s["k_new"].to(dev)[: m.n_tok],
+                                   s["v_new"].to(dev)[: m.n_tok], s["k_cache"].to(dev), s["v_cache"].to(dev),
+                                   s["dm"].tok_pos, s["dm"].prompt_len, s["dm"].vis_base, s["dm"].vis_off,
+                                   s["dm"].vis_words, s["dm"].block_tables, plan, s["block"])

@@ -21,6 +21,7 @@ ap.add_argument("--dump", default="")
 ap.add_argument("--ab", action="store_true")
 ap.add_argument("--dbgs", default="0,16")  # OPTIMUS_DBG[:OPTIMUS_K2_RINGS] per variant
 ap.add_argument("--plans", default="both")
+ap.add_argument("--trace-fused", action="store_true")
 a = ap.parse_args()
 a.steps = 1
 dev = torch.device("cuda")
@@ -128,16 +129,24 @@ t_k2_same = timed(lambda: [k2(0) for _ in range(L)], label="K2 x L same layer")
 t_k2 = timed(lambda: [k2(l) for l in range(L)], label="K2 x L layers")
 t_k1 = timed(lambda: [k1(l) for l in range(L)], label="K1 x L layers")
 t_both = timed(lambda: [(k1(l), k2(l)) for l in range(L)], label="K1+K2 x L layers")
+slot_abs = ops.slot_mapping(dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, cfg.page_size, n_tok=m.n_tok)
+def k2f(l):
+    q, k, v = fwd.qkv(l, dm); kc, vc = dec.cache.layer(l)
+    ops.paged_attention_append(q, k, v, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off,
+                               dm.vis_words, dm.block_tables, plan, cfg.block_size, out=out[: m.n_tok],
+                               ws_o=dec._ws_o, ws_ml=dec._ws_ml, slot_abs=slot_abs)
+t_k2f = timed(lambda: [k2f(l) for l in range(L)], label="K2+append fused x L layers") if plan.single_tile else 0
 t_k3 = timed(k3, label="K3")
 t_step = timed(lambda: dec.device_step(dm), label="full step")
 print(f"K2 per launch (layers): {t_k2/L*1e3:.1f} us -> {k2b/(t_k2/L*1e-3)/1e9:.0f} GB/s; same-layer {t_k2_same/L*1e3:.1f} us")
+print(f"fused K1+K2 per layer: {t_k2f/L*1e3:.1f} us vs separate {t_both/L*1e3:.1f} us")
 print(f"K1 per launch: {t_k1/L*1e3:.2f} us -> {k1b/(t_k1/L*1e-3)/1e9:.0f} GB/s ; K3 {t_k3*1e3:.1f} us -> {k3b/(t_k3*1e-3)/1e9:.0f} GB/s")
 
 # ---- timeline trace of one K2 launch
 from paper_2605_24832_b200 import _lib
 tr = torch.zeros((plan.grid, 4096), dtype=torch.int64, device=dev)
 _lib.call("optimus_set_attn_trace", tr.data_ptr())
-k2(0)
+(k2f if a.trace_fused else k2)(0)
 torch.cuda.synchronize()
 _lib.call("optimus_set_attn_trace", None)
 t = tr.cpu().numpy().astype(np.float64)

@@ -25,3 +25,5 @@ for c in ctas:
     print("metadata staged (kcyc):", [round((t[c, 6 * 256 + 5 + i] - c0) / 1e3, 2) for i in range(nit)])
     for nm, r in (("epi entry", 13), ("epi O full", 14), ("epi O freed", 15)):
         print(f"{nm:12s}", [round((t[c, r * 256 + i] - c0) / 1e3, 2) for i in range(nit)])
+    if t[c, 6 * 256 + 250] > 0:
+        print("append start / done (kcyc):", (t[c, 6 * 256 + 250] - c0) / 1e3, (t[c, 6 * 256 + 251] - c0) / 1e3)
