@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--workload", choices=["sharegpt", "ctx4096", "longbench", "llada"], default="sharegpt")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-target", action="store_true", help="skip the 4K-context K2 roofline line")
     ap.add_argument("--seed", type=int, default=0)
     a = ap.parse_args()
     if a.batch is None:
@@ -402,6 +403,12 @@ def main():
 
     hbm, peak_kind = peaks()
     achieved = k2b / (k2_us * 1e-6) / 1e9
+    traffic, traffic_src = profiled_traffic(args)
+    target = None
+    if world == 1 and not args.no_target:
+        del graph
+        torch.cuda.empty_cache()
+        target = target_roofline(args, dev)
     value = commits_per_step * world / world / (ms * 1e-3)  # commits are global (identical on all ranks)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -428,14 +435,15 @@ def main():
                    "l2": "inputs > L2: 36 per-layer KV caches read once per step "
                          f"({vis_keys * cfg.num_kv_heads * cfg.head_dim * 4 * cfg.num_layers / 1e9:.2f} GB)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "kernel": "paged_attn_kernel (K2)",
-                     "peak_kind": peak_kind,
+                     "frac": achieved / hbm, "traffic": traffic, "kernel": "paged_attn_kernel (K2)",
+                     "peak_kind": peak_kind, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": k2b, "launch_us": k2_us},
         "kernels_us": {"k1_kv_append": k1_us, "k2_paged_attn": k2_us, "k3_unmask": k3_us,
                        "k2_share_of_step": k2_us * cfg.num_layers / (ms * 1e3),
                        "k1_gbs": k1b / (k1_us * 1e-6) / 1e9, "k3_gbs": k3b / (k3_us * 1e-6) / 1e9,
                        "k2_tflops": flops / (k2_us * 1e-6) / 1e12},
         "attention_hbm_gbs": achieved,
+        "roofline_target_4k": target,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_launch * args.steps,
@@ -444,6 +452,74 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def target_roofline(args, dev, n_layers=8):
+    """K2 roofline at BASELINE north_star's target shape (SDAR-8B heads, block 32,
+    4K context, batch 64, chunk 32): 8 per-layer caches (9 GB, > L2) read back to back."""
+    import torch
+    from paper_2605_24832_b200 import ops
+    from paper_2605_24832_b200.decode import DecodeConfig, StreamingDecoder
+    from paper_2605_24832_b200.engine import plan_batch
+    from paper_2605_24832_b200.synthetic import SyntheticForward
+
+    class A:
+        pass
+    a = A()
+    a.workload, a.chunk, a.page, a.batch, a.seed, a.steps = "ctx4096", 32, args.page, 64, args.seed, 1
+    reqs = workload_requests(a)
+    P = a.page
+    M = SDAR8B
+    cfg = DecodeConfig(num_layers=n_layers, num_q_heads=M["num_q_heads"], num_kv_heads=M["num_kv_heads"],
+                       head_dim=M["head_dim"], vocab=M["vocab"], page_size=P, max_batch=a.batch,
+                       num_pages=pages_needed(reqs, P) + 64,
+                       max_pages_per_req=max((r.prompt_tokens + r.output_tokens + P - 1) // P for r in reqs) + 1)
+    fwd = SyntheticForward(cfg, a.batch * a.chunk, a.batch, device=dev, seed=args.seed)
+    dec = StreamingDecoder(cfg, fwd, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    for l in range(n_layers):
+        dec.cache.k[l].normal_(generator=g)
+        dec.cache.v[l].normal_(generator=g)
+    dm = dec.prepare(reqs, plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule))
+    dec.device_step(dm)
+    torch.cuda.synchronize()
+    m = dm.host
+    plan = dm.__dict__["attn_plan"]
+    out = dec._workspaces(plan, m.n_tok)
+    k2b = algorithmic_bytes(dm, cfg)[0]
+
+    def k2(l):
+        q, k, v = fwd.qkv(l, dm)
+        kc, vc = dec.cache.layer(l)
+        ops.paged_attention(q, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off,
+                            dm.vis_words, dm.block_tables, plan, cfg.block_size, out=out[: m.n_tok],
+                            ws_o=dec._ws_o, ws_ml=dec._ws_ml)
+    us = graph_time(lambda: [k2(l) for l in range(n_layers)], dev) / n_layers * 1e3
+    hbm, kind = peaks()
+    ach = k2b / (us * 1e-6) / 1e9
+    res = {"workload": "sdar8b-attn-ctx4096 (north_star target: 4K context, batch 64, chunk 32)",
+           "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "peak_kind": kind,
+           "algorithmic_bytes_per_launch": k2b, "launch_us": us, "split_kv_groups": plan.n_groups}
+    del dec, fwd
+    torch.cuda.empty_cache()
+    return res
+
+
+def profiled_traffic(args):
+    """DRAM bytes per K2 launch from the committed ncu --set full capture of this
+    workload (profiles/*_ncu.json, tools/ncu_summary.py), else None."""
+    if args.workload != "sharegpt" or args.chunk != 32 or args.page != 64:
+        return None, None
+    best = None
+    for f in sorted((ROOT / "profiles").glob("*_ncu.json")):
+        try:
+            d = json.loads(f.read_text()).get("k2_sharegpt")
+        except (OSError, ValueError):
+            continue
+        if d and "dram_bytes_per_launch" in d:
+            best = (d["dram_bytes_per_launch"], f.name)
+    return best if best else (None, None)
 
 
 def graph_time(fn, dev, reps=10):
