@@ -288,7 +288,9 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
   // state): every item pays a fixed prologue/epilogue (Q load, O drain, pipeline
   // refill, measured ~2.5 tiles) and a cut item also pays its partial write and
   // the combine read.
-  const double kItem = 2.5, kSplit = 1.5;
+  double kItem = 2.5;
+  const double kSplit = 1.5;
+  if (const char* e = std::getenv("OPTIMUS_PLAN_KITEM")) kItem = std::atof(e);  // diagnostics
   const int hard_cap = item_tile_cap(page_size);
   const int nu = static_cast<int>(units.size());
   std::vector<int> order(nu);

@@ -201,7 +201,7 @@ class NativeStepper:
         V = self._views(n)
         plan = ops.AttnPlan(self.grid, nw, ng.value, npart.value, V["work"], V["cta_off"], V["groups"],
                             A.h("work", nw * 8).reshape(-1, 8), A.h("cta_off"), A.h("groups", ng.value * 8).reshape(-1, 8),
-                            ops.single_query_tile(A.h("work", nw * 8).reshape(-1, 8)))
+                            ops.single_query_tile(host.cu_seqlens, cfg.num_q_heads, cfg.num_kv_heads))
         dm = SimpleNamespace(host=host, tok_req=V["tok_req"], tok_pos=V["tok_pos"],
                              prompt_len=V["prompt_len"], vis_base=V["vis_base"], vis_off=V["vis_off"],
                              vis_words=V["vis_words"], block_tables=V["block_tables"],

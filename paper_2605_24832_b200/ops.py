@@ -136,13 +136,13 @@ class AttnPlan:
     single_tile: bool = False  # every (request, KV head) is one query tile: K1 may fold into K2
 
 
-def single_query_tile(work_host: np.ndarray) -> bool:
-    """True when no request's query tokens span two tiles (one tok_begin per request),
-    the precondition of the fused append (optimus_paged_attn_append)."""
-    if len(work_host) == 0:
+def single_query_tile(cu_seqlens_q: np.ndarray, num_q_heads: int, num_kv_heads: int) -> bool:
+    """True when no request's query tokens span two MMA tiles (q_r x Hq/Hkv <= 128):
+    the planner then emits one token group per (request, KV head), the precondition of
+    the fused append (optimus_paged_attn_append)."""
+    if len(cu_seqlens_q) < 2:
         return True
-    pairs = np.unique(work_host[:, [0, 2]], axis=0)
-    return len(pairs) == len(np.unique(pairs[:, 0]))
+    return int(np.diff(cu_seqlens_q).max()) * (num_q_heads // num_kv_heads) <= 128
 
 
 def plan_attention(
@@ -192,7 +192,7 @@ def plan_attention(
         dev_off = torch.from_numpy(cta_off).to(device)
         dev_groups = torch.from_numpy(groups).to(device)
     return AttnPlan(grid, n, ng.value, npart.value, dev_work, dev_off, dev_groups, work, cta_off, groups,
-                    single_query_tile(work))
+                    single_query_tile(cu, num_q_heads, num_kv_heads))
 
 
 # --------------------------------------------------------------------------- K2

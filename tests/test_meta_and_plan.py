@@ -114,3 +114,20 @@ def test_planner_balances_uniform_long_contexts():
     tiles = (plan.work_host[:, 5] - plan.work_host[:, 4] + 63) // 64
     per_cta = [tiles[a:b].sum() + 2 * (b - a) for a, b in zip(plan.cta_off_host[:-1], plan.cta_off_host[1:])]
     assert max(per_cta) <= 1.12 * np.mean(per_cta)
+
+
+@pytest.mark.parametrize("hq,hkv,maxq", [(32, 8, 33), (32, 8, 41), (64, 8, 20), (4, 4, 140), (12, 4, 50)])
+def test_single_query_tile_matches_work_list(hq, hkv, maxq):
+    """plan.single_tile (precondition of the fused append) holds exactly when every
+    (request, KV head) is one query tile in the planner's work list."""
+    rng = np.random.default_rng(hq * 7 + maxq)
+    for _ in range(6):
+        n = 23
+        counts = rng.integers(0, maxq, n)
+        cu = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+        ke = rng.integers(1, 5000, n).astype(np.int32)
+        plan = _plan(cu, ke, hq, hkv, 148, page_size=64)
+        w = plan.work_host
+        pairs = np.unique(w[:, [0, 2]], axis=0)
+        one_group = len(pairs) == len(np.unique(pairs[:, 0]))
+        assert plan.single_tile == one_group
