@@ -85,3 +85,72 @@ def commit_step_decisions(q: float, rate_multiplier: float, window_len: int, uni
         p = min(1.0, rate_multiplier * q ** j)
         out.append(bool(uniforms[j - 1] < p))
     return out
+
+
+class OracleEmptyWindow(Exception):
+    """Mirrors ``EmptyWindow`` (reference errors.py:12)."""
+
+
+def block_step_window(req: dict, block_size: int) -> list:
+    """Masked positions of the current block (reference engine.py:100-101 / 128-131)."""
+    lo, hi = block_span(req, block_size)
+    return [p for p in range(lo, hi) if req["states"][p] == MASKED]
+
+
+def block_diffusion_step(req: dict, commits, block_size: int) -> int:
+    """reference engine.py:98-117 with the oracle's answer ``commits``: returns the
+    computed count (the whole block extent)."""
+    lo, hi = block_span(req, block_size)
+    extent = hi - lo
+    window = block_step_window(req, block_size)
+    if not window:
+        raise OracleEmptyWindow(req)
+    for p in commits:
+        if p not in window or req["states"][p] != MASKED:
+            raise OracleIllegalCommit(p)
+    for p in commits:
+        req["states"][p] = UNCACHED
+    req["committed"] += len(commits)
+    req["steps"] += 1
+    while all(s != MASKED for s in req["states"][lo:hi]):
+        for p in range(lo, hi):
+            req["states"][p] = CACHED
+        advance_blocks(req, block_size)
+        if req["committed"] >= req["out"]:
+            break
+        lo, hi = block_span(req, block_size)
+    return extent
+
+
+def prefix_cached_step(req: dict, commits, block_size: int) -> int:
+    """reference engine.py:120-145: commits are cached at once; computed =
+    extent - cached + uncached of the block before the step."""
+    lo, hi = block_span(req, block_size)
+    span = req["states"][lo:hi]
+    cached = sum(1 for s in span if s == CACHED)
+    uncached = sum(1 for s in span if s == UNCACHED)
+    window = block_step_window(req, block_size)
+    if not window:
+        raise OracleEmptyWindow(req)
+    computed = (hi - lo) - cached + uncached
+    for p in commits:
+        if p not in window or req["states"][p] != MASKED:
+            raise OracleIllegalCommit(p)
+    for p in commits:
+        req["states"][p] = CACHED
+    req["committed"] += len(commits)
+    req["steps"] += 1
+    advance_blocks(req, block_size)
+    return computed
+
+
+def ar_step(req: dict) -> int:
+    """reference engine.py:148-157: the next position commits and caches."""
+    p = req["committed"]
+    if p >= req["out"]:
+        raise OracleEmptyWindow(req)
+    req["states"][p] = CACHED
+    req["committed"] += 1
+    req["steps"] += 1
+    advance_blocks(req, 1)
+    return 1

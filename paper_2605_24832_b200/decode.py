@@ -32,7 +32,7 @@ import torch
 
 from . import ops
 from .core import rule_value
-from .engine import ChunkPlan, StepSummary, apply_batch, plan_batch
+from .engine import ChunkPlan, StepSummary, apply_batch, apply_block, plan_batch, plan_block
 from .errors import ConfigError
 from .kvcache import BlockTables, PagedKVCache, PagePool
 from .meta import DeviceMeta, build_step_meta
@@ -319,6 +319,26 @@ class StreamingDecoder:
             return out
         return self.step_python(requests, chunk_size)
 
+    def step_baseline(self, requests: Sequence, mode: str) -> list:
+        """One iteration of a baseline policy on the same kernels: the
+        batched twin of _Loop.run_decode's AR / block branches (sim.py:253-267) —
+        ``mode`` "bd" (block_diffusion_step), "prefix" (prefix_cached_step) or "ar"
+        (ar_step, engine.py:98-157).  One device step (K1, K2, K3) for the batch, then
+        the reference's state rules per request."""
+        cfg = self.cfg
+        block = cfg.block_size
+        plans = [plan_block(r, block, mode) for r in requests]
+        dm = self.prepare(requests, plans)
+        res = self.device_step(dm)
+        commits = self.fetch_commits(dm, res)
+        if mode == "ar":  # the next position commits whatever its confidence
+            commits = [{p.window[0]} for p in plans]
+        summaries = [apply_block(r, p, c, block, mode) for r, p, c in zip(requests, plans, commits)]
+        for req in requests:
+            if req.finished:
+                self.release(req)
+        return summaries
+
     def step_python(self, requests: Sequence, chunk_size: int) -> list:
         """The same iteration with the host half in Python (plan_batch / apply_batch)."""
         cfg = self.cfg
@@ -343,8 +363,9 @@ class B200Oracle:
     parity (commit.py:310-312).
     """
 
-    def __init__(self, decoder: StreamingDecoder):
+    def __init__(self, decoder: StreamingDecoder, mode: str = "stream"):
         self.decoder = decoder
+        self.mode = mode  # "stream" (chunked), or the block baselines "bd" / "prefix"
         self._cache: dict = {}
 
     def commits_batch(self, requests: Sequence, plans: Sequence[ChunkPlan]) -> list:
@@ -365,10 +386,15 @@ class B200Oracle:
         key = (request.id, tuple(window))
         if key in self._cache:
             return self._cache.pop(key)
-        # Standalone use inside dllmsim's loop: a non-empty window means plan_chunk
-        # had capacity left after the backlog (engine.py:58-59), so the plan's kv
-        # positions are the whole uncached queue.
-        plan = ChunkPlan(kv_positions=tuple(request.uncached_queue), window=tuple(window))
+        # Standalone use inside dllmsim's loop.  Streaming: a non-empty window means
+        # plan_chunk had capacity left after the backlog (engine.py:58-59), so the
+        # plan's kv positions are the whole uncached queue.  Block baselines: the
+        # block step recomputes the block's decoded (bd) / uncached (prefix) positions.
+        if self.mode in ("bd", "prefix"):
+            plan = ChunkPlan(kv_positions=plan_block(request, self.decoder.cfg.block_size, self.mode).kv_positions,
+                             window=tuple(window))
+        else:
+            plan = ChunkPlan(kv_positions=tuple(request.uncached_queue), window=tuple(window))
         [c] = self.commits_batch([request], [plan])
         self._cache.pop(key, None)
         return c

@@ -27,7 +27,7 @@ from typing import Iterable, Sequence
 import numpy as np
 
 from .core import TokenState, advance_blocks, rule_value
-from .errors import ChunkTooSmall, IllegalCommit
+from .errors import ChunkTooSmall, EmptyWindow, IllegalCommit
 
 
 @dataclass(frozen=True)
@@ -147,7 +147,115 @@ def apply_batch(requests, plans, commit_sets, block_size: int) -> list:
     ]
 
 
+# --------------------------------------------------------------------------- baselines
+# The paper's comparison modes on the same kernels: a whole-block
+# denoise step (BD), a prefix-cached block step and an autoregressive step, with the
+# reference's state rules and computed counts (engine.py:98-157).  ``plan_block``
+# gives the device step's query tokens (kv = positions recomputed with their
+# committed ids, window = the MASK rows the unmask scores); ``apply_block`` applies
+# the device's commits exactly as the reference step applies its oracle's.
+BASELINE_MODES = ("bd", "prefix", "ar")
+
+
+def plan_block(request, block_size: int, mode: str) -> ChunkPlan:
+    """Query tokens of one baseline step.
+
+    ``bd``: the whole block extent — every decoded position of the block is
+    recomputed, the masked ones are the window (engine.py:98-102).
+    ``prefix``: cached positions are reused; the block's uncached positions are
+    recomputed and its masked positions are the window (engine.py:120-131).
+    ``ar``: one row, the next position (engine.py:148-151)."""
+    if mode == "ar":
+        p = request.committed
+        if p >= request.output_tokens:
+            raise EmptyWindow(f"request {request.id} is already finished")
+        return ChunkPlan(kv_positions=(), window=(p,))
+    if mode not in ("bd", "prefix"):
+        raise ValueError(f"unknown baseline mode {mode!r}")
+    lo = request.block_index * block_size
+    hi = min(lo + block_size, request.output_tokens)
+    span = request.states[lo:hi]
+    window = tuple((np.flatnonzero(span == TokenState.MASKED) + lo).tolist())
+    if not window:
+        raise EmptyWindow(f"request {request.id} has no masked token in its block")
+    if mode == "bd":
+        kv = tuple((np.flatnonzero(span != TokenState.MASKED) + lo).tolist())
+    else:
+        kv = tuple((np.flatnonzero(span == TokenState.DECODED_UNCACHED) + lo).tolist())
+    return ChunkPlan(kv_positions=kv, window=window)
+
+
+def apply_block(request, plan: ChunkPlan, commits, block_size: int, mode: str) -> StepSummary:
+    """The reference baseline step's state update for the given commits."""
+    states = request.states
+    if mode == "ar":
+        p = plan.window[0]
+        states[p] = TokenState.DECODED_CACHED
+        request.committed += 1
+        request.steps_taken += 1
+        advance_blocks(request, 1)
+        return StepSummary(computed=1, commits=frozenset({p}))
+    lo = request.block_index * block_size
+    hi = min(lo + block_size, request.output_tokens)
+    check_commits(request, plan.window, commits)
+    if mode == "bd":
+        extent = hi - lo
+        for p in commits:
+            states[p] = TokenState.DECODED_UNCACHED
+        request.committed += len(commits)
+        request.steps_taken += 1
+        while np.all(states[lo:hi] != TokenState.MASKED):
+            states[lo:hi] = TokenState.DECODED_CACHED
+            advance_blocks(request, block_size)
+            if request.finished:
+                break
+            lo = request.block_index * block_size
+            hi = min(lo + block_size, request.output_tokens)
+        return StepSummary(computed=extent, commits=frozenset(commits))
+    span = states[lo:hi]
+    cached = int(np.count_nonzero(span == TokenState.DECODED_CACHED))
+    uncached = int(np.count_nonzero(span == TokenState.DECODED_UNCACHED))
+    computed = (hi - lo) - cached + uncached
+    for p in commits:
+        states[p] = TokenState.DECODED_CACHED
+    request.committed += len(commits)
+    request.steps_taken += 1
+    advance_blocks(request, block_size)
+    return StepSummary(computed=computed, commits=frozenset(commits))
+
+
+def block_diffusion_step(request, oracle, block_size: int) -> StepSummary:
+    """Reference signature (engine.py:98): one full-block denoise step."""
+    plan = plan_block(request, block_size, "bd")
+    commits = oracle.commits(request, list(plan.window))
+    summary = apply_block(request, plan, commits, block_size, "bd")
+    if hasattr(oracle, "consume"):
+        oracle.consume(request, commits)
+    return summary
+
+
+def prefix_cached_step(request, oracle, block_size: int) -> StepSummary:
+    """Reference signature (engine.py:120): block step reusing cached positions."""
+    plan = plan_block(request, block_size, "prefix")
+    commits = oracle.commits(request, list(plan.window))
+    summary = apply_block(request, plan, commits, block_size, "prefix")
+    if hasattr(oracle, "consume"):
+        oracle.consume(request, commits)
+    return summary
+
+
+def ar_step(request) -> StepSummary:
+    """Reference signature (engine.py:148): the next position commits and caches."""
+    return apply_block(request, plan_block(request, 1, "ar"), None, 1, "ar")
+
+
 __all__ = [
+    "BASELINE_MODES",
+    "plan_block",
+    "apply_block",
+    "block_diffusion_step",
+    "prefix_cached_step",
+    "ar_step",
     "StepSummary",
     "ChunkPlan",
     "plan_chunk",

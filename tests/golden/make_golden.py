@@ -28,7 +28,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from dllmsim.costmodel import fit as ref_fit, profile_to_csv  # noqa: E402
 from dllmsim.commit import CommitProfile, StochasticOracle, calibrate_q, commit_step  # noqa: E402
 from dllmsim.core import Request, TokenState, WindowRule  # noqa: E402
-from dllmsim.engine import apply_chunk, plan_chunk  # noqa: E402
+from dllmsim.engine import apply_chunk, ar_step, block_diffusion_step, plan_chunk, prefix_cached_step  # noqa: E402
 from dllmsim.workload import PROFILES, calibrated_profile  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -68,6 +68,30 @@ def replay_case(seed: int, out_tokens: int, chunk: int, block: int, rule: str, q
         "q": q, "m": m, "schedule": chunk_schedule, "steps": steps,
         "final_states": req.states.tolist(), "final_queue": list(req.uncached_queue),
     }
+
+
+def baseline_case(seed: int, out_tokens: int, block: int, mode: str, q: float, m: float) -> dict:
+    """A whole request under one of the reference's baseline steps
+    (engine.py:98-157) with StochasticOracle: per step the window (masked positions
+    of the block), the commits, the computed count and the state after."""
+    rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(1, seed)))
+    req = Request(id=seed, arrival_time=0.0, prompt_tokens=5, output_tokens=out_tokens, rng=rng)
+    req.rate_multiplier = m
+    oracle = StochasticOracle(CommitProfile(q=q))
+    steps = []
+    while not req.finished:
+        lo, hi = req.block_span(block if mode != "ar" else 1)
+        window = [int(p) for p in range(lo, hi) if req.states[p] == TokenState.MASKED]
+        if mode == "bd":
+            s = block_diffusion_step(req, oracle, block)
+        elif mode == "prefix":
+            s = prefix_cached_step(req, oracle, block)
+        else:
+            s = ar_step(req)
+        steps.append({"window": window, "commits": sorted(int(p) for p in s.commits), "computed": int(s.computed),
+                      "states": [int(x) for x in req.states], "block": int(req.block_index),
+                      "committed": int(req.committed)})
+    return {"seed": seed, "out": out_tokens, "block": block, "mode": mode, "steps": steps}
 
 
 def engine_cases() -> list:
@@ -117,7 +141,12 @@ def main() -> None:
     for bs in (4, 8):
         cases.append(replay_case(3000 + k, 41, 6, bs, "in_block", 0.7, 0.8))
         k += 1
-    (OUT / "control.json").write_text(json.dumps({"replays": cases, "engine_cases": engine_cases()}))
+    baselines = []
+    for mode in ("bd", "prefix", "ar"):
+        for j, (out_tokens, block) in enumerate(((40, 32), (97, 32), (33, 8), (64, 16))):
+            baselines.append(baseline_case(4000 + 10 * j + len(baselines), out_tokens, block, mode, sharegpt.q, 1.0))
+    (OUT / "control.json").write_text(json.dumps({"replays": cases, "engine_cases": engine_cases(),
+                                                  "baselines": baselines}))
 
     draws = []
     for seed in range(40):

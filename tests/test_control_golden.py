@@ -120,3 +120,50 @@ def test_apply_advances_block():
     plan = pe.plan_chunk(r, 4, 4)
     pe.apply_chunk(r, plan, {0, 1, 2, 3}, 4)
     assert r.block_index == 1
+
+
+def _baselines():
+    from pathlib import Path
+    return json.loads((Path(__file__).resolve().parent / "golden" / "control.json").read_text())["baselines"]
+
+
+@pytest.mark.parametrize("k", range(12))
+def test_baseline_steps_match_reference(k):
+    """BD / prefix-cached / AR steps (reference engine.py:98-157): the
+    oracle restatement and the product host mirror (plan_block / apply_block)
+    reproduce dllmsim's traces step for step given its commits."""
+    case = _baselines()[k]
+    mode, block, out = case["mode"], case["block"], case["out"]
+    oreq = oc.new_request(out)
+    req = Request(id=case["seed"], arrival_time=0.0, prompt_tokens=5, output_tokens=out)
+    for st in case["steps"]:
+        commits = set(st["commits"])
+        if mode == "ar":
+            comp_o = oc.ar_step(oreq)
+        else:
+            assert oc.block_step_window(oreq, block) == st["window"]
+            comp_o = (oc.block_diffusion_step if mode == "bd" else oc.prefix_cached_step)(oreq, commits, block)
+        assert comp_o == st["computed"] and oreq["states"] == st["states"]
+        assert (oreq["block"], oreq["committed"]) == (st["block"], st["committed"])
+        plan = pe.plan_block(req, block, mode)
+        assert list(plan.window) == st["window"]
+        summ = pe.apply_block(req, plan, commits if mode != "ar" else None, block, mode)
+        assert summ.computed == st["computed"] and sorted(summ.commits) == st["commits"]
+        assert req.states.tolist() == st["states"]
+        assert (req.block_index, req.committed) == (st["block"], st["committed"])
+    assert req.finished
+
+
+def test_baseline_bd_plan_recomputes_the_whole_block():
+    req = Request(id=0, arrival_time=0.0, prompt_tokens=3, output_tokens=20)
+    req.states[[1, 4]] = TokenState.DECODED_UNCACHED
+    plan = pe.plan_block(req, 8, "bd")
+    assert plan.kv_positions == (1, 4) and plan.window == (0, 2, 3, 5, 6, 7)
+    assert plan.computed == 8
+    pplan = pe.plan_block(req, 8, "prefix")
+    assert pplan.kv_positions == (1, 4)
+    from paper_2605_24832_b200.errors import EmptyWindow
+    req.states[:8] = TokenState.DECODED_CACHED
+    req.block_index = 0
+    with pytest.raises(EmptyWindow):
+        pe.plan_block(req, 8, "bd")

@@ -95,3 +95,54 @@ def test_oracle_protocol_per_request_calls():
             pe.apply_chunk(req, plan, commits, block)
         for a, b in zip(ref, dev):
             assert np.array_equal(a.states, b.states)
+
+
+def _reference_baseline_step(batch, block, mode):
+    """sim.py:253-267 with StochasticOracle: the reference's block / AR steps."""
+    for req in batch:
+        if mode == "ar":
+            pe.ar_step(req)
+            continue
+        plan = pe.plan_block(req, block, mode)
+        n = len(plan.window)
+        u = req.rng.random(n - 1) if n > 1 else []
+        dec = oc.commit_step_decisions(Q, req.rate_multiplier, n, u)
+        commits = {p for p, d in zip(plan.window, dec) if d}
+        pe.apply_block(req, plan, commits, block, mode)
+
+
+@pytest.mark.parametrize("mode", ["bd", "prefix", "ar"])
+def test_baseline_modes_reproduce_reference_schedule(mode):
+    """BD / prefix-cached / AR on the B200 kernels: the device step's
+    commits reproduce the reference baseline schedule step for step."""
+    block, page = 16, 16
+    ref = _requests(13, 5)
+    dev = _requests(13, 5)
+    cfg = _cfg(block, page, "in_block")
+    dec = StreamingDecoder(cfg, OracleDrivenForward(cfg, 8 * block, Q, seed=3))
+    steps = 0
+    while not all(r.finished for r in ref):
+        _reference_baseline_step([r for r in ref if not r.finished], block, mode)
+        summ = dec.step_baseline([r for r in dev if not r.finished], mode)
+        assert all(s.computed >= 1 for s in summ)
+        for a, b in zip(ref, dev):
+            assert np.array_equal(a.states, b.states), (mode, steps, a.id)
+            assert (a.block_index, a.committed, a.steps_taken) == (b.block_index, b.committed, b.steps_taken)
+        steps += 1
+        assert steps < 500
+    assert all(r.finished for r in dev)
+
+
+def test_bd_oracle_inside_reference_block_step():
+    """B200Oracle(mode="bd") behind the reference-signature block_diffusion_step."""
+    block, page = 16, 16
+    ref = _requests(17, 3)
+    dev = _requests(17, 3)
+    cfg = _cfg(block, page, "in_block")
+    oracle = B200Oracle(StreamingDecoder(cfg, OracleDrivenForward(cfg, 8 * block, Q, seed=4)), mode="bd")
+    for _ in range(5):
+        _reference_baseline_step([r for r in ref if not r.finished], block, "bd")
+        for req in [r for r in dev if not r.finished]:
+            pe.block_diffusion_step(req, oracle, block)
+        for a, b in zip(ref, dev):
+            assert np.array_equal(a.states, b.states)
