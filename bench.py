@@ -282,10 +282,18 @@ def main():
     if args.gpus != world:
         if world == 1 and args.gpus > 1:
             sys.exit("--gpus N > 1 must be launched with torchrun --nproc-per-node N")
+    # OPTIMUS_DIST_BACKEND=gloo (validation only): ranks may share a GPU and the
+    # unmask partials travel through host memory; production is NCCL, one GPU per rank
+    backend = os.environ.get("OPTIMUS_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2605_24832_b200 import ops
     from paper_2605_24832_b200.decode import DecodeConfig, StreamingDecoder
@@ -332,17 +340,29 @@ def main():
     commits_per_step = int(res.commit_mask[: dm.host.n_rows].sum().item())
     k2b, k1b, k3b, vis_keys, flops = algorithmic_bytes(dm, cfg)
 
-    # ---- capture the device step once; replay = one step
-    stream = torch.cuda.Stream(device=dev)
-    stream.wait_stream(torch.cuda.current_stream())
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
+    # ---- capture the device step once; replay = one step.  With N > 1 the step holds
+    # the NCCL all-gather of the unmask partials: it is replayed eagerly (the launches
+    # overlap the ~1.4 ms of device work) instead of capturing a collective.
+    if world == 1:
+        stream = torch.cuda.Stream(device=dev)
+        stream.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                dec.device_step(dm)
+            stream.synchronize()
+            with torch.cuda.graph(graph, stream=stream):
+                dec.device_step(dm)
+        torch.cuda.synchronize()
+    else:
+        class _Eager:
+            @staticmethod
+            def replay():
+                dec.device_step(dm)
+        graph = _Eager()
         for _ in range(2):
-            dec.device_step(dm)
-        stream.synchronize()
-        with torch.cuda.graph(graph, stream=stream):
-            dec.device_step(dm)
-    torch.cuda.synchronize()
+            graph.replay()
+        torch.cuda.synchronize()
     n_launch = 2 * cfg.num_layers + (cfg.num_layers if dec.last_plan.n_groups else 0) + 2
 
     sampler = ClockSampler(local)
@@ -395,7 +415,7 @@ def main():
     L = cfg.num_layers
     k1_us = graph_time(lambda: [k1(l) for l in range(L)], dev) / L * 1e3
     k2_us = graph_time(lambda: [k2(l) for l in range(L)], dev) / L * 1e3
-    k3_us = graph_time(lambda: dec.run_unmask(dm), dev) * 1e3
+    k3_us = graph_time(lambda: dec.run_unmask(dm), dev, use_graph=world == 1) * 1e3
 
     # ---- end to end through the public per-step call (closed loop, live state)
     dec.release_all(reqs)
@@ -522,9 +542,22 @@ def profiled_traffic(args):
     return best if best else (None, None)
 
 
-def graph_time(fn, dev, reps=10):
-    """Milliseconds per replay of fn captured as one CUDA graph (events on the stream)."""
+def graph_time(fn, dev, reps=10, use_graph=True):
+    """Milliseconds per replay of fn captured as one CUDA graph (events on the stream);
+    use_graph=False times eager calls (fn holds a collective)."""
     import torch
+    if not use_graph:
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
     s = torch.cuda.Stream(device=dev)
     s.wait_stream(torch.cuda.current_stream())
     g = torch.cuda.CUDAGraph()

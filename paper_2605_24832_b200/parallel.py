@@ -56,6 +56,12 @@ class TensorParallelUnmask:
         if self._gather is None or self._gather.numel() < self.world * part.numel():
             self._gather = torch.empty(self.world * part.numel(), dtype=torch.float32, device=part.device)
         out = self._gather[: self.world * part.numel()].view(need)
-        dist.all_gather_into_tensor(out, part.contiguous(), group=self.group)
+        if dist.get_backend(self.group) == "gloo":
+            # host-staged exchange (validation runs of the sharded path on one GPU)
+            host = [torch.empty_like(part, device="cpu") for _ in range(self.world)]
+            dist.all_gather(host, part.cpu(), group=self.group)
+            out.copy_(torch.stack(host).view(need))
+        else:
+            dist.all_gather_into_tensor(out, part.contiguous(), group=self.group)
         return ops.unmask_finalize(out, self.world, m.n_rows, n_vsplit, dm.cu_rows,
                                    dec.cfg.confidence_threshold, dec.cfg.fallback)
