@@ -330,14 +330,22 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     }
   }
 
+  // Whole-unit LPT within 3% of the mean CTA load (the bound no cutting can beat):
+  // keep it and skip candidate B.
+  double lb = 0;
+  for (const Unit& u : units) lb += u.tiles + kItem;
+  lb /= grid;
+  const bool a_good = span_a <= 1.03 * lb && std::getenv("OPTIMUS_PLAN_FORCE") == nullptr;
+
   // ---- candidate B: LPT with cutting.  Pieces are placed largest first on the
   // least-loaded CTA; a piece that would push that CTA past the balanced budget
   // (mean load + one item) is cut to fit and its remainder re-queued, so only the
   // units that do not pack are split, and each only as far as needed.
   std::vector<Piece> pb;
-  pb.reserve(nu + 2 * grid + 16);
-  double span_b = 0;
-  {
+  double span_b = 1e300;
+  if (!a_good) {
+    pb.reserve(nu + 2 * grid + 16);
+    span_b = 0;
     double total_cost = 0;
     for (const Unit& u : units) total_cost += u.tiles + kItem;
     const double budget = total_cost / grid + kItem;

@@ -39,6 +39,8 @@ class Arena:
         self.host_t = torch.empty(total, dtype=torch.int32, pin_memory=True)
         self.host = self.host_t.numpy()
         self.dev = torch.empty(total, dtype=torch.int32, device=device)
+        base = self.host.ctypes.data  # (numpy builds a ctypes object per .ctypes access)
+        self.ptr = {name: base + 4 * o for name, o in self.offs.items()}
 
     def h(self, name, n=None):
         o = self.offs[name]
@@ -49,7 +51,7 @@ class Arena:
         return self.dev[o:o + (self.caps[name] if n is None else n)]
 
     def hptr(self, name):
-        return self.host.ctypes.data + 4 * self.offs[name]
+        return self.ptr[name]
 
 
 class NativeStepper:
@@ -60,6 +62,11 @@ class NativeStepper:
         self.max_chunk = max_chunk
         B = cfg.max_batch
         self.bs = BatchState(B, max_out, qcap)
+        # fixed host arrays: their addresses once (numpy builds a ctypes object per access)
+        self._bsp = {k: getattr(self.bs, k).ctypes.data for k in (
+            "states", "queue", "q_head", "q_len", "block_index", "cached_prefix", "prompt", "out_len",
+            "committed", "steps_taken")}
+        self._bsp["table"] = decoder.tables.table.ctypes.data
         T = B * max_chunk
         R = B * min(max_chunk, cfg.block_size)
         W = B * (max_out // 32 + 4)
@@ -167,10 +174,10 @@ class NativeStepper:
         st = L.optimus_host_plan(
             n, A.hptr("slots"), chunk0, chunk_ptr, cfg.block_size,
             0 if rule_value(cfg.window_rule) == "in_block" else 1,
-            bs.states.ctypes.data, bs.states.shape[1], bs.queue.ctypes.data, bs.qcap,
-            bs.q_head.ctypes.data, bs.q_len.ctypes.data, bs.block_index.ctypes.data,
-            bs.cached_prefix.ctypes.data, bs.prompt.ctypes.data, bs.out_len.ctypes.data,
-            tables.table.ctypes.data, MP, A.hptr("cu_seqlens"), A.hptr("tok_req"), A.hptr("tok_pos"),
+            self._bsp['states'], bs.states.shape[1], self._bsp['queue'], bs.qcap,
+            self._bsp['q_head'], self._bsp['q_len'], self._bsp['block_index'],
+            self._bsp['cached_prefix'], self._bsp['prompt'], self._bsp['out_len'],
+            self._bsp['table'], MP, A.hptr("cu_seqlens"), A.hptr("tok_req"), A.hptr("tok_pos"),
             A.caps["tok_pos"], A.hptr("prompt_len"), A.hptr("key_end"), A.hptr("vis_base"),
             A.hptr("vis_off"), A.hptr("vis_words"), A.caps["vis_words"], A.hptr("cu_rows"),
             A.hptr("row_tok"), A.hptr("row_pos"), A.hptr("row_req"), A.caps["row_pos"],
@@ -238,10 +245,10 @@ class NativeStepper:
         bs = self.bs
         st = self.lib.optimus_host_apply(
             n, A.hptr("slots"), self.cfg.block_size, A.hptr("cu_seqlens"), A.hptr("tok_pos"),
-            A.hptr("cu_rows"), A.hptr("row_pos"), self.mask_host.data_ptr(), bs.states.ctypes.data,
-            bs.states.shape[1], bs.queue.ctypes.data, bs.qcap, bs.q_head.ctypes.data, bs.q_len.ctypes.data,
-            bs.block_index.ctypes.data, bs.committed.ctypes.data, bs.steps_taken.ctypes.data,
-            bs.cached_prefix.ctypes.data, bs.out_len.ctypes.data, A.hptr("commits"))
+            A.hptr("cu_rows"), A.hptr("row_pos"), self.mask_host.data_ptr(), self._bsp['states'],
+            bs.states.shape[1], self._bsp['queue'], bs.qcap, self._bsp['q_head'], self._bsp['q_len'],
+            self._bsp['block_index'], self._bsp['committed'], self._bsp['steps_taken'],
+            self._bsp['cached_prefix'], self._bsp['out_len'], A.hptr("commits"))
         _lib.check(st, "optimus_host_apply")
         return A.h("commits", n)
 
