@@ -42,6 +42,11 @@ SDAR8B = dict(num_layers=36, num_q_heads=32, num_kv_heads=8, head_dim=128, vocab
 # Model dims are not in /root/reference ([external, assumed]); BASELINE.json fixes the
 # 157K vocabulary, batch 128 and mixed per-request chunks.
 LLADA16B = dict(num_layers=20, num_q_heads=16, num_kv_heads=4, head_dim=128, vocab=157184)
+# SDAR-30B-A3B-shaped (config 5): Qwen3-30B-A3B attention geometry, 48 layers, hidden 2048
+# ([external, assumed]: model dims are not in /root/reference).  4 KV heads: at TP 8 every
+# KV head is replicated on 2 ranks, each rank computing 4 of its 8 query heads.
+SDAR30B = dict(num_layers=48, num_q_heads=32, num_kv_heads=4, head_dim=128, vocab=151936)
+SDAR30B_HIDDEN = 2048
 # commit profiles (calibrated_profile, tests/golden/commits.json and SURVEY §8d)
 Q_SHAREGPT_DENSE = 0.7758267092770552
 Q_LONGBENCH_DENSE = 0.835508
@@ -59,6 +64,9 @@ def workload_spec(name):
                           clip=(4096, 16384), mixed=None),
         "llada": dict(model=LLADA16B, batch=128, lengths=SHAREGPT, q=Q_SHAREGPT_MOE, prompt=None, clip=None,
                       mixed=(8, 16, 24, 32)),
+        # config 5: the TP decode step with the row-parallel o-proj + all-reduce per layer
+        "tp30b": dict(model=SDAR30B, batch=64, lengths=SHAREGPT, q=Q_SHAREGPT_MOE, prompt=None, clip=None,
+                      mixed=None, oproj_hidden=SDAR30B_HIDDEN),
     }[name]
 
 
@@ -71,7 +79,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--page", type=int, default=64)
-    ap.add_argument("--workload", choices=["sharegpt", "ctx4096", "longbench", "llada"], default="sharegpt")
+    ap.add_argument("--workload", choices=["sharegpt", "ctx4096", "longbench", "llada", "tp30b"],
+                    default="sharegpt")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-target", action="store_true", help="skip the 4K-context K2 roofline line")
@@ -302,8 +311,10 @@ def main():
     from paper_2605_24832_b200.synthetic import SyntheticForward
 
     M = workload_spec(args.workload)["model"]
-    if M["num_kv_heads"] % world:
-        sys.exit(f"world size must divide the {M['num_kv_heads']} KV heads")
+    if M["num_q_heads"] % world or (M["num_kv_heads"] % world and world % M["num_kv_heads"]):
+        sys.exit(f"world size must divide the {M['num_q_heads']} query heads and divide or be a multiple "
+                 f"of the {M['num_kv_heads']} KV heads")
+    kv_local = max(1, M["num_kv_heads"] // world)  # > Hkv ranks: each KV head replicated
     reqs = workload_requests(args)
     P = args.page
     long_ctx = args.workload in ("longbench", "ctx4096")
@@ -314,15 +325,20 @@ def main():
     n_pages = pages_needed(reqs, P) + sum(pages_needed(b, P) for b in e2e_pool) + 64
     maxp = max((r.prompt_tokens + r.output_tokens + P - 1) // P for b in [reqs] + e2e_pool for r in b) + 1
     cfg = DecodeConfig(num_layers=M["num_layers"], num_q_heads=M["num_q_heads"] // world,
-                       num_kv_heads=M["num_kv_heads"] // world, head_dim=M["head_dim"],
+                       num_kv_heads=kv_local, head_dim=M["head_dim"],
                        vocab=M["vocab"], page_size=P, max_batch=args.batch,
                        num_pages=n_pages, max_pages_per_req=maxp)
     vshard = (rank * cfg.vocab // world, (rank + 1) * cfg.vocab // world)
     wl = workload_spec(args.workload)
     max_chunk = max(wl["mixed"]) if wl["mixed"] else args.chunk
     max_tok = args.batch * max(max_chunk, 2)
-    fwd = SyntheticForward(cfg, max_tok, args.batch, device=dev, seed=args.seed, vocab_shard=vshard,
-                           q=wl["q"])
+    if wl.get("oproj_hidden"):
+        from paper_2605_24832_b200.synthetic import TPForward
+        fwd = TPForward(cfg, max_tok, args.batch, wl["oproj_hidden"], M["num_q_heads"], world, rank,
+                        seed=args.seed, vocab_shard=vshard, q=wl["q"], device=dev)
+    else:
+        fwd = SyntheticForward(cfg, max_tok, args.batch, device=dev, seed=args.seed, vocab_shard=vshard,
+                               q=wl["q"])
     dec = StreamingDecoder(cfg, fwd, device=dev)
     if world > 1:
         dec.unmask_impl = TensorParallelUnmask(world, rank, vshard[0])
@@ -586,6 +602,8 @@ def cfg_full(args):
 
 
 def workload_name(args):
+    if args.workload == "tp30b":
+        return "sdar30b-tp-attn-oproj-allreduce-unmask"
     base = "llada16b" if args.workload == "llada" else "sdar8b"
     return f"{base}-attn-unmask-{args.workload}"
 

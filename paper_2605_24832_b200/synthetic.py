@@ -250,3 +250,23 @@ class OracleDrivenForward(Forward):
             c = torch.as_tensor(confs, device=self.device, dtype=torch.float32)
             x.scatter_(1, tok[:, None], (lse + torch.log(c / (1 - c)))[:, None])
         return x.to(self.cfg.logits_dtype), None
+
+
+class TPForward(SyntheticForward):
+    """SyntheticForward plus the row-parallel o-proj + all-reduce after every
+    layer's attention (BASELINE configs[4]: head-sharded attention, NCCL o-proj
+    all-reduce).  Layers run one at a time (the o-proj sits between them)."""
+
+    def __init__(self, cfg: DecodeConfig, max_tokens: int, max_slots: int, hidden: int, full_q_heads: int,
+                 world: int = 1, rank: int = 0, group=None, **kw):
+        super().__init__(cfg, max_tokens, max_slots, **kw)
+        from .tp import RowParallelOProj
+        self.resident_layers = False
+        self.oproj = RowParallelOProj(cfg.num_layers, full_q_heads, cfg.head_dim, hidden, world, rank,
+                                      device=self.device, seed=kw.get("seed", 0), group=group)
+        self.last_hidden = None
+
+    def post_attn(self, layer: int, attn_out, dm) -> None:
+        n = dm.host.n_tok
+        if n:
+            self.last_hidden = self.oproj(layer, attn_out[:n])

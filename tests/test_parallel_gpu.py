@@ -107,3 +107,36 @@ def test_two_rank_tp_step_equals_single_rank(tmp_path):
             rms = np.sqrt((ref ** 2).mean(axis=-1, keepdims=True))
             assert (np.abs(part - ref) <= np.maximum(ulp, 2e-3 * rms)).all(), np.abs(part - ref).max()
             assert (part == ref).mean() > 0.95
+
+
+def _oproj(rank, world, port, outdir):
+    from paper_2605_24832_b200.tp import RowParallelOProj
+    if world > 1:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(21)
+    n, hq, d, hidden = 77, 32, 128, 2048
+    full = torch.randn((n, hq, d), generator=g, device=dev).to(torch.bfloat16)
+    per = hq // world
+    op = RowParallelOProj(2, hq, d, hidden, world, rank, device=dev, seed=4)
+    outs = [op(l, full[:, rank * per:(rank + 1) * per].contiguous()).float().cpu().numpy() for l in range(2)]
+    np.save(os.path.join(outdir, f"oproj_r{rank}_w{world}.npy"), np.stack(outs))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def test_row_parallel_oproj_allreduce_equals_unsharded(tmp_path):
+    """Config 5's exchange: the per-layer all-reduce of the row-parallel o-proj
+    partials equals the unsharded projection (two ranks on one GPU, gloo)."""
+    _oproj(0, 1, 0, str(tmp_path))
+    mp.start_processes(_oproj, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    one = np.load(tmp_path / "oproj_r0_w1.npy")
+    for r in range(2):
+        two = np.load(tmp_path / f"oproj_r{r}_w2.npy")
+        # bf16 partials summed vs one bf16 GEMM: two roundings apart
+        err = np.abs(two - one).max() / np.abs(one).max()
+        assert err < 1e-2, err
+    assert np.array_equal(np.load(tmp_path / "oproj_r0_w2.npy"), np.load(tmp_path / "oproj_r1_w2.npy"))
