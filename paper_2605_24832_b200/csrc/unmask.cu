@@ -94,22 +94,29 @@ __global__ void __launch_bounds__(THREADS) unmask_partial_kernel(
     for (int u = 0; u < U; ++u) VecLoad<T>::load(base, i + u * THREADS, v[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      // vector max by a 3-input FMNMX tree; the position of the max is searched only
+      // when it beats the running max (rare after the first vectors)
       float cm = v[u][0];
-      int ci = 0;
 #pragma unroll
-      for (int k = 1; k < N; ++k)
-        if (v[u][k] > cm) {
-          cm = v[u][k];
-          ci = k;
-        }
-      if (cm > m) {
+      for (int k = 1; k + 1 < N; k += 2) cm = fmax3(cm, v[u][k], v[u][k + 1]);
+      if constexpr (N % 2 == 0) cm = fmaxf(cm, v[u][N - 1]);
+      if (__builtin_expect(cm > m, 0)) {
+        int ci = N - 1;
+#pragma unroll
+        for (int k = N - 2; k >= 0; --k) ci = (v[u][k] == cm) ? k : ci;
         s = (m == -INFINITY) ? 0.f : s * fast_exp2((m - cm) * kLog2e);
         m = cm;
         idx = (i + u * THREADS) * N + ci;
       }
-      const float mb = m * kLog2e;
+      const float mb = -m * kLog2e;
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int k = 0; k < N; ++k) s += fast_exp2(fmaf(v[u][k], kLog2e, -mb));
+      for (int k = 0; k + 1 < N; k += 2) {
+        float e0, e1;
+        ffma2(e0, e1, v[u][k], v[u][k + 1], kLog2e, kLog2e, mb, mb);
+        fadd2(s0, s1, s0, s1, fast_exp2(e0), fast_exp2(e1));
+      }
+      s += s0 + s1;
     }
   }
   for (; i < v1; i += THREADS) {
