@@ -277,3 +277,47 @@ def test_fused_append_rejects_multi_tile_requests():
                                    s["v_new"].to(dev)[: m.n_tok], s["k_cache"].to(dev), s["v_cache"].to(dev),
                                    s["dm"].tok_pos, s["dm"].prompt_len, s["dm"].vis_base, s["dm"].vis_off,
                                    s["dm"].vis_words, s["dm"].block_tables, plan, s["block"])
+
+
+@pytest.mark.parametrize("case", ["page8_forced_cut", "page256", "g8_two_token_groups", "block64_chunk64",
+                                  "single_request_single_key", "bf16v_split_kv"])
+def test_paged_attention_edge_cases(case):
+    """Edge shapes: an item capped at 255 pages (page 8, ~3K keys -> cut), page 256,
+    G = 8 with 32-token chunks (a request spans two query tiles), block = chunk = 64,
+    a lone request whose first decode step sees 1 prompt key, a bf16 V cache with split-KV."""
+    if case == "page8_forced_cut":
+        s = _step(61, 3, 8, 32, 8, 32, 8, 128, prompt_range=(2600, 3200), out_range=(10, 60))
+        plan, err, got, ref = _attn_check(s, min_split_tiles=64, grid=148)
+        w = plan.work_host
+        assert (((w[:, 5] - 1) // 8) - (w[:, 4] // 8) + 1 <= 255).all()
+        assert plan.n_groups > 0
+    elif case == "page256":
+        s = _step(62, 7, 16, 32, 256, 32, 8, 128, prompt_range=(100, 900))
+        plan, err, got, ref = _attn_check(s)
+    elif case == "g8_two_token_groups":
+        s = _step(63, 6, 32, 32, 16, 64, 8, 128)
+        plan, err, got, ref = _attn_check(s)
+        assert not plan.single_tile
+    elif case == "block64_chunk64":
+        s = _step(64, 6, 64, 64, 16, 16, 8, 128)
+        plan, err, got, ref = _attn_check(s)
+    elif case == "single_request_single_key":
+        s = _step(65, 1, 2, 32, 16, 32, 8, 128, prompt_range=(1, 2), out_range=(2, 3))
+        plan, err, got, ref = _attn_check(s)
+    else:
+        s = _step(66, 5, 8, 32, 64, 32, 8, 128, prompt_range=(4096, 8000), out_range=(20, 80),
+                  v_dtype=torch.bfloat16)
+        plan, err, got, ref = _attn_check(s, min_split_tiles=4, grid=148)
+        assert plan.n_groups > 0
+    assert np.isfinite(got).all()
+    assert err <= ATTN_RTOL, err
+
+
+def test_decoder_step_with_no_requests():
+    """An empty batch is a no-op through the public per-step call."""
+    from paper_2605_24832_b200.decode import DecodeConfig, StreamingDecoder
+    from paper_2605_24832_b200.synthetic import SyntheticForward
+    cfg = DecodeConfig(num_layers=2, num_q_heads=8, num_kv_heads=2, head_dim=128, vocab=4096, page_size=16,
+                       max_batch=4, max_pages_per_req=16, num_pages=64)
+    dec = StreamingDecoder(cfg, SyntheticForward(cfg, 64, 4))
+    assert dec.step([], 8) == []
