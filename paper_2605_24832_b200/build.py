@@ -22,6 +22,8 @@ HEADERS = ["ptx.cuh", "attn.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
     "-O3",
+    "-Xcompiler",
+    "-O3",
     "-lineinfo",
     "-std=c++17",
     "--expt-relaxed-constexpr",

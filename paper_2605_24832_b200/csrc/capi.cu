@@ -330,12 +330,14 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     }
   }
 
-  // Whole-unit LPT within 3% of the mean CTA load (the bound no cutting can beat):
-  // keep it and skip candidate B.
+  // Cutting can only win if even a perfectly balanced cut plan (the mean CTA load)
+  // plus the combine launch beats whole units by > 3% (the rule below): otherwise
+  // keep candidate A and skip B.
+  const double kCombine = 7.0;
   double lb = 0;
   for (const Unit& u : units) lb += u.tiles + kItem;
   lb /= grid;
-  const bool a_good = span_a <= 1.03 * lb && std::getenv("OPTIMUS_PLAN_FORCE") == nullptr;
+  const bool a_good = lb + kCombine >= 0.97 * span_a && std::getenv("OPTIMUS_PLAN_FORCE") == nullptr;
 
   // ---- candidate B: LPT with cutting.  Pieces are placed largest first on the
   // least-loaded CTA; a piece that would push that CTA past the balanced budget
@@ -393,7 +395,6 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
 
   // Prefer whole units unless cutting buys >3% of the makespan, net of the split
   // combine launch it brings (~5 us ~ 7 tiles, measured).
-  const double kCombine = 7.0;
   bool use_b = span_b + kCombine < 0.97 * span_a && static_cast<int>(pb.size()) <= max_work;
   if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE"))  // diagnostics: "whole" | "cut"
     use_b = std::strcmp(f, "cut") == 0 && static_cast<int>(pb.size()) <= max_work;

@@ -46,18 +46,16 @@ import ctypes as C
 from paper_2605_24832_b200 import _lib
 A = nat.arena; L = nat.lib
 n = len(batch)
-t = time.perf_counter()
-for _ in range(20):
-    ng, npart = C.c_int(0), C.c_int(0)
-    L.optimus_attn_plan(n, A.hptr("cu_seqlens"), A.hptr("key_end"), 32, 8, nat.grid, 4, 64, A.hptr("work"), nat.max_work, A.hptr("cta_off"), A.hptr("groups"), nat.max_groups, C.byref(ng), C.byref(npart))
-print("attn_plan C++ ms", (time.perf_counter() - t) / 20 * 1e3)
 bs = nat.bs
-sl = A.h("slots", n)
+import types
 t = time.perf_counter()
 for _ in range(20):
-    L.optimus_host_plan(n, A.hptr("slots"), 32, 32, 0, bs.states.ctypes.data, bs.states.shape[1], bs.queue.ctypes.data, bs.qcap,
-        bs.q_head.ctypes.data, bs.q_len.ctypes.data, bs.block_index.ctypes.data, bs.cached_prefix.ctypes.data, bs.prompt.ctypes.data, bs.out_len.ctypes.data,
-        dec.tables.table.ctypes.data, cfg.max_pages_per_req, A.hptr("cu_seqlens"), A.hptr("tok_req"), A.hptr("tok_pos"), A.caps["tok_pos"], A.hptr("prompt_len"), A.hptr("key_end"), A.hptr("vis_base"),
-        A.hptr("vis_off"), A.hptr("vis_words"), A.caps["vis_words"], A.hptr("cu_rows"), A.hptr("row_tok"), A.hptr("row_pos"), A.hptr("row_req"), A.caps["row_pos"], A.hptr("block_tables"), A.hptr("counts"))
-print("host_plan C++ ms", (time.perf_counter() - t) / 20 * 1e3)
-
+    nat.plan(batch, 32)
+print("nat.plan (python + host_plan + attn_plan) ms", (time.perf_counter() - t) / 20 * 1e3)
+cu = A.h("cu_seqlens", n + 1).copy(); ke = A.h("key_end", n).copy()
+t = time.perf_counter()
+for _ in range(50):
+    ng, npart = C.c_int(0), C.c_int(0)
+    L.optimus_attn_plan(n, cu.ctypes.data, ke.ctypes.data, 32, 8, nat.grid, 4, 64, A.hptr("work"), nat.max_work,
+                        A.hptr("cta_off"), A.hptr("groups"), nat.max_groups, C.byref(ng), C.byref(npart))
+print("attn_plan C++ ms", (time.perf_counter() - t) / 50 * 1e3)
