@@ -286,9 +286,20 @@ class StreamingDecoder:
         if self.unmask_impl is not None:
             return self.unmask_impl(self, dm, logits, row_src)
         n_vsplit = ops.unmask_splits(m.n_rows, logits.shape[-1])
-        part = ops.unmask_partials(logits, row_src, m.n_rows, n_vsplit)
+        # per-decoder workspaces, grown on demand (no allocation per step)
+        rows = max(m.n_rows, 1)
+        ws = self.__dict__.get("_unmask_ws")
+        if ws is None or ws[0].numel() < rows * n_vsplit * 3 or ws[1].commit_mask.numel() < rows:
+            cap = max(rows, 2 * (ws[1].commit_mask.numel() if ws else 0), 256)
+            part = torch.empty(cap * max(n_vsplit, 32) * 3, dtype=torch.float32, device=self.device)
+            res = ops.UnmaskResult(torch.empty(cap, dtype=torch.uint8, device=self.device),
+                                   torch.empty(cap, dtype=torch.int32, device=self.device),
+                                   torch.empty(cap, dtype=torch.float32, device=self.device))
+            ws = self._unmask_ws = (part, res)
+        part = ops.unmask_partials(logits, row_src, m.n_rows, n_vsplit,
+                                   part=ws[0][: rows * n_vsplit * 3].view(rows, n_vsplit, 3))
         return ops.unmask_finalize(part, 1, m.n_rows, n_vsplit, dm.cu_rows,
-                                   self.cfg.confidence_threshold, self.cfg.fallback)
+                                   self.cfg.confidence_threshold, self.cfg.fallback, result=ws[1])
 
     def device_step(self, dm: DeviceMeta) -> ops.UnmaskResult:
         self.run_layers(dm)
