@@ -264,6 +264,30 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
 /* Recommended vocab split count for n_rows x vocab on the current device. */
 int optimus_unmask_splits(int n_rows, int vocab);
 
+/*
+ * Device twins of optimus_host_plan / optimus_host_apply (device half):
+ * the same packed per-slot state and step metadata, all pointers DEVICE pointers,
+ * enqueued on `stream`, bit-identical results (tests/test_device_step_gpu.py).
+ * n <= 256 requests, out_len <= 4096 positions, chunk <= 128.  counts[0..4) =
+ * {n_tok, n_rows, n_words, status}; *status (apply) is set to OPTIMUS_EINVAL on an
+ * illegal plan / commit (caller zeroes it).
+ */
+int optimus_device_plan(int n, const int32_t* slots, int chunk, const int32_t* chunk_per_req, int block,
+                        int window_rule, const int8_t* states, int64_t state_stride, const int32_t* queue,
+                        int qcap, const int32_t* q_head, const int32_t* q_len, const int32_t* block_index,
+                        const int32_t* cached_prefix, const int32_t* prompt, const int32_t* out_len,
+                        const int32_t* block_tables, int max_pages, int32_t* cu_seqlens, int32_t* tok_req,
+                        int32_t* tok_pos, int cap_tok, int32_t* prompt_len, int32_t* key_end,
+                        int32_t* vis_base, int32_t* vis_off, uint32_t* vis_words, int cap_words,
+                        int32_t* cu_rows, int32_t* row_tok, int32_t* row_pos, int32_t* row_req, int cap_rows,
+                        int32_t* block_tables_out, int32_t* counts, void* stream);
+int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* cu_seqlens,
+                         const int32_t* tok_pos, const int32_t* cu_rows, const int32_t* row_pos,
+                         const uint8_t* commit_mask, int8_t* states, int64_t state_stride, int32_t* queue,
+                         int qcap, int32_t* q_head, int32_t* q_len, int32_t* block_index, int32_t* committed,
+                         int32_t* steps_taken, int32_t* cached_prefix, const int32_t* out_len,
+                         int32_t* commits_out, int32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

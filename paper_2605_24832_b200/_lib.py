@@ -76,6 +76,11 @@ SIGNATURES = {
          _vp, _i32, _i32, _vp, _vp],
     ),
     "optimus_kv_append_slots": (_i32, [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _i32, _vp]),
+    "optimus_device_plan": (_i32, [_i32, _vp, _i32, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
+                                   _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32,
+                                   _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "optimus_device_apply": (_i32, [_i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _vp,
+                                    _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "optimus_slot_mapping": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "optimus_host_plan": (_i32, [_i32, _vp, _i32, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,

@@ -1,0 +1,408 @@
+// device_step.cu — the control half of the streaming decode step on the device
+// (device half).
+//
+// optimus_device_plan / optimus_device_apply are the device twins of
+// optimus_host_plan / optimus_host_apply (host_step.cu), which mirror the
+// reference's plan_chunk (engine.py:45-67) and apply_chunk + advance_blocks
+// (engine.py:79-95, core.py:109-116) batch-wide.  Same packed per-slot state (now
+// device-resident), same step metadata out, bit for bit
+// (tests/test_device_step_gpu.py): with them the plan -> K1/K2 -> K3 -> apply loop
+// needs no host round trip, which is what a graph-captured step requires.
+//
+// Plan: one CTA of 32 warps; warp w plans requests w, w+32, ...  Pass 1 selects each
+// request's kv positions (FIFO front of the uncached ring) and window (earliest
+// MASKED of the current block, or anywhere capped at the block for OUT_BLOCK) with
+// warp ballots in position order, and derives key_end / vis_base from a per-warp
+// "planned" bitmap in shared memory; a block scan turns the counts into offsets;
+// pass 2 writes the query / row layouts, the rule-V visibility words and the
+// gathered block-table rows.
+// Apply: one warp per request.
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "../../include/optimus_b200.h"
+
+namespace optimus {
+namespace dstep {
+
+constexpr int8_t MASKED = 0, UNCACHED = 1, CACHED = 2;
+constexpr int kWarps = 32;
+constexpr int kMaxOut = 4096;          // planned bitmap capacity per warp (positions)
+constexpr int kMaxReq = 256;           // requests per step (the reference's max_batch, sim.py:62)
+constexpr int kMaxChunk = 128;
+
+struct PlanArgs {
+  int n;
+  const int32_t* slots;
+  int chunk;
+  const int32_t* chunk_per_req;
+  int block, window_rule;
+  const int8_t* states;
+  int64_t stride;
+  const int32_t* queue;
+  int qcap;
+  const int32_t* q_head;
+  const int32_t* q_len;
+  const int32_t* block_index;
+  const int32_t* cached_prefix;
+  const int32_t* prompt;
+  const int32_t* out_len;
+  const int32_t* block_tables;
+  int max_pages;
+  int32_t* cu_seqlens;
+  int32_t* tok_req;
+  int32_t* tok_pos;
+  int cap_tok;
+  int32_t* prompt_len;
+  int32_t* key_end;
+  int32_t* vis_base;
+  int32_t* vis_off;
+  uint32_t* vis_words;
+  int cap_words;
+  int32_t* cu_rows;
+  int32_t* row_tok;
+  int32_t* row_pos;
+  int32_t* row_req;
+  int cap_rows;
+  int32_t* block_tables_out;
+  int32_t* counts;  // {n_tok, n_rows, n_words, status}
+};
+
+__device__ __forceinline__ bool planned_bit(const uint32_t* bm, int p) { return (bm[p >> 5] >> (p & 31)) & 1u; }
+
+__global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) {
+  __shared__ uint32_t bitmap[kWarps][kMaxOut / 32];
+  __shared__ int ntok_s[kMaxReq], nrow_s[kMaxReq], nword_s[kMaxReq], nkv_s[kMaxReq];
+  __shared__ int ke_s[kMaxReq], vb_s[kMaxReq];
+  __shared__ int bad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  uint32_t* bm = bitmap[warp];
+  // ---- pass 1: counts, key_end, vis_base
+  for (int r = warp; r < a.n; r += kWarps) {
+    const int s = a.slots[r];
+    const int out = a.out_len[s];
+    const int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
+    const int chunk_r = a.chunk_per_req ? a.chunk_per_req[r] : a.chunk;
+    if (chunk_r < 2 || chunk_r > kMaxChunk || out > kMaxOut) {
+      if (lane == 0) bad = 1;
+      continue;
+    }
+    const int nkv = min(a.q_len[s], chunk_r);
+    int room = chunk_r - nkv;
+    int lo = a.block_index[s] * a.block;
+    int hi = min(lo + a.block, out);
+    if (a.window_rule == 1) {
+      hi = out;
+      room = min(room, a.block);
+    }
+    for (int w = lane; w < (out + 31) / 32; w += 32) bm[w] = 0;
+    __syncwarp();
+    // kv positions: the FIFO front of the uncached ring
+    int maxq = -1;
+    for (int i = lane; i < nkv; i += 32) {
+      const int p = a.queue[static_cast<int64_t>(s) * a.qcap + (a.q_head[s] + i) % a.qcap];
+      atomicOr(&bm[p >> 5], 1u << (p & 31));
+      maxq = max(maxq, p);
+    }
+    // window: earliest MASKED in [lo, hi), up to `room`, in position order
+    int nwin = 0;
+    for (int base = lo; base < hi && nwin < room; base += 32) {
+      const int p = base + lane;
+      const bool m = p < hi && st[p] == MASKED;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+      const int rank = __popc(bal & ((1u << lane) - 1u));
+      if (m && nwin + rank < room) {
+        atomicOr(&bm[p >> 5], 1u << (p & 31));
+        maxq = max(maxq, p);
+      }
+      nwin = min(room, nwin + __popc(bal));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxq = max(maxq, __shfl_xor_sync(0xFFFFFFFFu, maxq, o));
+    if (lane == 0) {
+      ntok_s[r] = nkv + nwin;
+      nrow_s[r] = nwin;
+      nkv_s[r] = nkv;
+    }
+    if (nkv + nwin == 0) {
+      if (lane == 0) {
+        ke_s[r] = 0;
+        vb_s[r] = 0;
+        nword_s[r] = 0;
+      }
+      continue;
+    }
+    // rule V: visible = CACHED before the step, or planned now
+    // cp: first position from cached_prefix on that is not visible
+    int cp = min(a.cached_prefix[s], out);
+    while (true) {
+      const int p = cp + lane;
+      const bool v = p < out && (st[p] == CACHED || planned_bit(bm, p));
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
+      if (bal == 0xFFFFFFFFu) {
+        cp += 32;
+        continue;
+      }
+      cp += __ffs(~bal) - 1;
+      break;
+    }
+    cp = min(cp, out);
+    const int cap_end = (maxq / a.block + 1) * a.block;
+    // last: the largest visible position
+    int last = -1;
+    for (int base = ((out - 1) / 32) * 32; base >= 0 && last < 0; base -= 32) {
+      const int p = base + lane;
+      const bool v = p < out && (st[p] == CACHED || planned_bit(bm, p));
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
+      if (bal) last = base + 31 - __clz(bal);
+    }
+    const int pr = a.prompt[s];
+    const int ke = pr + min(last + 1, cap_end);
+    int vb = ((pr + cp) / 32) * 32;
+    if (vb > ke) vb = (ke / 32) * 32;
+    if (lane == 0) {
+      ke_s[r] = ke;
+      vb_s[r] = vb;
+      nword_s[r] = ke > vb ? (ke - vb + 31) / 32 : 0;
+    }
+  }
+  __syncthreads();
+  // ---- offsets (one thread: n <= 1024, cheap)
+  if (threadIdx.x == 0) {
+    int nt = 0, nr = 0, nw = 0;
+    a.cu_seqlens[0] = 0;
+    a.cu_rows[0] = 0;
+    for (int r = 0; r < a.n; ++r) {
+      a.vis_off[r] = nw;
+      nt += ntok_s[r];
+      nr += nrow_s[r];
+      nw += nword_s[r];
+      a.cu_seqlens[r + 1] = nt;
+      a.cu_rows[r + 1] = nr;
+      a.prompt_len[r] = a.prompt[a.slots[r]];
+      a.key_end[r] = ke_s[r];
+      a.vis_base[r] = vb_s[r];
+    }
+    a.vis_off[a.n] = nw;
+    if (nt > a.cap_tok || nr > a.cap_rows || nw > a.cap_words) bad = 1;
+    a.counts[0] = nt;
+    a.counts[1] = nr;
+    a.counts[2] = nw;
+    a.counts[3] = bad ? OPTIMUS_EINVAL : 0;
+  }
+  __syncthreads();
+  if (bad) return;
+  // ---- pass 2: layouts, visibility words, block tables
+  for (int r = warp; r < a.n; r += kWarps) {
+    const int s = a.slots[r];
+    const int out = a.out_len[s];
+    const int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
+    const int t0 = a.cu_seqlens[r], r0 = a.cu_rows[r];
+    const int nkv = nkv_s[r], nwin = nrow_s[r];
+    // rebuild the planned bitmap and window of this request (pass 1's were per warp
+    // and reused by later requests of the same warp)
+    for (int w = lane; w < (out + 31) / 32; w += 32) bm[w] = 0;
+    __syncwarp();
+    for (int i = lane; i < nkv; i += 32) {
+      const int p = a.queue[static_cast<int64_t>(s) * a.qcap + (a.q_head[s] + i) % a.qcap];
+      a.tok_req[t0 + i] = r;
+      a.tok_pos[t0 + i] = p;
+      atomicOr(&bm[p >> 5], 1u << (p & 31));
+    }
+    {
+      const int chunk_r = a.chunk_per_req ? a.chunk_per_req[r] : a.chunk;
+      int room = chunk_r - nkv;
+      int lo = a.block_index[s] * a.block;
+      int hi = min(lo + a.block, out);
+      if (a.window_rule == 1) {
+        hi = out;
+        room = min(room, a.block);
+      }
+      int got = 0;
+      for (int base = lo; base < hi && got < room; base += 32) {
+        const int p = base + lane;
+        const bool m = p < hi && st[p] == MASKED;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+        const int rank = __popc(bal & ((1u << lane) - 1u));
+        if (m && got + rank < room) {
+          const int k = got + rank;
+          a.row_tok[r0 + k] = t0 + nkv + k;
+          a.row_pos[r0 + k] = p;
+          a.row_req[r0 + k] = r;
+          a.tok_req[t0 + nkv + k] = r;
+          a.tok_pos[t0 + nkv + k] = p;
+          atomicOr(&bm[p >> 5], 1u << (p & 31));
+        }
+        got = min(room, got + __popc(bal));
+      }
+      (void)nwin;
+    }
+    __syncwarp();
+    const int pr = a.prompt[s];
+    const int ke = ke_s[r], vb = vb_s[r];
+    const int words = nword_s[r];
+    uint32_t* vw = a.vis_words + a.vis_off[r];
+    for (int w = 0; w < words; ++w) {
+      const int abs = vb + w * 32 + lane;
+      const int p = abs - pr;
+      const bool v = abs < ke && (p < 0 || (p < out && (st[p] == CACHED || planned_bit(bm, p))));
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
+      if (lane == 0) vw[w] = bal;
+    }
+    const int32_t* src = a.block_tables + static_cast<int64_t>(s) * a.max_pages;
+    int32_t* dst = a.block_tables_out + static_cast<int64_t>(r) * a.max_pages;
+    for (int i = lane; i < a.max_pages; i += 32) dst[i] = src[i];
+  }
+}
+
+struct ApplyArgs {
+  int n;
+  const int32_t* slots;
+  int block;
+  const int32_t* cu_seqlens;
+  const int32_t* tok_pos;
+  const int32_t* cu_rows;
+  const int32_t* row_pos;
+  const uint8_t* commit_mask;
+  int8_t* states;
+  int64_t stride;
+  int32_t* queue;
+  int qcap;
+  int32_t* q_head;
+  int32_t* q_len;
+  int32_t* block_index;
+  int32_t* committed;
+  int32_t* steps;
+  int32_t* cached_prefix;
+  const int32_t* out_len;
+  int32_t* commits_out;
+  int32_t* status;
+};
+
+// One warp per request (lane 0 walks the FIFO; the rest scan in parallel).
+__global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= a.n) return;
+  const int s = a.slots[r];
+  int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
+  int32_t* q = a.queue + static_cast<int64_t>(s) * a.qcap;
+  const int out = a.out_len[s];
+  int ok = 1;
+  if (lane == 0) {
+    const int nkv = (a.cu_seqlens[r + 1] - a.cu_seqlens[r]) - (a.cu_rows[r + 1] - a.cu_rows[r]);
+    int head = a.q_head[s], len = a.q_len[s];
+    for (int i = 0; i < nkv && ok; ++i) {
+      const int p = a.tok_pos[a.cu_seqlens[r] + i];
+      if (len == 0 || q[head] != p) {
+        ok = 0;  // KV plan out of order
+        break;
+      }
+      head = (head + 1) % a.qcap;
+      --len;
+      st[p] = CACHED;
+    }
+    int k = 0;
+    for (int i = a.cu_rows[r]; i < a.cu_rows[r + 1] && ok; ++i) {
+      if (!a.commit_mask[i]) continue;
+      const int p = a.row_pos[i];
+      if (st[p] != MASKED || len >= a.qcap) {
+        ok = 0;
+        break;
+      }
+      st[p] = UNCACHED;
+      q[(head + len) % a.qcap] = p;
+      ++len;
+      ++k;
+    }
+    if (ok) {
+      a.q_head[s] = head;
+      a.q_len[s] = len;
+      a.commits_out[r] = k;
+      a.committed[s] += k;
+      a.steps[s] += 1;
+    } else {
+      *a.status = OPTIMUS_EINVAL;
+    }
+  }
+  if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return;
+  __syncwarp();
+  // advance_blocks: skip blocks without MASKED positions
+  int bi = a.block_index[s];
+  const int committed = a.committed[s];
+  while (committed < out) {
+    const int lo = bi * a.block, hi = min(lo + a.block, out);
+    bool any = false;
+    for (int base = lo; base < hi; base += 32) {
+      const int p = base + lane;
+      if (__any_sync(0xFFFFFFFFu, p < hi && st[p] == MASKED)) {
+        any = true;
+        break;
+      }
+    }
+    if (any) break;
+    ++bi;
+  }
+  // cached_prefix: first non-CACHED position
+  int cp = a.cached_prefix[s];
+  while (cp < out) {
+    const int p = cp + lane;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, p < out && st[p] == CACHED);
+    if (bal == 0xFFFFFFFFu) {
+      cp += 32;
+      continue;
+    }
+    cp += __ffs(~bal) - 1;
+    break;
+  }
+  if (lane == 0) {
+    a.block_index[s] = bi;
+    a.cached_prefix[s] = min(cp, out);
+  }
+}
+
+}  // namespace dstep
+}  // namespace optimus
+
+extern "C" {
+
+int optimus_device_plan(int n, const int32_t* slots, int chunk, const int32_t* chunk_per_req, int block,
+                        int window_rule, const int8_t* states, int64_t state_stride, const int32_t* queue,
+                        int qcap, const int32_t* q_head, const int32_t* q_len, const int32_t* block_index,
+                        const int32_t* cached_prefix, const int32_t* prompt, const int32_t* out_len,
+                        const int32_t* block_tables, int max_pages, int32_t* cu_seqlens, int32_t* tok_req,
+                        int32_t* tok_pos, int cap_tok, int32_t* prompt_len, int32_t* key_end,
+                        int32_t* vis_base, int32_t* vis_off, uint32_t* vis_words, int cap_words,
+                        int32_t* cu_rows, int32_t* row_tok, int32_t* row_pos, int32_t* row_req, int cap_rows,
+                        int32_t* block_tables_out, int32_t* counts, void* stream) {
+  using namespace optimus::dstep;
+  if (n < 0 || n > kMaxReq || block < 1 || (window_rule != 0 && window_rule != 1)) return OPTIMUS_EINVAL;
+  if (n == 0) return 0;
+  PlanArgs a{n, slots, chunk, chunk_per_req, block, window_rule, states, state_stride, queue, qcap,
+             q_head, q_len, block_index, cached_prefix, prompt, out_len, block_tables, max_pages,
+             cu_seqlens, tok_req, tok_pos, cap_tok, prompt_len, key_end, vis_base, vis_off, vis_words,
+             cap_words, cu_rows, row_tok, row_pos, row_req, cap_rows, block_tables_out, counts};
+  plan_kernel<<<1, kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* cu_seqlens,
+                         const int32_t* tok_pos, const int32_t* cu_rows, const int32_t* row_pos,
+                         const uint8_t* commit_mask, int8_t* states, int64_t state_stride, int32_t* queue,
+                         int qcap, int32_t* q_head, int32_t* q_len, int32_t* block_index, int32_t* committed,
+                         int32_t* steps_taken, int32_t* cached_prefix, const int32_t* out_len,
+                         int32_t* commits_out, int32_t* status, void* stream) {
+  using namespace optimus::dstep;
+  if (n < 0 || block < 1) return OPTIMUS_EINVAL;
+  if (n == 0) return 0;
+  ApplyArgs a{n, slots, block, cu_seqlens, tok_pos, cu_rows, row_pos, commit_mask, states, state_stride, queue,
+              qcap, q_head, q_len, block_index, committed, steps_taken, cached_prefix, out_len, commits_out,
+              status};
+  apply_kernel<<<(n * 32 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // extern "C"

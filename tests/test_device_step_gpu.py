@@ -1,0 +1,133 @@
+"""Device twins of the native host step (csrc/device_step.cu, SURVEY §8f-1 device
+half): optimus_device_plan / optimus_device_apply over device-resident packed state
+produce the same step metadata and state transitions as optimus_host_plan /
+optimus_host_apply (themselves pinned to the Python mirror and to dllmsim), bit for
+bit, step by step over whole decodes."""
+
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_24832_b200 import _lib
+from paper_2605_24832_b200.batch_state import BatchState
+from tests.scenario import make_requests
+from tests.test_host_step import _native_apply, _native_plan
+
+pytestmark = pytest.mark.gpu
+
+CAPS = 4096
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _p(t):
+    return t.data_ptr() if t is not None else None
+
+
+@pytest.mark.parametrize("rule,chunk,block", [("in_block", 8, 32), ("in_block", 32, 32), ("out_block", 8, 16),
+                                              ("in_block", 2, 8), ("in_block", "mixed", 32)])
+def test_device_plan_and_apply_match_host(rule, chunk, block):
+    rng = np.random.default_rng(40 + block + (7 if chunk == "mixed" else chunk))
+    reqs = make_requests(21 + block, 12, (1, 300), (3, 200), 8, block, rule)
+    bs = BatchState(16, 256, qcap=64)
+    for i, r in enumerate(copy.deepcopy(reqs)):
+        bs.bind(r, i)
+    tables = np.arange(16 * 40, dtype=np.int32).reshape(16, 40)
+    # device copy of the packed state
+    D = {k: _dev(getattr(bs, k)) for k in ("states", "queue", "q_head", "q_len", "block_index", "committed",
+                                            "steps_taken", "cached_prefix", "prompt", "out_len")}
+    Dt = _dev(tables)
+    L = _lib.load()
+    stream = torch.cuda.current_stream().cuda_stream
+    steps = 0
+    while True:
+        idx = [i for i in range(len(reqs)) if bs.committed[i] < bs.out_len[i]]
+        if not idx:
+            break
+        n = len(idx)
+        c = rng.choice([2, 4, 8, 16, 24, 32], n).astype(np.int32) if chunk == "mixed" else chunk
+        out, counts = _native_plan(bs, idx, c, block, rule, tables, caps=CAPS)
+        n_tok, n_rows, n_words = (int(x) for x in counts[:3])
+        # device plan
+        O = {k: torch.zeros(n + 1, dtype=torch.int32, device="cuda") for k in ("cu_seqlens", "vis_off", "cu_rows")}
+        O.update({k: torch.zeros(n, dtype=torch.int32, device="cuda") for k in ("prompt_len", "key_end", "vis_base")})
+        O.update({k: torch.zeros(CAPS, dtype=torch.int32, device="cuda")
+                  for k in ("tok_req", "tok_pos", "row_tok", "row_pos", "row_req", "vis_words")})
+        O["block_tables"] = torch.zeros((n, tables.shape[1]), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(4, dtype=torch.int32, device="cuda")
+        sl = _dev(np.asarray(idx, dtype=np.int32))
+        cpr = _dev(c) if chunk == "mixed" else None
+        st = L.optimus_device_plan(
+            n, _p(sl), 0 if chunk == "mixed" else chunk, _p(cpr), block, 0 if rule == "in_block" else 1,
+            _p(D["states"]), D["states"].shape[1], _p(D["queue"]), bs.qcap, _p(D["q_head"]), _p(D["q_len"]),
+            _p(D["block_index"]), _p(D["cached_prefix"]), _p(D["prompt"]), _p(D["out_len"]), _p(Dt),
+            tables.shape[1], _p(O["cu_seqlens"]), _p(O["tok_req"]), _p(O["tok_pos"]), CAPS, _p(O["prompt_len"]),
+            _p(O["key_end"]), _p(O["vis_base"]), _p(O["vis_off"]), _p(O["vis_words"]), CAPS, _p(O["cu_rows"]),
+            _p(O["row_tok"]), _p(O["row_pos"]), _p(O["row_req"]), CAPS, _p(O["block_tables"]), _p(cnt), stream)
+        assert st == 0
+        torch.cuda.synchronize()
+        assert cnt.cpu().tolist() == [n_tok, n_rows, n_words, 0], steps
+        for k in ("cu_seqlens", "prompt_len", "key_end", "vis_base", "vis_off", "cu_rows"):
+            assert np.array_equal(O[k].cpu().numpy(), out[k]), (k, steps)
+        for k, m in (("tok_req", n_tok), ("tok_pos", n_tok), ("row_tok", n_rows), ("row_pos", n_rows),
+                     ("row_req", n_rows)):
+            assert np.array_equal(O[k].cpu().numpy()[:m], out[k][:m]), (k, steps)
+        assert np.array_equal(O["vis_words"].cpu().numpy().view(np.uint32)[:n_words], out["vis_words"][:n_words])
+        assert np.array_equal(O["block_tables"].cpu().numpy(), out["block_tables"])
+        # commits: random, the first window row of each request always
+        mask = rng.random(n_rows) < 0.35
+        for r in range(n):
+            a, b = out["cu_rows"][r], out["cu_rows"][r + 1]
+            if b > a:
+                mask[a] = True
+        commits_h = _native_apply(bs, idx, block, out, mask)
+        commits_d = torch.zeros(n, dtype=torch.int32, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dm = _dev(mask.astype(np.uint8))
+        st = L.optimus_device_apply(
+            n, _p(sl), block, _p(O["cu_seqlens"]), _p(O["tok_pos"]), _p(O["cu_rows"]), _p(O["row_pos"]), _p(dm),
+            _p(D["states"]), D["states"].shape[1], _p(D["queue"]), bs.qcap, _p(D["q_head"]), _p(D["q_len"]),
+            _p(D["block_index"]), _p(D["committed"]), _p(D["steps_taken"]), _p(D["cached_prefix"]),
+            _p(D["out_len"]), _p(commits_d), _p(status), stream)
+        assert st == 0
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        assert commits_d.cpu().tolist() == list(commits_h)
+        for k in ("states", "q_head", "q_len", "block_index", "committed", "steps_taken", "cached_prefix"):
+            assert np.array_equal(D[k].cpu().numpy(), getattr(bs, k)), (k, steps)
+        # the ring: compare the live entries
+        for i in range(len(reqs)):
+            h, ln = int(bs.q_head[i]), int(bs.q_len[i])
+            live = [(h + j) % bs.qcap for j in range(ln)]
+            assert np.array_equal(D["queue"].cpu().numpy()[i][live], bs.queue[i][live])
+        steps += 1
+        assert steps < 500
+    assert steps > 5
+
+
+def test_device_apply_rejects_out_of_order_kv():
+    bs = BatchState(2, 64, qcap=8)
+    reqs = make_requests(5, 1, (3, 10), (20, 30), 8, 16, "in_block")
+    for i, r in enumerate(reqs):
+        bs.bind(r, i)
+    L = _lib.load()
+    # a plan claiming a kv position the ring does not hold at its front
+    cu = _dev(np.array([0, 1], np.int32))
+    tok = _dev(np.array([5], np.int32))
+    cur = _dev(np.array([0, 0], np.int32))
+    rp = _dev(np.zeros(1, np.int32))
+    D = {k: _dev(getattr(bs, k)) for k in ("states", "queue", "q_head", "q_len", "block_index", "committed",
+                                            "steps_taken", "cached_prefix", "out_len")}
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = L.optimus_device_apply(
+        1, _p(_dev(np.array([0], np.int32))), 16, _p(cu), _p(tok), _p(cur), _p(rp), _p(_dev(np.zeros(1, np.uint8))),
+        _p(D["states"]), D["states"].shape[1], _p(D["queue"]), bs.qcap, _p(D["q_head"]), _p(D["q_len"]),
+        _p(D["block_index"]), _p(D["committed"]), _p(D["steps_taken"]), _p(D["cached_prefix"]), _p(D["out_len"]),
+        _p(torch.zeros(1, dtype=torch.int32, device="cuda")), _p(status), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    assert int(status.item()) == -1
