@@ -288,6 +288,16 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
                          int32_t* steps_taken, int32_t* cached_prefix, const int32_t* out_len,
                          int32_t* commits_out, int32_t* status, void* stream);
 
+/*
+ * Device twin of optimus_attn_plan's whole-unit placement (its candidate A): same
+ * work / cta_off / groups output as the host planner under OPTIMUS_PLAN_FORCE=whole,
+ * from device-resident cu_seqlens / key_end (n_req <= 256, <= 4096 units and pieces,
+ * grid <= 1024).  counts[0..4) = {n_work, n_groups, n_partials, status}.
+ */
+int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, const int32_t* key_end, int num_q_heads,
+                             int num_kv_heads, int grid, int page_size, int32_t* work, int max_work,
+                             int32_t* cta_off, int32_t* groups, int max_groups, int32_t* counts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,8 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "optimus_device_apply": (_i32, [_i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _vp,
                                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "optimus_device_attn_plan": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp,
+                                        _vp]),
     "optimus_slot_mapping": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "optimus_host_plan": (_i32, [_i32, _vp, _i32, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,

@@ -17,6 +17,8 @@
 // pass 2 writes the query / row layouts, the rule-V visibility words and the
 // gathered block-table rows.
 // Apply: one warp per request.
+#include <algorithm>
+#include <climits>
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -406,3 +408,227 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------------------
+// Device twin of the attention work planner's whole-unit candidate
+// (optimus_attn_plan, capi.cu, candidate A): units (request, KV head, query tile)
+// sorted longest first (stable), each cut only at the per-item page cap, placed
+// piece by piece on the least-loaded CTA (ties: lowest CTA), costs in half-tiles
+// (2 * tiles + 5 per item, + 3 for a cut piece: the host's 2.5 / 1.5 exactly);
+// work list in CTA order, split groups / partial slots in unit order.  Same output
+// as the host planner whenever it keeps whole units (OPTIMUS_PLAN_FORCE=whole);
+// one CTA, ~10 us for 512 units.
+namespace optimus {
+namespace dstep {
+
+constexpr int kPlanThreads = 1024;
+constexpr int kMaxUnits = 4096;
+
+__global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
+    int n_req, const int32_t* __restrict__ cu, const int32_t* __restrict__ key_end, int hkv, int T, int grid,
+    int hard_cap, int32_t* __restrict__ work, int max_work, int32_t* __restrict__ cta_off,
+    int32_t* __restrict__ groups, int max_groups, int32_t* __restrict__ counts) {
+  extern __shared__ uint8_t sm_raw[];
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm_raw);  // [kMaxUnits]
+  int* u_req = reinterpret_cast<int*>(keys + kMaxUnits);
+  int* u_head = u_req + kMaxUnits;
+  int* u_tok = u_head + kMaxUnits;
+  int* u_ntok = u_tok + kMaxUnits;
+  int* u_tiles = u_ntok + kMaxUnits;
+  int* u_first = u_tiles + kMaxUnits;  // first piece of the unit
+  int* p_unit = u_first + kMaxUnits;   // pieces in placement order
+  int* p_t0 = p_unit + kMaxUnits;
+  int* p_nt = p_t0 + kMaxUnits;
+  int* p_cta = p_nt + kMaxUnits;
+  int* p_slot = p_cta + kMaxUnits;
+  __shared__ int req_off[257];
+  __shared__ int n_units_s, n_pieces_s, bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) bad = 0;
+  // 1. units: per request hkv * ceil(nq / T), request-major then head then token group
+  if (tid < n_req) {
+    const int nq = cu[tid + 1] - cu[tid];
+    req_off[tid + 1] = nq > 0 ? hkv * ((nq + T - 1) / T) : 0;
+    if (nq > 0 && key_end[tid] < 1) bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    req_off[0] = 0;
+    for (int r = 0; r < n_req; ++r) req_off[r + 1] += req_off[r];
+    n_units_s = req_off[n_req];
+    if (n_units_s > kMaxUnits) bad = 1;
+  }
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) counts[3] = OPTIMUS_EINVAL;
+    return;
+  }
+  const int nu = n_units_s;
+  if (tid < n_req) {
+    const int nq = cu[tid + 1] - cu[tid];
+    if (nq > 0) {
+      const int nt = (key_end[tid] + 63) / 64;
+      int u = req_off[tid];
+      for (int h = 0; h < hkv; ++h)
+        for (int t0 = 0; t0 < nq; t0 += T, ++u) {
+          u_req[u] = tid;
+          u_head[u] = h;
+          u_tok[u] = cu[tid] + t0;
+          u_ntok[u] = min(T, nq - t0);
+          u_tiles[u] = nt;
+        }
+    }
+  }
+  __syncthreads();
+  // 2. stable sort by tiles, descending: ascending keys (~tiles, index), bitonic
+  int np2 = 1;
+  while (np2 < nu) np2 <<= 1;
+  for (int i = tid; i < np2; i += kPlanThreads)
+    keys[i] = i < nu ? (static_cast<unsigned long long>(0x7FFFFFFF - u_tiles[i]) << 32) | static_cast<unsigned>(i)
+                     : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= np2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < np2; i += kPlanThreads) {
+        const int ix = i ^ j;
+        if (ix > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = keys[i], b = keys[ix];
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[ix] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // 3. LPT placement by warp 0 (loads in half-tiles, CTA c held by lane c % 32)
+  if (warp == 0) {
+    constexpr int kPer = 32;  // CTAs per lane (grid <= 1024)
+    long long load[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) load[i] = 0;
+    int np = 0;
+    for (int o = 0; o < nu; ++o) {
+      const int u = static_cast<int>(keys[o] & 0xFFFFFFFFu);
+      const int tiles = u_tiles[u];
+      const int sc = (tiles + hard_cap - 1) / hard_cap;
+      const int base = tiles / sc, rem = tiles % sc;
+      if (lane == 0) u_first[u] = np;
+      int t0 = 0;
+      for (int k = 0; k < sc; ++k, ++np) {
+        const int nt = base + (k < rem ? 1 : 0);
+        long long best = LLONG_MAX;
+        int bc = 0x7FFFFFFF;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int c = lane + 32 * i;
+          if (c < grid && load[i] < best) {  // increasing c per lane: first minimum
+            best = load[i];
+            bc = c;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const long long b2 = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+          const int c2 = __shfl_xor_sync(0xFFFFFFFFu, bc, off);
+          if (b2 < best || (b2 == best && c2 < bc)) {
+            best = b2;
+            bc = c2;
+          }
+        }
+        if ((bc & 31) == lane) load[bc >> 5] += 2LL * nt + 5 + (sc > 1 ? 3 : 0);
+        if (lane == 0 && np < kMaxUnits) {
+          p_unit[np] = u;
+          p_t0[np] = t0;
+          p_nt[np] = nt;
+          p_cta[np] = bc;
+        }
+        t0 += nt;
+      }
+    }
+    if (lane == 0) n_pieces_s = np;
+  }
+  __syncthreads();
+  const int npc = n_pieces_s;
+  if (npc > kMaxUnits || npc > max_work) {
+    if (tid == 0) counts[3] = OPTIMUS_EINVAL;
+    return;
+  }
+  // 4. split groups and partial slots, in unit order
+  if (tid == 0) {
+    int ng = 0, npart = 0;
+    for (int u = 0; u < nu; ++u) {
+      const int tiles = u_tiles[u];
+      const int sc = (tiles + hard_cap - 1) / hard_cap;
+      const int f = u_first[u];
+      if (sc > 1) {
+        if (ng >= max_groups) {
+          bad = 1;
+          break;
+        }
+        int32_t* g = groups + 8 * ng++;
+        g[0] = u_req[u];
+        g[1] = u_head[u];
+        g[2] = u_tok[u];
+        g[3] = u_ntok[u];
+        g[4] = npart;
+        g[5] = sc;
+        g[6] = 0;
+        g[7] = 0;
+        for (int k = 0; k < sc; ++k) p_slot[f + k] = npart++;
+      } else {
+        p_slot[f] = -1;
+      }
+    }
+    counts[0] = npc;
+    counts[1] = ng;
+    counts[2] = npart;
+    counts[3] = bad ? OPTIMUS_EINVAL : 0;
+  }
+  __syncthreads();
+  // 5. work list in CTA order (each CTA's pieces in placement order)
+  for (int c = tid; c < grid; c += kPlanThreads) {
+    int k = 0;
+    for (int x = 0; x < npc; ++x) k += p_cta[x] < c;
+    cta_off[c] = k;
+    for (int x = 0; x < npc; ++x) {
+      if (p_cta[x] != c) continue;
+      const int u = p_unit[x];
+      int32_t* w = work + 8 * k++;
+      w[0] = u_req[u];
+      w[1] = u_head[u];
+      w[2] = u_tok[u];
+      w[3] = u_ntok[u];
+      w[4] = p_t0[x] * 64;
+      w[5] = min(key_end[u_req[u]], (p_t0[x] + p_nt[x]) * 64);
+      w[6] = p_slot[x];
+      w[7] = 0;
+    }
+  }
+  if (tid == 0) cta_off[grid] = npc;
+}
+
+}  // namespace dstep
+}  // namespace optimus
+
+extern "C" int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, const int32_t* key_end, int hq,
+                                        int hkv, int grid, int page_size, int32_t* work, int max_work,
+                                        int32_t* cta_off, int32_t* groups, int max_groups, int32_t* counts,
+                                        void* stream) {
+  using namespace optimus::dstep;
+  if (n_req < 0 || n_req > 256 || hkv < 1 || hq % hkv || grid < 1 || grid > 1024) return OPTIMUS_EINVAL;
+  const int G = hq / hkv;
+  if (G > 128) return OPTIMUS_EINVAL;
+  const int hard_cap = static_cast<int>(std::max(1LL, std::min((255LL * std::max(page_size, 1)) / 64, 1LL << 20)));
+  const size_t smem = kMaxUnits * (8 + 11 * 4);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(work_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  work_plan_kernel<<<1, kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      n_req, cu_seqlens, key_end, hkv, 128 / G, grid, hard_cap, work, max_work, cta_off, groups, max_groups,
+      counts);
+  return static_cast<int>(cudaGetLastError());
+}

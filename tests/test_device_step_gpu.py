@@ -123,11 +123,46 @@ def test_device_apply_rejects_out_of_order_kv():
     D = {k: _dev(getattr(bs, k)) for k in ("states", "queue", "q_head", "q_len", "block_index", "committed",
                                             "steps_taken", "cached_prefix", "out_len")}
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sl0, m0, c0 = _dev(np.array([0], np.int32)), _dev(np.zeros(1, np.uint8)), torch.zeros(1, dtype=torch.int32,
+                                                                                           device="cuda")
     st = L.optimus_device_apply(
-        1, _p(_dev(np.array([0], np.int32))), 16, _p(cu), _p(tok), _p(cur), _p(rp), _p(_dev(np.zeros(1, np.uint8))),
+        1, _p(sl0), 16, _p(cu), _p(tok), _p(cur), _p(rp), _p(m0),
         _p(D["states"]), D["states"].shape[1], _p(D["queue"]), bs.qcap, _p(D["q_head"]), _p(D["q_len"]),
         _p(D["block_index"]), _p(D["committed"]), _p(D["steps_taken"]), _p(D["cached_prefix"]), _p(D["out_len"]),
-        _p(torch.zeros(1, dtype=torch.int32, device="cuda")), _p(status), torch.cuda.current_stream().cuda_stream)
+        _p(c0), _p(status), torch.cuda.current_stream().cuda_stream)
     assert st == 0
     torch.cuda.synchronize()
     assert int(status.item()) == -1
+
+
+@pytest.mark.parametrize("hq,hkv,page,maxq,ke_hi", [(32, 8, 64, 33, 3000), (32, 8, 16, 33, 9000), (64, 8, 16, 33, 800),
+                                                    (16, 4, 64, 33, 600), (4, 4, 8, 9, 40000)])
+def test_device_work_planner_matches_host_whole_unit_plan(hq, hkv, page, maxq, ke_hi, monkeypatch):
+    """optimus_device_attn_plan == optimus_attn_plan's whole-unit placement (incl. the
+    255-page cap cuts and their split groups at page 8 / 16 with long contexts)."""
+    monkeypatch.setenv("OPTIMUS_PLAN_FORCE", "whole")
+    from paper_2605_24832_b200 import ops
+    rng = np.random.default_rng(hq * 31 + page + maxq)
+    L = _lib.load()
+    for _ in range(4):
+        n = int(rng.integers(1, 65))
+        counts = rng.integers(0, maxq, n)
+        cu = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+        ke = rng.integers(1, ke_hi, n).astype(np.int32)
+        grid = 148
+        plan = ops.plan_attention(cu, ke, hq, hkv, grid=grid, min_split_tiles=4, page_size=page)
+        mw = 4096
+        work = torch.zeros((mw, 8), dtype=torch.int32, device="cuda")
+        off = torch.zeros(grid + 1, dtype=torch.int32, device="cuda")
+        groups = torch.zeros((1024, 8), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(4, dtype=torch.int32, device="cuda")
+        dcu, dke = _dev(cu), _dev(ke)  # keep the device copies alive across the launch
+        st = L.optimus_device_attn_plan(n, _p(dcu), _p(dke), hq, hkv, grid, page, _p(work), mw, _p(off),
+                                        _p(groups), 1024, _p(cnt), torch.cuda.current_stream().cuda_stream)
+        assert st == 0
+        torch.cuda.synchronize()
+        c = cnt.cpu().tolist()
+        assert c[3] == 0 and c[0] == plan.n_work and c[1] == plan.n_groups and c[2] == plan.n_partials
+        assert np.array_equal(off.cpu().numpy(), plan.cta_off_host)
+        assert np.array_equal(work.cpu().numpy()[: c[0]], plan.work_host)
+        assert np.array_equal(groups.cpu().numpy()[: c[1]], plan.groups_host)
