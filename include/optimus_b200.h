@@ -298,6 +298,23 @@ int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, const int32_t
                              int num_kv_heads, int grid, int page_size, int32_t* work, int max_work,
                              int32_t* cta_off, int32_t* groups, int max_groups, int32_t* counts, void* stream);
 
+/*
+ * Device-planned steps (counts produced on the device by optimus_device_plan):
+ * K1 and the K3 partials with their token / row count read from device memory and
+ * grids sized for the capacity (graph-capturable), and the slot-indexed logits-row
+ * map of the synthetic forward (counts = optimus_device_plan's counts).
+ */
+int optimus_kv_append_dev(const void* k_new, const void* v_new, int64_t new_stride_tok, const int32_t* tok_req,
+                          const int32_t* tok_pos, const int32_t* prompt_len, const int32_t* block_tables,
+                          int max_pages, int n_tok_cap, const int32_t* n_tok_dev, int num_kv_heads, int head_dim,
+                          int page_size, void* k_cache, void* v_cache, int v_dtype, void* stream);
+int optimus_unmask_partials_dev(const void* logits, int logits_dtype, int64_t row_stride, const int32_t* row_src,
+                                int n_rows_cap, const int32_t* n_rows_dev, int vocab, int vocab_offset,
+                                int n_vsplit, float* part, void* stream);
+int optimus_device_row_src(const int32_t* counts, const int32_t* slots, const int32_t* cu_rows,
+                           const int32_t* row_req, int cap_rows, int rows_per_slot, int base, int32_t* row_src,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,10 @@ namespace optimus {
 
 int launch_kv_append_slots(const void*, const void*, int64_t, const int32_t*, int, int, int, int,
                            void*, void*, int, cudaStream_t);
+int launch_kv_append_dev(const void*, const void*, int64_t, const int32_t*, const int32_t*, const int32_t*,
+                         const int32_t*, int, int, const int32_t*, int, int, int, void*, void*, int, cudaStream_t);
+int launch_unmask_partials_dev(const void*, int, int64_t, const int32_t*, int, const int32_t*, int, int, int,
+                               float*, cudaStream_t);
 int launch_slot_map(const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int,
                     int32_t*, cudaStream_t);
 int launch_kv_append(const void*, const void*, int64_t, const int32_t*, const int32_t*,
@@ -212,6 +216,38 @@ int optimus_kv_append_slots(const void* k_new, const void* v_new, int64_t new_st
                                             head_dim, page_size, k_cache, v_cache, v_dtype,
                                             static_cast<cudaStream_t>(stream)),
                      "kv_append_slots");
+}
+
+int optimus_kv_append_dev(const void* k_new, const void* v_new, int64_t new_stride_tok, const int32_t* tok_req,
+                          const int32_t* tok_pos, const int32_t* prompt_len, const int32_t* block_tables,
+                          int max_pages, int n_tok_cap, const int32_t* n_tok_dev, int num_kv_heads, int head_dim,
+                          int page_size, void* k_cache, void* v_cache, int v_dtype, void* stream) {
+  if (v_dtype != 0 && v_dtype != 1) return fail("kv_append_dev: v_dtype must be 0 or 1");
+  if (n_tok_cap < 0 || num_kv_heads < 1 || head_dim % 8 || page_size < 1) return fail("kv_append_dev: bad sizes");
+  if (new_stride_tok < static_cast<int64_t>(num_kv_heads) * head_dim || new_stride_tok % 8)
+    return fail("kv_append_dev: bad new_stride_tok");
+  if (!n_tok_dev || !k_new || !v_new || !tok_req || !tok_pos || !prompt_len || !block_tables || !k_cache ||
+      !v_cache)
+    return fail("kv_append_dev: null pointer");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_kv_append_dev(k_new, v_new, new_stride_tok, tok_req, tok_pos, prompt_len, block_tables,
+                                          max_pages, n_tok_cap, n_tok_dev, num_kv_heads, head_dim, page_size,
+                                          k_cache, v_cache, v_dtype, static_cast<cudaStream_t>(stream)),
+                     "kv_append_dev");
+}
+
+int optimus_unmask_partials_dev(const void* logits, int logits_dtype, int64_t row_stride, const int32_t* row_src,
+                                int n_rows_cap, const int32_t* n_rows_dev, int vocab, int vocab_offset,
+                                int n_vsplit, float* part, void* stream) {
+  if (logits_dtype != 0 && logits_dtype != 1) return fail("unmask_dev: logits_dtype must be 0 or 1");
+  const int vec = logits_dtype == 0 ? 8 : 4;
+  if (vocab < 1 || vocab % vec || row_stride % vec || row_stride < vocab) return fail("unmask_dev: bad vocab");
+  if (n_rows_cap < 0 || n_vsplit < 1 || !n_rows_dev || !logits || !part) return fail("unmask_dev: bad args");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_unmask_partials_dev(logits, logits_dtype, row_stride, row_src, n_rows_cap, n_rows_dev,
+                                                vocab, vocab_offset, n_vsplit, part,
+                                                static_cast<cudaStream_t>(stream)),
+                     "unmask_partials_dev");
 }
 
 int optimus_slot_mapping(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,

@@ -91,8 +91,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
       if (lane == 0) bad = 1;
       continue;
     }
-    const int nkv = min(a.q_len[s], chunk_r);
-    int room = chunk_r - nkv;
+    // finished (no MASKED left in the current block, advance_blocks' invariant): nothing
+    bool done;
+    {
+      const int b0 = a.block_index[s] * a.block, b1 = min(b0 + a.block, out);
+      bool any = false;
+      for (int base = b0; base < b1; base += 32)
+        any = any || __any_sync(0xFFFFFFFFu, base + lane < b1 && st[base + lane] == MASKED);
+      done = !any;
+    }
+    const int nkv = done ? 0 : min(a.q_len[s], chunk_r);
+    int room = done ? 0 : chunk_r - nkv;
     int lo = a.block_index[s] * a.block;
     int hi = min(lo + a.block, out);
     if (a.window_rule == 1) {
@@ -215,8 +224,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
       atomicOr(&bm[p >> 5], 1u << (p & 31));
     }
     {
-      const int chunk_r = a.chunk_per_req ? a.chunk_per_req[r] : a.chunk;
-      int room = chunk_r - nkv;
+      int room = nwin;  // pass 1's window size (0 for a finished request)
       int lo = a.block_index[s] * a.block;
       int hi = min(lo + a.block, out);
       if (a.window_rule == 1) {
@@ -240,7 +248,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
         }
         got = min(room, got + __popc(bal));
       }
-      (void)nwin;
     }
     __syncwarp();
     const int pr = a.prompt[s];
@@ -293,6 +300,10 @@ __global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
   int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
   int32_t* q = a.queue + static_cast<int64_t>(s) * a.qcap;
   const int out = a.out_len[s];
+  if (a.committed[s] >= out) {  // finished: not stepped (sim.py:307-313)
+    if (lane == 0) a.commits_out[r] = 0;
+    return;
+  }
   int ok = 1;
   if (lane == 0) {
     const int nkv = (a.cu_seqlens[r + 1] - a.cu_seqlens[r]) - (a.cu_rows[r + 1] - a.cu_rows[r]);
@@ -630,5 +641,31 @@ extern "C" int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, co
   work_plan_kernel<<<1, kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       n_req, cu_seqlens, key_end, hkv, 128 / G, grid, hard_cap, work, max_work, cta_off, groups, max_groups,
       counts);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------------------
+// Window row -> logits row of a slot-indexed logits table (the synthetic forward's
+// layout: rows_per_slot rows per batch slot, version block `base`), for device-planned
+// steps: row_src[i] = base + slot(row i) * rows_per_slot + min(rank in request, rows_per_slot - 1).
+namespace optimus {
+namespace dstep {
+__global__ void row_src_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ slots,
+                               const int32_t* __restrict__ cu_rows, const int32_t* __restrict__ row_req,
+                               int rows_per_slot, int base, int32_t* __restrict__ row_src) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= counts[1]) return;
+  const int r = row_req[i];
+  row_src[i] = base + slots[r] * rows_per_slot + min(i - cu_rows[r], rows_per_slot - 1);
+}
+}  // namespace dstep
+}  // namespace optimus
+
+extern "C" int optimus_device_row_src(const int32_t* counts, const int32_t* slots, const int32_t* cu_rows,
+                                      const int32_t* row_req, int cap_rows, int rows_per_slot, int base,
+                                      int32_t* row_src, void* stream) {
+  if (cap_rows <= 0 || rows_per_slot < 1) return OPTIMUS_EINVAL;
+  optimus::dstep::row_src_kernel<<<(cap_rows + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, slots, cu_rows, row_req, rows_per_slot, base, row_src);
   return static_cast<int>(cudaGetLastError());
 }

@@ -80,14 +80,23 @@ int optimus_host_plan(int n, const int32_t* slots, int chunk, const int32_t* chu
     const int8_t* st = states + static_cast<int64_t>(s) * state_stride;
     const int chunk_r = chunk_per_req ? chunk_per_req[r] : chunk;  // mixed chunks (elastic)
     if (chunk_r < 2) return OPTIMUS_EINVAL;                        // ChunkTooSmall, engine.py:56
-    const int nkv = std::min(q_len[s], chunk_r);
+    // A finished request plans nothing (the reference's loop drops it, sim.py:307-313).
+    // advance_blocks keeps an unfinished request's current block holding a MASKED
+    // position, so "finished" == no MASKED position in the current block.
+    bool done = true;
+    for (int p = block_index[s] * block, e = std::min(p + block, out); p < e; ++p)
+      if (st[p] == MASKED) {
+        done = false;
+        break;
+      }
+    const int nkv = done ? 0 : std::min(q_len[s], chunk_r);
     if (nt + chunk_r > cap_tok) return OPTIMUS_EINVAL;
     const int t0 = nt;
     for (int i = 0; i < nkv; ++i) {
       tok_req[nt] = r;
       tok_pos[nt++] = qget(P, s, i);
     }
-    int room = chunk_r - nkv;
+    int room = done ? 0 : chunk_r - nkv;
     const int r0 = nr;
     int lo = block_index[s] * block;
     int hi = std::min(lo + block, out);
@@ -172,6 +181,10 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
   if (n < 0 || block < 1) return OPTIMUS_EINVAL;
   for (int r = 0; r < n; ++r) {
     const int s = slots[r];
+    if (committed[s] >= out_len[s]) {  // finished: not stepped (sim.py:307-313)
+      commits_out[r] = 0;
+      continue;
+    }
     int8_t* st = states + static_cast<int64_t>(s) * state_stride;
     int32_t* q = queue + static_cast<int64_t>(s) * qcap;
     const int nkv = (cu_seqlens[r + 1] - cu_seqlens[r]) - (cu_rows[r + 1] - cu_rows[r]);

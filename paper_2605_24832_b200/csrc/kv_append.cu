@@ -26,10 +26,12 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
     const int32_t* __restrict__ tok_req, const int32_t* __restrict__ tok_pos,
     const int32_t* __restrict__ prompt_len, const int32_t* __restrict__ block_tables,
     int max_pages, int n_tok, int hkv, int vec_per_head, int page_size, uint4* __restrict__ k_cache,
-    uint4* __restrict__ v_cache, int64_t* __restrict__ slot_out, int v_fp16) {
+    uint4* __restrict__ v_cache, int64_t* __restrict__ slot_out, int v_fp16,
+    const int32_t* __restrict__ n_tok_dev) {
   // let a PDL-launched dependent (the attention kernel) start its prologue now; it
   // waits for this grid's completion before reading the cache.
   grid_dep_launch();
+  if (n_tok_dev != nullptr) n_tok = *n_tok_dev;  // device-planned step (grid sized for capacity)
   const int per_tok = hkv * vec_per_head;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= static_cast<int64_t>(n_tok) * per_tok) return;
@@ -75,7 +77,24 @@ int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_to
   kv_append_kernel<<<blocks, threads, 0, stream>>>(
       static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
       tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok, hkv, vec_per_head, page_size,
-      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), slot_out, v_fp16);
+      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), slot_out, v_fp16, nullptr);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Same, with the token count read from device memory (n_tok_cap sizes the grid).
+int launch_kv_append_dev(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                         const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                         const int32_t* block_tables, int max_pages, int n_tok_cap, const int32_t* n_tok_dev,
+                         int hkv, int head_dim, int page_size, void* k_cache, void* v_cache, int v_fp16,
+                         cudaStream_t stream) {
+  if (n_tok_cap == 0) return 0;
+  const int vec_per_head = head_dim / 8;
+  const int64_t total = static_cast<int64_t>(n_tok_cap) * hkv * vec_per_head;
+  const int blocks = static_cast<int>((total + 255) / 256);
+  kv_append_kernel<<<blocks, 256, 0, stream>>>(
+      static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
+      tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok_cap, hkv, vec_per_head, page_size,
+      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), nullptr, v_fp16, n_tok_dev);
   return static_cast<int>(cudaGetLastError());
 }
 

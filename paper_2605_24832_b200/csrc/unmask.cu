@@ -71,10 +71,12 @@ struct VecLoad<float> {
 template <typename T, int THREADS>
 __global__ void __launch_bounds__(THREADS) unmask_partial_kernel(
     const T* __restrict__ logits, int64_t row_stride, const int32_t* __restrict__ row_src,
-    int vocab, int vocab_offset, int n_vsplit, Part* __restrict__ part) {
+    int vocab, int vocab_offset, int n_vsplit, Part* __restrict__ part,
+    const int32_t* __restrict__ n_rows_dev = nullptr) {
   constexpr int N = VecLoad<T>::N;
   const int row = blockIdx.x;
   const int split = blockIdx.y;
+  if (n_rows_dev != nullptr && row >= *n_rows_dev) return;  // device-planned step
   const int64_t src = row_src ? row_src[row] : row;
   const T* base = logits + src * row_stride;
   // vocab slice of this split, in whole vectors (vocab is a multiple of N here)
@@ -248,6 +250,24 @@ int launch_unmask_partials(const void* logits, int dtype, int64_t row_stride,
     unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
         static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
         reinterpret_cast<Part*>(part));
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Phase (a) with the row count read from device memory (grid sized for n_rows_cap).
+int launch_unmask_partials_dev(const void* logits, int dtype, int64_t row_stride, const int32_t* row_src,
+                               int n_rows_cap, const int32_t* n_rows_dev, int vocab, int vocab_offset,
+                               int n_vsplit, float* part, cudaStream_t stream) {
+  if (n_rows_cap == 0) return 0;
+  dim3 grid(n_rows_cap, n_vsplit);
+  if (dtype == 0) {
+    unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
+        reinterpret_cast<Part*>(part), n_rows_dev);
+  } else {
+    unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
+        static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
+        reinterpret_cast<Part*>(part), n_rows_dev);
   }
   return static_cast<int>(cudaGetLastError());
 }

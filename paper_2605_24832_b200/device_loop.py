@@ -1,0 +1,205 @@
+"""Graph-captured streaming decode step with its control half on the device.
+
+``DeviceLoop`` runs the whole iteration of the streaming branch of ``_Loop.run_decode``
+(sim.py:269-305) as ONE CUDA graph on device-resident request state:
+
+    optimus_device_plan       plan_chunk for every request + the step metadata
+    optimus_device_attn_plan  the attention work list (whole-unit LPT placement)
+    L x (optimus_kv_append_dev, optimus_paged_attn)
+    optimus_device_row_src, optimus_unmask_partials_dev, optimus_unmask_finalize
+    optimus_device_apply      apply_chunk + advance_blocks
+    D2H of the plan arrays and the commit mask into pinned buffers
+
+so no host round trip sits between steps.  The host keeps the reference-facing
+``Request`` objects exact by replaying the same transitions with
+``optimus_host_apply`` from the copied plan (bit-identical to the device's; see
+tests/test_device_loop_gpu.py, which also checks the whole loop against the host
+native step).  The batch is fixed for the loop's lifetime (finished requests plan
+zero tokens); every request's pages are allocated up front.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .core import rule_value
+from .engine import StepSummary
+from .errors import ConfigError
+
+
+class DeviceLoop:
+    def __init__(self, decoder, requests, chunk: int):
+        cfg = decoder.cfg
+        if not getattr(decoder.forward, "resident_layers", False) or not hasattr(decoder.forward, "row_src_host"):
+            raise ConfigError("DeviceLoop needs a forward with resident per-layer activations and a slot-indexed "
+                              "logits table (SyntheticForward)")
+        self.dec, self.cfg, self.chunk = decoder, cfg, int(chunk)
+        nat = decoder.native()
+        self.nat = nat
+        self.requests = list(requests)
+        self.n = n = len(self.requests)
+        dev = decoder.device
+        self.dev = dev
+        slots = []
+        for r in self.requests:
+            s = nat._slot(r)
+            decoder.tables.ensure(s, r.prompt_tokens + r.output_tokens)
+            slots.append(s)
+        self.slots_h = np.asarray(slots, dtype=np.int32)
+        max_pages = cfg.max_pages_per_req
+        if max(r.prompt_tokens + r.output_tokens for r in self.requests) > 255 * cfg.page_size:
+            raise ConfigError("DeviceLoop: an item would exceed 255 pages (split-KV groups need the host planner)")
+        bs = nat.bs
+        self.bs = bs
+        self.state_keys = ("states", "queue", "q_head", "q_len", "block_index", "committed", "steps_taken",
+                           "cached_prefix", "prompt", "out_len")
+        self.D = {k: torch.from_numpy(np.ascontiguousarray(getattr(bs, k))).to(dev) for k in self.state_keys}
+        self.Dt = torch.from_numpy(np.ascontiguousarray(decoder.tables.table)).to(dev)
+        self.slots = torch.from_numpy(self.slots_h).to(dev)
+        ct = n * self.chunk
+        cr = n * min(self.chunk, cfg.block_size)
+        cw = n * (bs.states.shape[1] // 32 + 4)
+        self.caps = (ct, cr, cw)
+        z = lambda m, dt=torch.int32: torch.zeros(max(m, 1), dtype=dt, device=dev)
+        M = dict(cu_seqlens=z(n + 1), tok_req=z(ct), tok_pos=z(ct), prompt_len=z(n), key_end=z(n), vis_base=z(n),
+                 vis_off=z(n + 1), vis_words=z(cw), cu_rows=z(n + 1), row_tok=z(cr), row_pos=z(cr), row_req=z(cr),
+                 counts=z(4), row_src=z(cr), commits=z(n), status=z(1))
+        M["block_tables"] = torch.zeros((n, max_pages), dtype=torch.int32, device=dev)
+        G = cfg.num_q_heads // cfg.num_kv_heads
+        T = 128 // G
+        self.max_work = n * cfg.num_kv_heads * ((self.chunk + T - 1) // T) * 2
+        self.grid = decoder.grid
+        M["work"] = torch.zeros((self.max_work, 8), dtype=torch.int32, device=dev)
+        M["cta_off"] = z(self.grid + 1)
+        M["groups"] = torch.zeros((64, 8), dtype=torch.int32, device=dev)
+        M["wcounts"] = z(4)
+        self.M = M
+        fwd = decoder.forward
+        self.logits = fwd.logit_table
+        self.n_vsplit = ops.unmask_splits(cr, self.logits.shape[-1])
+        self.part = torch.empty((cr, self.n_vsplit, 3), dtype=torch.float32, device=dev)
+        self.res = ops.UnmaskResult(z(cr, torch.uint8), z(cr), z(cr, torch.float32))
+        self.out = torch.empty((ct, cfg.num_q_heads, cfg.head_dim), dtype=torch.bfloat16, device=dev)
+        # pinned host mirrors of what the host replay needs
+        self.H = {k: torch.zeros(M[k].numel(), dtype=torch.int32, pin_memory=True)
+                  for k in ("counts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos")}
+        self.H["mask"] = torch.zeros(max(cr, 1), dtype=torch.uint8, pin_memory=True)
+        self.graph = None
+
+    # ------------------------------------------------------------------ device
+    def _enqueue(self, stream) -> None:
+        cfg, D, M, n = self.cfg, self.D, self.M, self.n
+        ct, cr, cw = self.caps
+        p = lambda t: t.data_ptr()
+        L = _lib
+        rule = 0 if rule_value(cfg.window_rule) == "in_block" else 1
+        _lib.check(L.call(
+            "optimus_device_plan", n, p(self.slots), self.chunk, None, cfg.block_size, rule, p(D["states"]),
+            D["states"].shape[1], p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]),
+            p(D["cached_prefix"]), p(D["prompt"]), p(D["out_len"]), p(self.Dt), self.Dt.shape[1],
+            p(M["cu_seqlens"]), p(M["tok_req"]), p(M["tok_pos"]), ct, p(M["prompt_len"]), p(M["key_end"]),
+            p(M["vis_base"]), p(M["vis_off"]), p(M["vis_words"]), cw, p(M["cu_rows"]), p(M["row_tok"]),
+            p(M["row_pos"]), p(M["row_req"]), cr, p(M["block_tables"]), p(M["counts"]), stream), "device_plan")
+        _lib.check(L.call(
+            "optimus_device_attn_plan", n, p(M["cu_seqlens"]), p(M["key_end"]), cfg.num_q_heads, cfg.num_kv_heads,
+            self.grid, cfg.page_size, p(M["work"]), self.max_work, p(M["cta_off"]), p(M["groups"]),
+            M["groups"].shape[0], p(M["wcounts"]), stream), "device_attn_plan")
+        fwd = self.dec.forward
+        scale = 1.0 / float(cfg.head_dim) ** 0.5
+        v_dtype = ops._v_dtype(self.dec.cache.v)
+        for layer in range(cfg.num_layers):
+            q, k, v = fwd.qkv_buf[layer][:, : cfg.num_q_heads], None, None
+            buf = fwd.qkv_buf[layer]
+            hq, hkv = cfg.num_q_heads, cfg.num_kv_heads
+            kc, vc = self.dec.cache.layer(layer)
+            _lib.check(L.call(
+                "optimus_kv_append_dev", p(buf[:, hq]), p(buf[:, hq + hkv]), buf.stride(0), p(M["tok_req"]),
+                p(M["tok_pos"]), p(M["prompt_len"]), p(M["block_tables"]), M["block_tables"].shape[1], ct,
+                p(M["counts"]), hkv, cfg.head_dim, cfg.page_size, p(kc), p(vc), v_dtype, stream), "kv_append_dev")
+            _lib.check(L.call(
+                "optimus_paged_attn", p(buf), buf.stride(0), buf.shape[0], p(kc), p(vc), kc.shape[0],
+                p(M["tok_pos"]), p(M["prompt_len"]), p(M["vis_base"]), p(M["vis_off"]), p(M["vis_words"]),
+                p(M["block_tables"]), M["block_tables"].shape[1], p(M["work"]), p(M["cta_off"]), self.grid,
+                p(M["groups"]), 0, cfg.block_size, hq, hkv, cfg.head_dim, cfg.page_size, scale, p(self.out),
+                self.out.stride(0), None, None, v_dtype, stream), "paged_attn")
+        _lib.check(L.call(
+            "optimus_device_row_src", p(M["counts"]), p(self.slots), p(M["cu_rows"]), p(M["row_req"]), cr,
+            fwd.rows_per_slot, fwd.version * fwd.max_slots * fwd.rows_per_slot, p(M["row_src"]), stream),
+            "device_row_src")
+        dt = 0 if self.logits.dtype == torch.bfloat16 else 1
+        _lib.check(L.call(
+            "optimus_unmask_partials_dev", p(self.logits), dt, self.logits.stride(0), p(M["row_src"]), cr,
+            p(M["counts"][1:]), self.logits.shape[-1], fwd.vocab_offset, self.n_vsplit, p(self.part), stream),
+            "unmask_partials_dev")
+        ops.unmask_finalize(self.part, 1, cr, self.n_vsplit, M["cu_rows"], cfg.confidence_threshold, cfg.fallback,
+                            result=self.res, stream=torch.cuda.ExternalStream(stream))
+        _lib.check(L.call(
+            "optimus_device_apply", n, p(self.slots), cfg.block_size, p(M["cu_seqlens"]), p(M["tok_pos"]),
+            p(M["cu_rows"]), p(M["row_pos"]), p(self.res.commit_mask), p(D["states"]), D["states"].shape[1],
+            p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
+            p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["status"]), stream),
+            "device_apply")
+        for k in ("counts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
+            self.H[k].copy_(M[k], non_blocking=True)
+        self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
+
+    def capture(self) -> None:
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        # the captured step mutates the device state: capture on a scratch copy,
+        # then restore it
+        saved = {k: v.clone() for k, v in self.D.items()}
+        with torch.cuda.stream(s):
+            self._enqueue(s.cuda_stream)  # warm (lazy kernel attributes)
+            s.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=s):
+                self._enqueue(s.cuda_stream)
+        torch.cuda.synchronize()
+        for k, v in saved.items():
+            self.D[k].copy_(v)
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------------ host
+    def step(self, summaries: bool = True):
+        """One iteration: replay the graph, then replay the same transitions on the
+        host mirror (Request objects) from the copied plan and commit mask."""
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+        torch.cuda.current_stream().synchronize()
+        H = self.H
+        n = self.n
+        n_tok, n_rows = int(H["counts"][0]), int(H["counts"][1])
+        if int(H["counts"][3]) != 0:
+            raise ConfigError("device plan rejected the step (capacity or chunk bounds)")
+        cu = H["cu_seqlens"].numpy()[: n + 1]
+        cur = H["cu_rows"].numpy()[: n + 1]
+        tok_pos = np.ascontiguousarray(H["tok_pos"].numpy()[: max(n_tok, 1)])
+        row_pos = np.ascontiguousarray(H["row_pos"].numpy()[: max(n_rows, 1)])
+        mask = np.ascontiguousarray(H["mask"].numpy()[: max(n_rows, 1)])
+        cu_c, cur_c = np.ascontiguousarray(cu), np.ascontiguousarray(cur)
+        commits = np.zeros(n, dtype=np.int32)
+        bs = self.bs
+        bp = self.nat._bsp
+        st = self.nat.lib.optimus_host_apply(
+            n, self.slots_h.ctypes.data, self.cfg.block_size, cu_c.ctypes.data, tok_pos.ctypes.data,
+            cur_c.ctypes.data, row_pos.ctypes.data, mask.ctypes.data, bp["states"], bs.states.shape[1],
+            bp["queue"], bs.qcap, bp["q_head"], bp["q_len"], bp["block_index"], bp["committed"],
+            bp["steps_taken"], bp["cached_prefix"], bp["out_len"], commits.ctypes.data)
+        _lib.check(st, "optimus_host_apply")
+        if not summaries:
+            return int(commits.sum())
+        out = []
+        for r in range(n):
+            a, b = int(cur[r]), int(cur[r + 1])
+            out.append(StepSummary(computed=int(cu[r + 1] - cu[r]),
+                                   commits=frozenset(row_pos[a:b][mask[a:b].astype(bool)].tolist())))
+        return out
+
+    def finished(self) -> bool:
+        return all(r.finished for r in self.requests)

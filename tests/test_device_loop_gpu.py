@@ -1,0 +1,67 @@
+"""The graph-captured device loop (device_loop.DeviceLoop: plan, work list, K1/K2,
+unmask and apply all on the device) against the host native step
+(NativeStepper: host planning, one H2D, device step, one D2H, host apply) on the
+same requests and logits: identical Request states and commits, step by step,
+through the end of every request."""
+
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import bench
+from paper_2605_24832_b200.decode import DecodeConfig, StreamingDecoder
+from paper_2605_24832_b200.device_loop import DeviceLoop
+from paper_2605_24832_b200.synthetic import SyntheticForward
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(seed, batch, chunk, page=64, layers=2):
+    class A:
+        pass
+    a = A()
+    a.workload, a.chunk, a.page, a.batch, a.seed, a.steps = "sharegpt", chunk, page, batch, seed, 1
+    reqs = bench.workload_requests(a)
+    cfg = DecodeConfig(num_layers=layers, page_size=page, max_batch=batch,
+                       num_pages=bench.pages_needed(reqs, page) + 2 * batch + 64,
+                       max_pages_per_req=max((r.prompt_tokens + r.output_tokens + page - 1) // page for r in reqs) + 2)
+    dev = torch.device("cuda")
+    fwd = SyntheticForward(cfg, batch * chunk, batch, device=dev, seed=seed)
+    dec = StreamingDecoder(cfg, fwd, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    for l in range(cfg.num_layers):
+        dec.cache.k[l].normal_(generator=g)
+        dec.cache.v[l].normal_(generator=g)
+    return reqs, dec
+
+
+@pytest.mark.parametrize("batch,chunk", [(12, 32), (24, 8)])
+def test_device_loop_matches_host_native_step(batch, chunk):
+    reqs_h, dec_h = _setup(3, batch, chunk)
+    reqs_d, dec_d = _setup(3, batch, chunk)
+    loop = DeviceLoop(dec_d, reqs_d, chunk)
+    steps = 0
+    while not all(r.finished for r in reqs_h):
+        active = [r for r in reqs_h if not r.finished]
+        sh = dec_h.step(active, chunk)
+        sd = loop.step()
+        by_id = {r.id: s for r, s in zip(active, sh)}
+        for r, s in zip(reqs_d, sd):
+            if r.id in by_id:
+                assert set(s.commits) == set(by_id[r.id].commits), (steps, r.id)
+                assert s.computed == by_id[r.id].computed
+            else:
+                assert s.computed == 0 and not s.commits
+        for a, b in zip(reqs_h, reqs_d):
+            assert np.array_equal(a.states, b.states), (steps, a.id)
+            assert list(a.uncached_queue) == list(b.uncached_queue)
+            assert (a.block_index, a.committed, a.steps_taken) == (b.block_index, b.committed, b.steps_taken)
+        steps += 1
+        assert steps < 5000
+    assert loop.finished()
+    # the device state ended where the host mirror did
+    for k in ("states", "block_index", "committed", "steps_taken"):
+        assert np.array_equal(loop.D[k].cpu().numpy(), getattr(loop.bs, k)), k
