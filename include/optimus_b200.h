@@ -289,14 +289,27 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
                          int32_t* commits_out, int32_t* status, void* stream);
 
 /*
- * Device twin of optimus_attn_plan's whole-unit placement (its candidate A): same
- * work / cta_off / groups output as the host planner under OPTIMUS_PLAN_FORCE=whole,
- * from device-resident cu_seqlens / key_end (n_req <= 256, <= 4096 units and pieces,
- * grid <= 1024).  counts[0..4) = {n_work, n_groups, n_partials, status}.
+ * Device twin of optimus_attn_plan (capi.cu) from device-resident cu_seqlens /
+ * key_end (n_req <= 256, <= 4096 units and pieces, grid <= 1024).  allow_cut = 0:
+ * its whole-unit placement (candidate A), output identical to the host planner under
+ * OPTIMUS_PLAN_FORCE=whole.  allow_cut = 1: units costlier than the per-CTA budget are
+ * cut into equal pieces when the longest unit would otherwise set the makespan (the
+ * host's candidate-B rule), merged by optimus_paged_attn_combine_dev.
+ * counts[0..4) = {n_work, n_groups, n_partials, status}.
  */
 int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, const int32_t* key_end, int num_q_heads,
-                             int num_kv_heads, int grid, int page_size, int32_t* work, int max_work,
+                             int num_kv_heads, int grid, int page_size, int allow_cut, int32_t* work, int max_work,
                              int32_t* cta_off, int32_t* groups, int max_groups, int32_t* counts, void* stream);
+
+/*
+ * Split-KV combine of a device-planned step: merges the partials of the groups
+ * optimus_device_attn_plan wrote (their count read from n_groups_dev = &counts[1];
+ * max_groups = the groups buffer capacity).  Launch right after the layer's
+ * optimus_paged_attn, with the same ws_o / ws_ml workspace.
+ */
+int optimus_paged_attn_combine_dev(const int32_t* groups, const int32_t* n_groups_dev, int max_groups,
+                                   const float* ws_o, const float* ws_ml, int num_q_heads, int num_kv_heads,
+                                   int head_dim, void* out, int64_t out_stride_tok, void* stream);
 
 /*
  * Device-planned steps (counts produced on the device by optimus_device_plan):

@@ -81,8 +81,9 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "optimus_device_apply": (_i32, [_i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _vp,
                                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "optimus_device_attn_plan": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp,
-                                        _vp]),
+    "optimus_device_attn_plan": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
+                                        _vp, _vp]),
+    "optimus_paged_attn_combine_dev": (_i32, [_vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _vp]),
     "optimus_kv_append_dev": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _i32, _i32, _i32, _vp,
                                      _vp, _i32, _vp]),
     "optimus_unmask_partials_dev": (_i32, [_vp, _i32, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp]),

@@ -45,6 +45,8 @@ struct AttnParams {
 
 int launch_paged_attn_dual(int head_dim, bool v_fp16, const CUtensorMap& tq, const CUtensorMap& tk,
                            const CUtensorMap& tv, const AttnParams& prm, int grid, cudaStream_t stream);
+int launch_attn_combine_dev(int head_dim, const AttnParams& prm, const int32_t* groups, int max_groups,
+                            const int32_t* n_groups_dev, cudaStream_t stream);
 int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CUtensorMap& tk,
                       const CUtensorMap& tv, const AttnParams& prm, int grid,
                       const int32_t* groups, int n_groups, cudaStream_t stream);

@@ -624,6 +624,27 @@ int optimus_paged_attn(const void* q, int64_t q_stride_tok, int n_tok_total, con
                          stream);
 }
 
+// Split-KV combine for a device-planned step: the group count is read from
+// n_groups_dev (optimus_device_attn_plan's counts[1]); max_groups bounds the grid.
+int optimus_paged_attn_combine_dev(const int32_t* groups, const int32_t* n_groups_dev, int max_groups,
+                                   const float* ws_o, const float* ws_ml, int hq, int hkv, int head_dim,
+                                   void* out, int64_t out_stride_tok, void* stream) {
+  if (head_dim != 64 && head_dim != 128) return fail("paged_attn_combine_dev: head_dim must be 64 or 128");
+  if (hkv < 1 || hq % hkv || hq / hkv > 128) return fail("paged_attn_combine_dev: bad head counts");
+  if (max_groups < 0 || !n_groups_dev) return fail("paged_attn_combine_dev: bad group capacity");
+  if (max_groups == 0) return 0;
+  if (!ws_o || !ws_ml) return fail("paged_attn_combine_dev: split-KV needs a workspace");
+  optimus::AttnParams prm = {};
+  prm.ws_o = const_cast<float*>(ws_o);
+  prm.ws_ml = const_cast<float*>(ws_ml);
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.out_stride_tok = out_stride_tok;
+  prm.group = hq / hkv;
+  return cuda_status(optimus::launch_attn_combine_dev(head_dim, prm, groups, max_groups, n_groups_dev,
+                                                      static_cast<cudaStream_t>(stream)),
+                     "paged_attn_combine_dev");
+}
+
 int optimus_paged_attn_append(const void* q, int64_t q_stride_tok, int n_tok_total,
                               const void* k_new, const void* v_new, int64_t new_stride_tok,
                               void* k_cache, void* v_cache, int64_t num_pages,

@@ -437,7 +437,7 @@ constexpr int kMaxUnits = 4096;
 
 __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     int n_req, const int32_t* __restrict__ cu, const int32_t* __restrict__ key_end, int hkv, int T, int grid,
-    int hard_cap, int32_t* __restrict__ work, int max_work, int32_t* __restrict__ cta_off,
+    int hard_cap, int allow_cut, int32_t* __restrict__ work, int max_work, int32_t* __restrict__ cta_off,
     int32_t* __restrict__ groups, int max_groups, int32_t* __restrict__ counts) {
   extern __shared__ uint8_t sm_raw[];
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm_raw);  // [kMaxUnits]
@@ -452,6 +452,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
   int* p_nt = p_t0 + kMaxUnits;
   int* p_cta = p_nt + kMaxUnits;
   int* p_slot = p_cta + kMaxUnits;
+  int* u_sc = p_slot + kMaxUnits;  // pieces per unit
   __shared__ int req_off[257];
   __shared__ int n_units_s, n_pieces_s, bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -515,6 +516,37 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     }
   // 3. LPT placement by warp 0 (loads in half-tiles, CTA c held by lane c % 32)
   if (warp == 0) {
+    // 3a. pieces per unit: the page cap, and with allow_cut a balanced cut of every
+    // unit costlier than the per-CTA budget (mean load + one item) when the longest
+    // unit exceeds the budget by more than the combine launch (the host planner's
+    // candidate-B rule, capacity permitting).
+    long long total = 0;
+    for (int u = lane; u < nu; u += 32) total += 2LL * u_tiles[u] + 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xFFFFFFFFu, total, off);
+    const long long budget = (total + grid - 1) / grid + 5;
+    const long long longest = nu > 0 ? 2LL * u_tiles[static_cast<int>(keys[0] & 0xFFFFFFFFu)] + 5 : 0;
+    const int nt_max = static_cast<int>(max(4LL, (budget - 8) / 2));
+    bool cut = allow_cut && 100 * (budget + 14) < 97 * longest;
+    for (int pass = 0; pass < 2; ++pass) {
+      int pieces = 0, cut_units = 0;
+      for (int u = lane; u < nu; u += 32) {
+        const int tiles = u_tiles[u];
+        int sc = (tiles + hard_cap - 1) / hard_cap;
+        if (cut && 2LL * tiles + 5 > budget) sc = max(sc, (tiles + nt_max - 1) / nt_max);
+        u_sc[u] = sc;
+        pieces += sc;
+        cut_units += sc > 1;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        pieces += __shfl_xor_sync(0xFFFFFFFFu, pieces, off);
+        cut_units += __shfl_xor_sync(0xFFFFFFFFu, cut_units, off);
+      }
+      if (!cut || (pieces <= min(max_work, kMaxUnits) && cut_units <= max_groups)) break;
+      cut = false;  // over capacity: whole units
+    }
+    __syncwarp();
     constexpr int kPer = 32;  // CTAs per lane (grid <= 1024)
     long long load[kPer];
 #pragma unroll
@@ -523,7 +555,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     for (int o = 0; o < nu; ++o) {
       const int u = static_cast<int>(keys[o] & 0xFFFFFFFFu);
       const int tiles = u_tiles[u];
-      const int sc = (tiles + hard_cap - 1) / hard_cap;
+      const int sc = u_sc[u];
       const int base = tiles / sc, rem = tiles % sc;
       if (lane == 0) u_first[u] = np;
       int t0 = 0;
@@ -570,8 +602,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
   if (tid == 0) {
     int ng = 0, npart = 0;
     for (int u = 0; u < nu; ++u) {
-      const int tiles = u_tiles[u];
-      const int sc = (tiles + hard_cap - 1) / hard_cap;
+      const int sc = u_sc[u];
       const int f = u_first[u];
       if (sc > 1) {
         if (ng >= max_groups) {
@@ -624,7 +655,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
 }  // namespace optimus
 
 extern "C" int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, const int32_t* key_end, int hq,
-                                        int hkv, int grid, int page_size, int32_t* work, int max_work,
+                                        int hkv, int grid, int page_size, int allow_cut, int32_t* work, int max_work,
                                         int32_t* cta_off, int32_t* groups, int max_groups, int32_t* counts,
                                         void* stream) {
   using namespace optimus::dstep;
@@ -632,14 +663,14 @@ extern "C" int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, co
   const int G = hq / hkv;
   if (G > 128) return OPTIMUS_EINVAL;
   const int hard_cap = static_cast<int>(std::max(1LL, std::min((255LL * std::max(page_size, 1)) / 64, 1LL << 20)));
-  const size_t smem = kMaxUnits * (8 + 11 * 4);
+  const size_t smem = kMaxUnits * (8 + 12 * 4);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(work_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
   work_plan_kernel<<<1, kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      n_req, cu_seqlens, key_end, hkv, 128 / G, grid, hard_cap, work, max_work, cta_off, groups, max_groups,
+      n_req, cu_seqlens, key_end, hkv, 128 / G, grid, hard_cap, allow_cut, work, max_work, cta_off, groups, max_groups,
       counts);
   return static_cast<int>(cudaGetLastError());
 }

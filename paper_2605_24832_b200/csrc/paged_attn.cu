@@ -803,55 +803,90 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __rest
                                                            const float* __restrict__ ws_o,
                                                            const float* __restrict__ ws_ml,
                                                            __nv_bfloat16* __restrict__ out,
-                                                           int64_t out_stride_tok, int group_sz) {
-  const int* gr = groups + 8 * blockIdx.x;
-  const int head = gr[1], tok_begin = gr[2], n_tok = gr[3], slot0 = gr[4], n_split = gr[5];
+                                                           int64_t out_stride_tok, int group_sz,
+                                                           int n_groups,
+                                                           const int32_t* __restrict__ n_groups_dev) {
+  // device-planned steps: the group count is read from device memory and the grid,
+  // sized for capacity, strides over the groups
+  if (n_groups_dev != nullptr) n_groups = *n_groups_dev;
   const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (r >= n_tok * group_sz) return;
-  grid_dep_wait();  // partials of the preceding attention grid are visible after this
-  const float2* ml = reinterpret_cast<const float2*>(ws_ml);
-  float mx = -INFINITY;
-  for (int s = lane; s < n_split; s += 32) {
-    const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
-    if (v.y > 0.f) mx = fmaxf(mx, v.x);
-  }
+  for (int gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+    const int* gr = groups + 8 * gi;
+    const int head = gr[1], tok_begin = gr[2], n_tok = gr[3], slot0 = gr[4], n_split = gr[5];
+    if (r >= n_tok * group_sz) continue;
+    grid_dep_wait();  // partials of the preceding attention grid are visible after this
+    const float2* ml = reinterpret_cast<const float2*>(ws_ml);
+    float mx = -INFINITY;
+    for (int s = lane; s < n_split; s += 32) {
+      const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
+      if (v.y > 0.f) mx = fmaxf(mx, v.x);
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-  float den = 0.f;
-  for (int s = lane; s < n_split; s += 32) {
-    const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
-    if (v.y > 0.f) den += exp2f(v.x - mx) * v.y;
-  }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    float den = 0.f;
+    for (int s = lane; s < n_split; s += 32) {
+      const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
+      if (v.y > 0.f) den += exp2f(v.x - mx) * v.y;
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xFFFFFFFFu, den, o);
-  constexpr int PER = HD / 32;  // columns per lane (4 for HD=128, 2 for HD=64)
-  float acc[PER];
+    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xFFFFFFFFu, den, o);
+    constexpr int PER = HD / 32;  // columns per lane (4 for HD=128, 2 for HD=64)
+    float acc[PER];
 #pragma unroll
-  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
-  for (int s = 0; s < n_split; ++s) {
-    const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
-    if (!(v.y > 0.f)) continue;
-    const float wgt = exp2f(v.x - mx);
-    const float* src = ws_o + (static_cast<int64_t>(slot0 + s) * kBlockM + r) * HD + lane * PER;
+    for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+    for (int s = 0; s < n_split; ++s) {
+      const float2 v = ml[static_cast<int64_t>(slot0 + s) * kBlockM + r];
+      if (!(v.y > 0.f)) continue;
+      const float wgt = exp2f(v.x - mx);
+      const float* src = ws_o + (static_cast<int64_t>(slot0 + s) * kBlockM + r) * HD + lane * PER;
+      if constexpr (PER == 4) {
+        const float4 o = *reinterpret_cast<const float4*>(src);
+        acc[0] += wgt * o.x; acc[1] += wgt * o.y; acc[2] += wgt * o.z; acc[3] += wgt * o.w;
+      } else {
+        const float2 o = *reinterpret_cast<const float2*>(src);
+        acc[0] += wgt * o.x; acc[1] += wgt * o.y;
+      }
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const int t = r / group_sz, g = r - t * group_sz;
+    __nv_bfloat16* dst = out + static_cast<int64_t>(tok_begin + t) * out_stride_tok +
+                         static_cast<int64_t>(head * group_sz + g) * HD + lane * PER;
     if constexpr (PER == 4) {
-      const float4 o = *reinterpret_cast<const float4*>(src);
-      acc[0] += wgt * o.x; acc[1] += wgt * o.y; acc[2] += wgt * o.z; acc[3] += wgt * o.w;
+      *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(acc[0] * inv, acc[1] * inv),
+                                                  pack_bf16x2(acc[2] * inv, acc[3] * inv));
     } else {
-      const float2 o = *reinterpret_cast<const float2*>(src);
-      acc[0] += wgt * o.x; acc[1] += wgt * o.y;
+      *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(acc[0] * inv, acc[1] * inv);
     }
   }
-  const float inv = den > 0.f ? 1.f / den : 0.f;
-  const int t = r / group_sz, g = r - t * group_sz;
-  __nv_bfloat16* dst = out + static_cast<int64_t>(tok_begin + t) * out_stride_tok +
-                       static_cast<int64_t>(head * group_sz + g) * HD + lane * PER;
-  if constexpr (PER == 4) {
-    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(acc[0] * inv, acc[1] * inv),
-                                                pack_bf16x2(acc[2] * inv, acc[3] * inv));
-  } else {
-    *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(acc[0] * inv, acc[1] * inv);
-  }
+}
+
+// Launch the combine with PDL after the attention grid; n_groups_dev != nullptr: the
+// count is on the device and the grid covers min(n_groups, 32) groups per pass.
+template <int HD>
+static int launch_combine_t(const AttnParams& prm, const int32_t* groups, int n_groups,
+                            const int32_t* n_groups_dev, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_groups_dev ? (n_groups < 32 ? n_groups : 32) : n_groups, kBlockM / 8);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, attn_combine_kernel<HD>, groups,
+                                             static_cast<const float*>(prm.ws_o),
+                                             static_cast<const float*>(prm.ws_ml), prm.out,
+                                             prm.out_stride_tok, prm.group, n_groups, n_groups_dev));
+}
+
+int launch_attn_combine_dev(int head_dim, const AttnParams& prm, const int32_t* groups, int max_groups,
+                            const int32_t* n_groups_dev, cudaStream_t stream) {
+  if (max_groups <= 0) return 0;
+  return head_dim == 128 ? launch_combine_t<128>(prm, groups, max_groups, n_groups_dev, stream)
+                         : launch_combine_t<64>(prm, groups, max_groups, n_groups_dev, stream);
 }
 
 template <int HD, int KST, int VST, bool VF16>
@@ -886,20 +921,7 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   if (n_groups > 0) {
     // PDL: the combine's CTAs are resident before K2 drains; they wait on
     // griddepcontrol.wait before reading the partials.
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(n_groups, kBlockM / 8);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, attn_combine_kernel<HD>, groups,
-                                       static_cast<const float*>(prm.ws_o),
-                                       static_cast<const float*>(prm.ws_ml), prm.out,
-                                       prm.out_stride_tok, prm.group);
+    cudaError_t e = static_cast<cudaError_t>(launch_combine_t<HD>(prm, groups, n_groups, nullptr, stream));
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   return 0;

@@ -4,8 +4,8 @@
 (sim.py:269-305) as ONE CUDA graph on device-resident request state:
 
     optimus_device_plan       plan_chunk for every request + the step metadata
-    optimus_device_attn_plan  the attention work list (whole-unit LPT placement)
-    L x (optimus_kv_append_dev, optimus_paged_attn)
+    optimus_device_attn_plan  the attention work list (LPT placement, balanced split-KV cuts)
+    L x (optimus_kv_append_dev, optimus_paged_attn, optimus_paged_attn_combine_dev)
     optimus_device_row_src, optimus_unmask_partials_dev, optimus_unmask_finalize
     optimus_device_apply      apply_chunk + advance_blocks
     D2H of the plan arrays and the commit mask into pinned buffers
@@ -20,7 +20,7 @@ zero tokens); every request's pages are allocated up front.
 
 from __future__ import annotations
 
-import ctypes as C
+import time
 
 import numpy as np
 import torch
@@ -51,8 +51,6 @@ class DeviceLoop:
             slots.append(s)
         self.slots_h = np.asarray(slots, dtype=np.int32)
         max_pages = cfg.max_pages_per_req
-        if max(r.prompt_tokens + r.output_tokens for r in self.requests) > 255 * cfg.page_size:
-            raise ConfigError("DeviceLoop: an item would exceed 255 pages (split-KV groups need the host planner)")
         bs = nat.bs
         self.bs = bs
         self.state_keys = ("states", "queue", "q_head", "q_len", "block_index", "committed", "steps_taken",
@@ -71,11 +69,18 @@ class DeviceLoop:
         M["block_tables"] = torch.zeros((n, max_pages), dtype=torch.int32, device=dev)
         G = cfg.num_q_heads // cfg.num_kv_heads
         T = 128 // G
-        self.max_work = n * cfg.num_kv_heads * ((self.chunk + T - 1) // T) * 2
         self.grid = decoder.grid
+        # units + the cut pieces (a balanced cut adds < 2 pieces per CTA) + page-cap cuts
+        units = n * cfg.num_kv_heads * ((self.chunk + T - 1) // T)
+        cap_cuts = units * (-(-max(r.prompt_tokens + r.output_tokens for r in self.requests)
+                               // (255 * cfg.page_size)) - 1)
+        self.max_work = min(4096, units + 2 * self.grid + 64 + cap_cuts)
         M["work"] = torch.zeros((self.max_work, 8), dtype=torch.int32, device=dev)
         M["cta_off"] = z(self.grid + 1)
-        M["groups"] = torch.zeros((64, 8), dtype=torch.int32, device=dev)
+        M["groups"] = torch.zeros((min(units, 1024), 8), dtype=torch.int32, device=dev)
+        # split-KV partials (m, l, O) of the cut pieces: at most one per work item
+        self.ws_o = torch.empty(self.max_work * 128 * cfg.head_dim, dtype=torch.float32, device=dev)
+        self.ws_ml = torch.empty(self.max_work * 128 * 2, dtype=torch.float32, device=dev)
         M["wcounts"] = z(4)
         self.M = M
         fwd = decoder.forward
@@ -86,9 +91,10 @@ class DeviceLoop:
         self.out = torch.empty((ct, cfg.num_q_heads, cfg.head_dim), dtype=torch.bfloat16, device=dev)
         # pinned host mirrors of what the host replay needs
         self.H = {k: torch.zeros(M[k].numel(), dtype=torch.int32, pin_memory=True)
-                  for k in ("counts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos")}
+                  for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos")}
         self.H["mask"] = torch.zeros(max(cr, 1), dtype=torch.uint8, pin_memory=True)
         self.graph = None
+        self.t_device = 0.0  # host seconds spent in replay + sync (diagnostics)
 
     # ------------------------------------------------------------------ device
     def _enqueue(self, stream) -> None:
@@ -106,7 +112,7 @@ class DeviceLoop:
             p(M["row_pos"]), p(M["row_req"]), cr, p(M["block_tables"]), p(M["counts"]), stream), "device_plan")
         _lib.check(L.call(
             "optimus_device_attn_plan", n, p(M["cu_seqlens"]), p(M["key_end"]), cfg.num_q_heads, cfg.num_kv_heads,
-            self.grid, cfg.page_size, p(M["work"]), self.max_work, p(M["cta_off"]), p(M["groups"]),
+            self.grid, cfg.page_size, 1, p(M["work"]), self.max_work, p(M["cta_off"]), p(M["groups"]),
             M["groups"].shape[0], p(M["wcounts"]), stream), "device_attn_plan")
         fwd = self.dec.forward
         scale = 1.0 / float(cfg.head_dim) ** 0.5
@@ -125,7 +131,11 @@ class DeviceLoop:
                 p(M["tok_pos"]), p(M["prompt_len"]), p(M["vis_base"]), p(M["vis_off"]), p(M["vis_words"]),
                 p(M["block_tables"]), M["block_tables"].shape[1], p(M["work"]), p(M["cta_off"]), self.grid,
                 p(M["groups"]), 0, cfg.block_size, hq, hkv, cfg.head_dim, cfg.page_size, scale, p(self.out),
-                self.out.stride(0), None, None, v_dtype, stream), "paged_attn")
+                self.out.stride(0), p(self.ws_o), p(self.ws_ml), v_dtype, stream), "paged_attn")
+            _lib.check(L.call(
+                "optimus_paged_attn_combine_dev", p(M["groups"]), p(M["wcounts"][1:]), M["groups"].shape[0],
+                p(self.ws_o), p(self.ws_ml), hq, hkv, cfg.head_dim, p(self.out), self.out.stride(0), stream),
+                "paged_attn_combine_dev")
         _lib.check(L.call(
             "optimus_device_row_src", p(M["counts"]), p(self.slots), p(M["cu_rows"]), p(M["row_req"]), cr,
             fwd.rows_per_slot, fwd.version * fwd.max_slots * fwd.rows_per_slot, p(M["row_src"]), stream),
@@ -143,7 +153,7 @@ class DeviceLoop:
             p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
             p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["status"]), stream),
             "device_apply")
-        for k in ("counts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
+        for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
             self.H[k].copy_(M[k], non_blocking=True)
         self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
 
@@ -170,13 +180,17 @@ class DeviceLoop:
         host mirror (Request objects) from the copied plan and commit mask."""
         if self.graph is None:
             self.capture()
+        t0 = time.perf_counter()
         self.graph.replay()
         torch.cuda.current_stream().synchronize()
+        self.t_device += time.perf_counter() - t0
         H = self.H
         n = self.n
         n_tok, n_rows = int(H["counts"][0]), int(H["counts"][1])
         if int(H["counts"][3]) != 0:
             raise ConfigError("device plan rejected the step (capacity or chunk bounds)")
+        if int(H["wcounts"][3]) != 0:
+            raise ConfigError("device attention planner rejected the step (work / group capacity)")
         cu = H["cu_seqlens"].numpy()[: n + 1]
         cur = H["cu_rows"].numpy()[: n + 1]
         tok_pos = np.ascontiguousarray(H["tok_pos"].numpy()[: max(n_tok, 1)])

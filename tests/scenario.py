@@ -36,7 +36,12 @@ def make_requests(seed: int, n_req: int, prompt_range, out_range, chunk: int, bl
     rng = np.random.default_rng(seed)
     reqs = []
     for i in range(n_req):
-        prompt = int(fixed_prompt) if fixed_prompt is not None else int(rng.integers(*prompt_range))
+        if fixed_prompt is None or isinstance(fixed_prompt, dict):
+            prompt = int(rng.integers(*prompt_range))
+            if fixed_prompt is not None:  # per-request overrides
+                prompt = int(fixed_prompt.get(i, prompt))
+        else:
+            prompt = int(fixed_prompt)
         out = int(rng.integers(*out_range))
         r = Request(id=i, arrival_time=0.0, prompt_tokens=prompt, output_tokens=out,
                     rng=np.random.default_rng(seed * 1000 + i))

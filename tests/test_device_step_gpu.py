@@ -157,7 +157,7 @@ def test_device_work_planner_matches_host_whole_unit_plan(hq, hkv, page, maxq, k
         groups = torch.zeros((1024, 8), dtype=torch.int32, device="cuda")
         cnt = torch.zeros(4, dtype=torch.int32, device="cuda")
         dcu, dke = _dev(cu), _dev(ke)  # keep the device copies alive across the launch
-        st = L.optimus_device_attn_plan(n, _p(dcu), _p(dke), hq, hkv, grid, page, _p(work), mw, _p(off),
+        st = L.optimus_device_attn_plan(n, _p(dcu), _p(dke), hq, hkv, grid, page, 0, _p(work), mw, _p(off),
                                         _p(groups), 1024, _p(cnt), torch.cuda.current_stream().cuda_stream)
         assert st == 0
         torch.cuda.synchronize()

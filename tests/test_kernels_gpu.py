@@ -101,6 +101,13 @@ def _attn_check(s, min_split_tiles=4, grid=None):
                               s["dm"].vis_off, s["dm"].vis_words, s["dm"].block_tables, plan,
                               s["block"])
     torch.cuda.synchronize()
+    err = _attn_compare(s, out, kc, vc, q, plan.n_groups)
+    return plan, err, out.float().cpu().numpy(), None
+
+
+def _attn_compare(s, out, kc, vc, q, n_groups):
+    """Global and per-element error of a K2 output against the fp64 oracle."""
+    m = s["meta"]
     got = out.float().cpu().numpy()
     kf = kc.float().cpu().numpy()
     vf = vc.float().cpu().numpy()
@@ -114,9 +121,9 @@ def _attn_check(s, min_split_tiles=4, grid=None):
     ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
     viol = np.abs(got - ref) / np.maximum(ulp, ATTN_RTOL * rms)
     print(f"ATTN global_vs_fp32={glob:.3e} (bf16 floor {floor:.3e}) max_elem_viol={viol.max():.3f} "
-          f"n_groups={plan.n_groups}")
+          f"n_groups={n_groups}")
     assert glob < ATTN_RTOL, glob
-    return plan, float(viol.max()) * ATTN_RTOL, got, ref
+    return float(viol.max()) * ATTN_RTOL
 
 
 @pytest.mark.parametrize("chunk", [1, 4, 8, 16, 32])
@@ -143,6 +150,70 @@ def test_paged_attention_long_context_split_kv():
     s = _step(99, 6, 8, 32, 64, 32, 8, 128, prompt_range=(4096, 9000), out_range=(20, 120))
     plan, err, got, ref = _attn_check(s, min_split_tiles=4, grid=148)
     assert plan.n_groups > 0
+    assert err <= ATTN_RTOL, err
+
+
+@pytest.mark.parametrize("case", ["one_long", "all_long", "short"])
+def test_device_planned_split_kv_matches_oracle(case):
+    """optimus_device_attn_plan with cutting -> optimus_paged_attn (partials) ->
+    optimus_paged_attn_combine_dev (group count read on the device) == the oracle."""
+    from paper_2605_24832_b200 import _lib
+    rng_p = {"one_long": None, "all_long": (3000, 9000), "short": (1, 300)}[case]
+    s = _step(123, 24, 8, 32, 16, 32, 8, 128, prompt_range=rng_p or (1, 300))
+    if case == "one_long":  # one LongBench-sized request among short ones sets the makespan
+        s = _step(124, 24, 8, 32, 16, 32, 8, 128, prompt_range=(1, 300), fixed_prompt={0: 12000})
+    dev = torch.device("cuda")
+    kc, vc, _ = _run_append(s)
+    m, dm = s["meta"], s["dm"]
+    q = s["q"].to(dev)[: m.n_tok]
+    grid = 148
+    L = _lib.load()
+    mw, mg = 4096, 1024
+    work = torch.zeros((mw, 8), dtype=torch.int32, device=dev)
+    off = torch.zeros(grid + 1, dtype=torch.int32, device=dev)
+    groups = torch.zeros((mg, 8), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(4, dtype=torch.int32, device=dev)
+    dcu = torch.from_numpy(np.ascontiguousarray(m.cu_seqlens, dtype=np.int32)).to(dev)
+    dke = torch.from_numpy(np.ascontiguousarray(m.key_end, dtype=np.int32)).to(dev)
+    st = L.optimus_device_attn_plan(len(m.key_end), dcu.data_ptr(), dke.data_ptr(), 32, 8, grid, 16, 1,
+                                    work.data_ptr(), mw, off.data_ptr(), groups.data_ptr(), mg, cnt.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    c = cnt.cpu().tolist()
+    assert c[3] == 0
+    # structure: each unit's pieces tile [0, key_end) in order; groups <-> cut units
+    w = work.cpu().numpy()[: c[0]]
+    o = off.cpu().numpy()
+    assert o[0] == 0 and o[-1] == c[0] and np.all(np.diff(o) >= 0)
+    keyed = {}
+    for r in w:
+        keyed.setdefault((r[0], r[1], r[2]), []).append((r[4], r[5], r[6]))
+    n_cut = 0
+    for (req, _, _), pcs in keyed.items():
+        pcs.sort()
+        assert pcs[0][0] == 0 and pcs[-1][1] == m.key_end[req]
+        assert all(pcs[i][1] == pcs[i + 1][0] for i in range(len(pcs) - 1))
+        assert all((p[2] >= 0) == (len(pcs) > 1) for p in pcs)
+        n_cut += len(pcs) > 1
+    assert n_cut == c[1]
+    if case != "short":
+        assert c[1] > 0  # the long units were cut
+    out = torch.empty((m.n_tok, 32, 128), dtype=torch.bfloat16, device=dev)
+    ws_o = torch.empty(mw * 128 * 128, dtype=torch.float32, device=dev)
+    ws_ml = torch.empty(mw * 128 * 2, dtype=torch.float32, device=dev)
+    sp = torch.cuda.current_stream().cuda_stream
+    st = L.optimus_paged_attn(q.data_ptr(), q.stride(0), m.n_tok, kc.data_ptr(), vc.data_ptr(), kc.shape[0],
+                              dm.tok_pos.data_ptr(), dm.prompt_len.data_ptr(), dm.vis_base.data_ptr(),
+                              dm.vis_off.data_ptr(), dm.vis_words.data_ptr(), dm.block_tables.data_ptr(),
+                              dm.block_tables.shape[1], work.data_ptr(), off.data_ptr(), grid, groups.data_ptr(),
+                              0, s["block"], 32, 8, 128, 16, 1.0 / 128 ** 0.5, out.data_ptr(), out.stride(0),
+                              ws_o.data_ptr(), ws_ml.data_ptr(), ops._v_dtype(vc), sp)
+    assert st == 0
+    st = L.optimus_paged_attn_combine_dev(groups.data_ptr(), cnt[1:].data_ptr(), mg, ws_o.data_ptr(),
+                                          ws_ml.data_ptr(), 32, 8, 128, out.data_ptr(), out.stride(0), sp)
+    assert st == 0
+    err = _attn_compare(s, out, kc, vc, q, c[1])
     assert err <= ATTN_RTOL, err
 
 
