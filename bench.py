@@ -436,6 +436,7 @@ def main():
     # ---- end to end through the public per-step call (closed loop, live state)
     dec.release_all(reqs)
     e2e = run_e2e(args, dec, fwd, e2e_pool, world, dev)
+    dloop = run_device_loop(args, dec, world)
 
     hbm, peak_kind = peaks()
     achieved = k2b / (k2_us * 1e-6) / 1e9
@@ -482,6 +483,7 @@ def main():
         "roofline_target_4k": target,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_device_loop": dloop,
         "gpu_launches": n_launch * args.steps,
         "clocks": clocks,
     }
@@ -649,6 +651,7 @@ def run_e2e(args, dec, fwd, pool, world, dev):
         d2h += dec.d2h_bytes
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
+    dec.release_all(batch)
     if world > 1:
         t = torch.tensor([el], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -656,6 +659,40 @@ def run_e2e(args, dec, fwd, pool, world, dev):
     return {"value": commits / el, "unit": "tokens/s", "h2d_bytes_per_step": h2d // n_steps,
             "d2h_bytes_per_step": d2h // n_steps, "steps": n_steps, "ms_per_step": el / n_steps * 1e3,
             "path": "StreamingDecoder.step (plan_batch -> H2D meta -> L x (K1,K2) -> K3 -> D2H -> apply_batch)"}
+
+
+def run_device_loop(args, dec, world):
+    """Fixed batch through DeviceLoop: plan, attention work list, L x
+    (K1, K2, combine), K3 and apply as ONE CUDA graph on device-resident request
+    state; per step the host copies back the plan and commit mask and replays the
+    transitions on its Request objects.  No H2D per step (the state stays resident);
+    D2H = the plan arrays + mask.  Timed on the host clock around whole steps."""
+    import torch
+    from paper_2605_24832_b200.device_loop import DeviceLoop
+    from paper_2605_24832_b200.errors import ConfigError
+    if world != 1 or workload_spec(args.workload)["mixed"] or args.workload == "tp30b":
+        return None
+    reqs = workload_requests(args, seed_offset=3)
+    try:
+        loop = DeviceLoop(dec, reqs, args.chunk)
+    except (ConfigError, RuntimeError) as e:
+        dec.release_all(reqs)
+        return {"unavailable": str(e)[:200]}
+    n_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 20)
+    for _ in range(3):
+        loop.step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    commits = 0
+    for _ in range(n_steps):
+        commits += loop.step(summaries=False)
+    el = time.perf_counter() - t0
+    d2h = sum(t.numel() * t.element_size() for t in loop.H.values())
+    dec.release_all(reqs)
+    return {"value": commits / el, "unit": "tokens/s", "steps": n_steps, "ms_per_step": el / n_steps * 1e3,
+            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h, "batch": "fixed (finished requests idle)",
+            "path": "DeviceLoop.step (one graph: device plan -> work plan -> L x (K1,K2,combine) -> K3 -> "
+                    "device apply; D2H plan + mask -> host apply)"}
 
 
 if __name__ == "__main__":

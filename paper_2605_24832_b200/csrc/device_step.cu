@@ -435,6 +435,35 @@ namespace dstep {
 constexpr int kPlanThreads = 1024;
 constexpr int kMaxUnits = 4096;
 
+// Exclusive prefix sum over the block's kPlanThreads values (warp shuffles, then one
+// warp over the 32 warp totals); *total = the sum.  All threads must call it.
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* ws, unsigned* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= o) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  const unsigned pre = (warp ? ws[warp - 1] : 0u) + x - v;
+  *total = ws[31];
+  __syncthreads();  // ws is reused by the next call
+  return pre;
+}
+
+template <int KPER>  // CTAs per lane: grid <= 32 * KPER
 __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     int n_req, const int32_t* __restrict__ cu, const int32_t* __restrict__ key_end, int hkv, int T, int grid,
     int hard_cap, int allow_cut, int32_t* __restrict__ work, int max_work, int32_t* __restrict__ cta_off,
@@ -455,20 +484,25 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
   int* u_sc = p_slot + kMaxUnits;  // pieces per unit
   __shared__ int req_off[257];
   __shared__ int n_units_s, n_pieces_s, bad;
+  __shared__ unsigned scan_ws[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) bad = 0;
   // 1. units: per request hkv * ceil(nq / T), request-major then head then token group
+  unsigned n_units_req = 0;
   if (tid < n_req) {
     const int nq = cu[tid + 1] - cu[tid];
-    req_off[tid + 1] = nq > 0 ? hkv * ((nq + T - 1) / T) : 0;
+    n_units_req = nq > 0 ? hkv * ((nq + T - 1) / T) : 0;
     if (nq > 0 && key_end[tid] < 1) bad = 1;
   }
-  __syncthreads();
-  if (tid == 0) {
-    req_off[0] = 0;
-    for (int r = 0; r < n_req; ++r) req_off[r + 1] += req_off[r];
-    n_units_s = req_off[n_req];
-    if (n_units_s > kMaxUnits) bad = 1;
+  {
+    unsigned total;
+    const unsigned pre = block_exclusive_scan(n_units_req, scan_ws, &total);
+    if (tid < n_req) req_off[tid] = static_cast<int>(pre);
+    if (tid == 0) {
+      req_off[n_req] = static_cast<int>(total);
+      n_units_s = static_cast<int>(total);
+      if (total > static_cast<unsigned>(kMaxUnits)) bad = 1;
+    }
   }
   __syncthreads();
   if (bad) {
@@ -514,7 +548,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
       }
       __syncthreads();
     }
-  // 3. LPT placement by warp 0 (loads in half-tiles, CTA c held by lane c % 32)
+  // 3. placement (loads in half-tiles)
   if (warp == 0) {
     // 3a. pieces per unit: the page cap, and with allow_cut a balanced cut of every
     // unit costlier than the per-CTA budget (mean load + one item) when the longest
@@ -546,51 +580,41 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
       if (!cut || (pieces <= min(max_work, kMaxUnits) && cut_units <= max_groups)) break;
       cut = false;  // over capacity: whole units
     }
-    __syncwarp();
-    constexpr int kPer = 32;  // CTAs per lane (grid <= 1024)
-    long long load[kPer];
+  }
+  __syncthreads();
+  // 3b. the flat piece list in placement order (units longest first, each unit's
+  // pieces in key order) with each piece's cost: a block scan of the piece counts
+  {
+    constexpr int kPT = kMaxUnits / kPlanThreads;
+    const int o0 = tid * kPT;
+    unsigned v = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) load[i] = 0;
-    int np = 0;
-    for (int o = 0; o < nu; ++o) {
-      const int u = static_cast<int>(keys[o] & 0xFFFFFFFFu);
-      const int tiles = u_tiles[u];
-      const int sc = u_sc[u];
-      const int base = tiles / sc, rem = tiles % sc;
-      if (lane == 0) u_first[u] = np;
-      int t0 = 0;
-      for (int k = 0; k < sc; ++k, ++np) {
-        const int nt = base + (k < rem ? 1 : 0);
-        long long best = LLONG_MAX;
-        int bc = 0x7FFFFFFF;
+    for (int k = 0; k < kPT; ++k)
+      if (o0 + k < nu) v += static_cast<unsigned>(u_sc[static_cast<int>(keys[o0 + k] & 0xFFFFFFFFu)]);
+    unsigned total;
+    unsigned pre = block_exclusive_scan(v, scan_ws, &total);
+    if (tid == 0) n_pieces_s = static_cast<int>(total);
+    if (total <= static_cast<unsigned>(kMaxUnits)) {
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          const int c = lane + 32 * i;
-          if (c < grid && load[i] < best) {  // increasing c per lane: first minimum
-            best = load[i];
-            bc = c;
-          }
+      for (int k = 0; k < kPT; ++k) {
+        const int o = o0 + k;
+        if (o >= nu) break;
+        const int u = static_cast<int>(keys[o] & 0xFFFFFFFFu);
+        const int tiles = u_tiles[u], sc = u_sc[u];
+        const int base = tiles / sc, rem = tiles % sc;
+        u_first[u] = static_cast<int>(pre);
+        int t0 = 0;
+        for (int q = 0; q < sc; ++q) {
+          const int x = static_cast<int>(pre) + q, nt = base + (q < rem ? 1 : 0);
+          p_unit[x] = u;
+          p_t0[x] = t0;
+          p_nt[x] = nt;
+          p_cta[x] = 2 * nt + 5 + (sc > 1 ? 3 : 0);  // cost in half-tiles, replaced by the placement
+          t0 += nt;
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const long long b2 = __shfl_xor_sync(0xFFFFFFFFu, best, off);
-          const int c2 = __shfl_xor_sync(0xFFFFFFFFu, bc, off);
-          if (b2 < best || (b2 == best && c2 < bc)) {
-            best = b2;
-            bc = c2;
-          }
-        }
-        if ((bc & 31) == lane) load[bc >> 5] += 2LL * nt + 5 + (sc > 1 ? 3 : 0);
-        if (lane == 0 && np < kMaxUnits) {
-          p_unit[np] = u;
-          p_t0[np] = t0;
-          p_nt[np] = nt;
-          p_cta[np] = bc;
-        }
-        t0 += nt;
+        pre += static_cast<unsigned>(sc);
       }
     }
-    if (lane == 0) n_pieces_s = np;
   }
   __syncthreads();
   const int npc = n_pieces_s;
@@ -598,46 +622,110 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     if (tid == 0) counts[3] = OPTIMUS_EINVAL;
     return;
   }
-  // 4. split groups and partial slots, in unit order
-  if (tid == 0) {
-    int ng = 0, npart = 0;
-    for (int u = 0; u < nu; ++u) {
-      const int sc = u_sc[u];
-      const int f = u_first[u];
-      if (sc > 1) {
-        if (ng >= max_groups) {
-          bad = 1;
-          break;
+  // 3c. LPT placement by warp 0.  CTA loads live in registers (lane l holds CTAs
+  // l, l + 32, ...; static indexing only, so nothing spills to local memory); the
+  // argmin is two warp reductions (min load, then min CTA among the lanes holding it:
+  // the host heap's tie order).  p_cta[x] becomes cta | rank-in-CTA << 10.
+  if (warp == 0) {
+    unsigned load[KPER];
+    int cnt[KPER];  // pieces booked per CTA
+#pragma unroll
+    for (int i = 0; i < KPER; ++i) {
+      load[i] = lane + 32 * i < grid ? 0u : 0xFFFFFFFFu;
+      cnt[i] = 0;
+    }
+#pragma unroll 4
+    for (int x = 0; x < npc; ++x) {
+      const unsigned cost = static_cast<unsigned>(p_cta[x]);
+      unsigned best = 0xFFFFFFFFu;
+      int bi = 0;
+#pragma unroll
+      for (int i = 0; i < KPER; ++i)
+        if (load[i] < best) {  // increasing CTA per lane: first minimum
+          best = load[i];
+          bi = i;
         }
-        int32_t* g = groups + 8 * ng++;
-        g[0] = u_req[u];
-        g[1] = u_head[u];
-        g[2] = u_tok[u];
-        g[3] = u_ntok[u];
-        g[4] = npart;
-        g[5] = sc;
-        g[6] = 0;
-        g[7] = 0;
-        for (int k = 0; k < sc; ++k) p_slot[f + k] = npart++;
+      const unsigned m = __reduce_min_sync(0xFFFFFFFFu, best);
+      const int bc = static_cast<int>(
+          __reduce_min_sync(0xFFFFFFFFu, best == m ? static_cast<unsigned>(lane + 32 * bi) : 0xFFFFFFFFu));
+      const int sel = (bc & 31) == lane ? (bc >> 5) : -1;  // the owning lane books the piece
+      int rank = 0;
+#pragma unroll
+      for (int i = 0; i < KPER; ++i) {  // selects, not an indexed store: the arrays stay in registers
+        const bool hit = i == sel;
+        rank = hit ? cnt[i] : rank;
+        load[i] += hit ? cost : 0u;
+        cnt[i] += hit ? 1 : 0;
+      }
+      if (sel >= 0) p_cta[x] = bc | (rank << 10);
+    }
+    __syncwarp();
+    int* cc = reinterpret_cast<int*>(keys);  // per-CTA piece counts (the keys are dead)
+#pragma unroll
+    for (int i = 0; i < KPER; ++i)
+      if (lane + 32 * i < grid) cc[lane + 32 * i] = cnt[i];
+  }
+  __syncthreads();
+  int* cta_cnt = reinterpret_cast<int*>(keys);  // the sort keys are dead now (written by warp 0 above)
+  // 4. split groups and partial slots, in unit order: one block scan of
+  // (cut units << 16 | their pieces) over 4 consecutive units per thread
+  {
+    constexpr int kPerThread = kMaxUnits / kPlanThreads;
+    const int u0 = tid * kPerThread;
+    unsigned v = 0;
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k)
+      if (u0 + k < nu && u_sc[u0 + k] > 1) v += (1u << 16) | static_cast<unsigned>(u_sc[u0 + k]);
+    unsigned total;
+    unsigned pre = block_exclusive_scan(v, scan_ws, &total);
+#pragma unroll
+    for (int k = 0; k < kPerThread; ++k) {
+      const int u = u0 + k;
+      if (u >= nu) break;
+      const int sc = u_sc[u], f = u_first[u];
+      if (sc > 1) {
+        const int gi = static_cast<int>(pre >> 16), part = static_cast<int>(pre & 0xFFFFu);
+        if (gi < max_groups) {
+          int32_t* g = groups + 8 * gi;
+          g[0] = u_req[u];
+          g[1] = u_head[u];
+          g[2] = u_tok[u];
+          g[3] = u_ntok[u];
+          g[4] = part;
+          g[5] = sc;
+          g[6] = 0;
+          g[7] = 0;
+        }
+        for (int q = 0; q < sc; ++q) p_slot[f + q] = part + q;
+        pre += (1u << 16) | static_cast<unsigned>(sc);
       } else {
         p_slot[f] = -1;
       }
     }
-    counts[0] = npc;
-    counts[1] = ng;
-    counts[2] = npart;
-    counts[3] = bad ? OPTIMUS_EINVAL : 0;
+    if (tid == 0) {
+      const int ng = static_cast<int>(total >> 16);
+      counts[0] = npc;
+      counts[1] = ng;
+      counts[2] = static_cast<int>(total & 0xFFFFu);
+      counts[3] = ng > max_groups ? OPTIMUS_EINVAL : 0;
+    }
   }
-  __syncthreads();
-  // 5. work list in CTA order (each CTA's pieces in placement order)
-  for (int c = tid; c < grid; c += kPlanThreads) {
-    int k = 0;
-    for (int x = 0; x < npc; ++x) k += p_cta[x] < c;
-    cta_off[c] = k;
-    for (int x = 0; x < npc; ++x) {
-      if (p_cta[x] != c) continue;
+  // 5. work list in CTA order (each CTA's pieces in placement order): scan of the
+  // per-CTA counts, then every piece written at cta_off[cta] + rank
+  {
+    unsigned total;
+    const unsigned pre =
+        block_exclusive_scan(tid < grid ? static_cast<unsigned>(cta_cnt[tid]) : 0u, scan_ws, &total);
+    if (tid < grid) {
+      cta_off[tid] = static_cast<int>(pre);
+      cta_cnt[tid] = static_cast<int>(pre);
+    }
+    if (tid == 0) cta_off[grid] = npc;
+    __syncthreads();
+    for (int x = tid; x < npc; x += kPlanThreads) {
+      const int c = p_cta[x] & 1023, rank = p_cta[x] >> 10;
       const int u = p_unit[x];
-      int32_t* w = work + 8 * k++;
+      int32_t* w = work + 8 * (cta_cnt[c] + rank);
       w[0] = u_req[u];
       w[1] = u_head[u];
       w[2] = u_tok[u];
@@ -648,7 +736,6 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
       w[7] = 0;
     }
   }
-  if (tid == 0) cta_off[grid] = npc;
 }
 
 }  // namespace dstep
@@ -666,10 +753,12 @@ extern "C" int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, co
   const size_t smem = kMaxUnits * (8 + 12 * 4);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(work_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(work_plan_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(work_plan_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
-  work_plan_kernel<<<1, kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+  auto kern = grid <= 256 ? work_plan_kernel<8> : work_plan_kernel<32>;
+  kern<<<1, kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       n_req, cu_seqlens, key_end, hkv, 128 / G, grid, hard_cap, allow_cut, work, max_work, cta_off, groups, max_groups,
       counts);
   return static_cast<int>(cudaGetLastError());

@@ -31,33 +31,56 @@ def setup():
     return reqs, dec
 
 
-N = 60
-reqs, dec = setup()
-for _ in range(3):
-    dec.step([r for r in reqs if not r.finished], 32)
-torch.cuda.synchronize()
-t = time.perf_counter()
-c = 0
-for _ in range(N):
-    c += sum(len(s.commits) for s in dec.step([r for r in reqs if not r.finished], 32))
-torch.cuda.synchronize()
-el = time.perf_counter() - t
-print(f"host native step : {c / el:9.0f} tok/s  {el / N * 1e3:.3f} ms/step")
-reqs, dec = setup()
-loop = DeviceLoop(dec, reqs, 32)
-for _ in range(3):
-    loop.step()
-torch.cuda.synchronize()
-t = time.perf_counter()
-c = 0
-for _ in range(N):
-    c += sum(len(s.commits) for s in loop.step())
-torch.cuda.synchronize()
-el = time.perf_counter() - t
-print(f"device loop graph: {c / el:9.0f} tok/s  {el / N * 1e3:.3f} ms/step, replay+sync {loop.t_device / (N + 3) * 1e3:.3f} ms")
-loop.t_device = 0.0
-t0 = time.perf_counter()
-for _ in range(20):
-    loop.step()
-el = time.perf_counter() - t0
-print(f"full step {el / 20 * 1e3:.3f} ms, of which replay+sync {loop.t_device / 20 * 1e3:.3f} ms")
+def profile_loop(steps=2):
+    """The device loop's kernels for `steps` graph replays, bracketed by the CUDA
+    profiler API (ncu --profile-from-start off)."""
+    reqs, dec = setup()
+    loop = DeviceLoop(dec, reqs, 32)
+    for _ in range(3):
+        loop.step()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    for _ in range(steps):
+        loop.step()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+
+
+def main():
+    N = 60
+    reqs, dec = setup()
+    for _ in range(3):
+        dec.step([r for r in reqs if not r.finished], 32)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    c = 0
+    for _ in range(N):
+        c += sum(len(s.commits) for s in dec.step([r for r in reqs if not r.finished], 32))
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t
+    print(f"host native step : {c / el:9.0f} tok/s  {el / N * 1e3:.3f} ms/step")
+    reqs, dec = setup()
+    loop = DeviceLoop(dec, reqs, 32)
+    for _ in range(3):
+        loop.step()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    c = 0
+    for _ in range(N):
+        c += sum(len(s.commits) for s in loop.step())
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t
+    print(f"device loop graph: {c / el:9.0f} tok/s  {el / N * 1e3:.3f} ms/step, replay+sync {loop.t_device / (N + 3) * 1e3:.3f} ms")
+    loop.t_device = 0.0
+    t0 = time.perf_counter()
+    for _ in range(20):
+        loop.step()
+    el = time.perf_counter() - t0
+    print(f"full step {el / 20 * 1e3:.3f} ms, of which replay+sync {loop.t_device / 20 * 1e3:.3f} ms")
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "profile":
+        profile_loop()
+    else:
+        main()
