@@ -672,25 +672,42 @@ def run_device_loop(args, dec, world):
     from paper_2605_24832_b200.errors import ConfigError
     if world != 1 or workload_spec(args.workload)["mixed"] or args.workload == "tp30b":
         return None
+    long_ctx = args.workload in ("longbench", "ctx4096")
     reqs = workload_requests(args, seed_offset=3)
+    spare = workload_requests(args, seed_offset=4, n=16 if long_ctx else None)
     try:
         loop = DeviceLoop(dec, reqs, args.chunk)
     except (ConfigError, RuntimeError) as e:
         dec.release_all(reqs)
         return {"unavailable": str(e)[:200]}
     n_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 20)
+    h2d = 0
+
+    def one():
+        nonlocal h2d
+        c = loop.step(summaries=False)
+        for i in sorted(loop.free):  # continuous batching: refill finished positions
+            if not spare:
+                break
+            loop.replace(i, spare.pop())
+            h2d += sum(loop.D[k][0].numel() * loop.D[k].element_size() for k in loop.state_keys) + \
+                loop.Dt.shape[1] * 4
+        return c
+
     for _ in range(3):
-        loop.step()
+        one()
     torch.cuda.synchronize()
+    h2d = 0
     t0 = time.perf_counter()
     commits = 0
     for _ in range(n_steps):
-        commits += loop.step(summaries=False)
+        commits += one()
     el = time.perf_counter() - t0
     d2h = sum(t.numel() * t.element_size() for t in loop.H.values())
-    dec.release_all(reqs)
+    dec.release_all([r for r in loop.requests if not r.finished])
     return {"value": commits / el, "unit": "tokens/s", "steps": n_steps, "ms_per_step": el / n_steps * 1e3,
-            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h, "batch": "fixed (finished requests idle)",
+            "h2d_bytes_per_step": h2d // n_steps, "d2h_bytes_per_step": d2h,
+            "batch": "closed loop: finished positions refilled from a spare pool (DeviceLoop.replace)",
             "path": "DeviceLoop.step (one graph: device plan -> work plan -> L x (K1,K2,combine) -> K3 -> "
                     "device apply; D2H plan + mask -> host apply)"}
 

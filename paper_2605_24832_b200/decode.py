@@ -130,10 +130,11 @@ class StreamingDecoder:
         self._native = None
 
     # ------------------------------------------------------------------ admission
-    def admit(self, request) -> int:
-        """Give a request a batch slot and pages for its prompt + first block."""
+    def admit(self, request, slot=None) -> int:
+        """Give a request a batch slot (`slot` if given) and pages for its prompt +
+        first block."""
         first = min(request.output_tokens, self.cfg.block_size)
-        return self.tables.admit(request.id, request.prompt_tokens + first)
+        return self.tables.admit(request.id, request.prompt_tokens + first, slot)
 
     def release(self, request) -> None:
         if self._native is not None and getattr(request, "_bs", None) is self._native.bs:

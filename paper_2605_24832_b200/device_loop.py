@@ -72,8 +72,7 @@ class DeviceLoop:
         self.grid = decoder.grid
         # units + the cut pieces (a balanced cut adds < 2 pieces per CTA) + page-cap cuts
         units = n * cfg.num_kv_heads * ((self.chunk + T - 1) // T)
-        cap_cuts = units * (-(-max(r.prompt_tokens + r.output_tokens for r in self.requests)
-                               // (255 * cfg.page_size)) - 1)
+        cap_cuts = units * (-(-max_pages // 255) - 1)  # any admitted request fits max_pages
         self.max_work = min(4096, units + 2 * self.grid + 64 + cap_cuts)
         M["work"] = torch.zeros((self.max_work, 8), dtype=torch.int32, device=dev)
         M["cta_off"] = z(self.grid + 1)
@@ -95,6 +94,7 @@ class DeviceLoop:
         self.H["mask"] = torch.zeros(max(cr, 1), dtype=torch.uint8, pin_memory=True)
         self.graph = None
         self.t_device = 0.0  # host seconds spent in replay + sync (diagnostics)
+        self.free = set()  # loop indices whose request finished and was released
 
     # ------------------------------------------------------------------ device
     def _enqueue(self, stream) -> None:
@@ -206,6 +206,10 @@ class DeviceLoop:
             bp["queue"], bs.qcap, bp["q_head"], bp["q_len"], bp["block_index"], bp["committed"],
             bp["steps_taken"], bp["cached_prefix"], bp["out_len"], commits.ctypes.data)
         _lib.check(st, "optimus_host_apply")
+        for i, r in enumerate(self.requests):  # finished: release pages and slot (it plans nothing)
+            if i not in self.free and r.finished:
+                self.nat.release(r)
+                self.free.add(i)
         if not summaries:
             return int(commits.sum())
         out = []
@@ -214,6 +218,24 @@ class DeviceLoop:
             out.append(StepSummary(computed=int(cu[r + 1] - cu[r]),
                                    commits=frozenset(row_pos[a:b][mask[a:b].astype(bool)].tolist())))
         return out
+
+    def replace(self, i: int, request) -> None:
+        """Continuous batching: admit `request` into loop position i, whose request
+        finished (released by step()).  The new request's batch-state row and
+        block-table row are copied into the device state the graph reads; the graph
+        itself is unchanged (it reads the slot map and the state by pointer)."""
+        if i not in self.free:
+            raise ConfigError(f"DeviceLoop.replace: position {i} still holds a live request")
+        # the position keeps its batch slot: another free position's slot map still
+        # points at its own (finished, idle) slot
+        s = self.nat._slot(request, int(self.slots_h[i]))
+        self.dec.tables.ensure(s, request.prompt_tokens + request.output_tokens)
+        bs = self.bs
+        for k in self.state_keys:
+            self.D[k][s : s + 1].copy_(torch.from_numpy(np.ascontiguousarray(getattr(bs, k)[s : s + 1])))
+        self.Dt[s].copy_(torch.from_numpy(self.dec.tables.table[s]))
+        self.requests[i] = request
+        self.free.discard(i)
 
     def finished(self) -> bool:
         return all(r.finished for r in self.requests)

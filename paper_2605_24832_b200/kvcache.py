@@ -70,12 +70,20 @@ class BlockTables:
     def slot(self, request_id: int) -> Optional[int]:
         return self._slot_of.get(request_id)
 
-    def admit(self, request_id: int, n_positions: int) -> int:
+    def admit(self, request_id: int, n_positions: int, slot: Optional[int] = None) -> int:
+        """Give a request a batch slot (the most recently freed one, or `slot` if
+        given and free) and pages for n_positions."""
         if request_id in self._slot_of:
             raise ConfigError(f"request {request_id} already admitted")
         if not self._free_slots:
             raise ConfigError("no free batch slot")
-        s = self._free_slots.pop()
+        if slot is not None:
+            if slot not in self._free_slots:
+                raise ConfigError(f"batch slot {slot} is not free")
+            self._free_slots.remove(slot)
+            s = slot
+        else:
+            s = self._free_slots.pop()
         self._slot_of[request_id] = s
         self.n_pages[s] = 0
         self.ensure(s, n_positions)

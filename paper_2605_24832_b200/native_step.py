@@ -126,11 +126,11 @@ class NativeStepper:
         return v
 
     # ------------------------------------------------------------------ admission
-    def _slot(self, req) -> int:
+    def _slot(self, req, slot=None) -> int:
         tables = self.dec.tables
         s = tables.slot(req.id)
         if s is None:
-            s = self.dec.admit(req)
+            s = self.dec.admit(req, slot)
         if self.bs._req.get(s) is not req:  # admitted elsewhere (e.g. prefill): bind now
             self.bs.bind(req, s)
         return s
