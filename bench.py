@@ -676,7 +676,7 @@ def run_device_loop(args, dec, world):
     reqs = workload_requests(args, seed_offset=3)
     spare = workload_requests(args, seed_offset=4, n=16 if long_ctx else None)
     try:
-        loop = DeviceLoop(dec, reqs, args.chunk)
+        loop = DeviceLoop(dec, reqs, args.chunk, lookahead=True)
     except (ConfigError, RuntimeError) as e:
         dec.release_all(reqs)
         return {"unavailable": str(e)[:200]}
@@ -703,13 +703,14 @@ def run_device_loop(args, dec, world):
     for _ in range(n_steps):
         commits += one()
     el = time.perf_counter() - t0
+    loop.drain()
     d2h = sum(t.numel() * t.element_size() for t in loop.H.values())
     dec.release_all([r for r in loop.requests if not r.finished])
     return {"value": commits / el, "unit": "tokens/s", "steps": n_steps, "ms_per_step": el / n_steps * 1e3,
             "h2d_bytes_per_step": h2d // n_steps, "d2h_bytes_per_step": d2h,
             "batch": "closed loop: finished positions refilled from a spare pool (DeviceLoop.replace)",
-            "path": "DeviceLoop.step (one graph: device plan -> work plan -> L x (K1,K2,combine) -> K3 -> "
-                    "device apply; D2H plan + mask -> host apply)"}
+            "path": "DeviceLoop.step, lookahead (one graph: device plan -> work plan -> L x (K1,K2,combine) -> "
+                    "K3 -> device apply; D2H plan + mask; the next graph runs during the host apply)"}
 
 
 if __name__ == "__main__":

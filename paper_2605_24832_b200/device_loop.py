@@ -32,7 +32,7 @@ from .errors import ConfigError
 
 
 class DeviceLoop:
-    def __init__(self, decoder, requests, chunk: int):
+    def __init__(self, decoder, requests, chunk: int, lookahead: bool = False):
         cfg = decoder.cfg
         if not getattr(decoder.forward, "resident_layers", False) or not hasattr(decoder.forward, "row_src_host"):
             raise ConfigError("DeviceLoop needs a forward with resident per-layer activations and a slot-indexed "
@@ -95,6 +95,9 @@ class DeviceLoop:
         self.graph = None
         self.t_device = 0.0  # host seconds spent in replay + sync (diagnostics)
         self.free = set()  # loop indices whose request finished and was released
+        self.lookahead = bool(lookahead)
+        self._inflight = False  # a lookahead iteration was launched and not yet consumed
+        self._stale = set()  # positions refilled while an iteration was in flight
 
     # ------------------------------------------------------------------ device
     def _enqueue(self, stream) -> None:
@@ -177,11 +180,17 @@ class DeviceLoop:
     # ------------------------------------------------------------------ host
     def step(self, summaries: bool = True):
         """One iteration: replay the graph, then replay the same transitions on the
-        host mirror (Request objects) from the copied plan and commit mask."""
+        host mirror (Request objects) from the copied plan and commit mask.
+
+        With ``lookahead`` the next iteration's graph is launched before the host
+        apply of this one (the device state is already advanced), so the host work
+        overlaps the GPU; a request admitted by ``replace`` then enters one
+        iteration later (the in-flight iteration planned nothing for its position)."""
         if self.graph is None:
             self.capture()
         t0 = time.perf_counter()
-        self.graph.replay()
+        if not self._inflight:
+            self.graph.replay()
         torch.cuda.current_stream().synchronize()
         self.t_device += time.perf_counter() - t0
         H = self.H
@@ -191,17 +200,30 @@ class DeviceLoop:
             raise ConfigError("device plan rejected the step (capacity or chunk bounds)")
         if int(H["wcounts"][3]) != 0:
             raise ConfigError("device attention planner rejected the step (work / group capacity)")
-        cu = H["cu_seqlens"].numpy()[: n + 1]
-        cur = H["cu_rows"].numpy()[: n + 1]
-        tok_pos = np.ascontiguousarray(H["tok_pos"].numpy()[: max(n_tok, 1)])
-        row_pos = np.ascontiguousarray(H["row_pos"].numpy()[: max(n_rows, 1)])
-        mask = np.ascontiguousarray(H["mask"].numpy()[: max(n_rows, 1)])
-        cu_c, cur_c = np.ascontiguousarray(cu), np.ascontiguousarray(cur)
-        commits = np.zeros(n, dtype=np.int32)
+        cu = H["cu_seqlens"].numpy()[: n + 1].copy()
+        cur = H["cu_rows"].numpy()[: n + 1].copy()
+        tok_pos = H["tok_pos"].numpy()[: max(n_tok, 1)].copy()
+        row_pos = H["row_pos"].numpy()[: max(n_rows, 1)].copy()
+        mask = H["mask"].numpy()[: max(n_rows, 1)].copy()
+        stale, self._stale = sorted(self._stale), set()
+        self._inflight = self.lookahead
+        if self.lookahead:
+            self.graph.replay()  # the next iteration runs while the host applies this one
+        # positions refilled after this iteration was launched: it planned nothing for
+        # them (their previous request had finished); drop them from the host replay
+        for i in stale:
+            if cu[i] != cu[i + 1] or cur[i] != cur[i + 1]:
+                raise ConfigError("DeviceLoop: a refilled position was planned by the in-flight iteration")
+        keep = np.setdiff1d(np.arange(n), stale) if stale else None
+        slots_c = np.ascontiguousarray(self.slots_h[keep] if stale else self.slots_h)
+        cu_c = np.ascontiguousarray(np.delete(cu, stale) if stale else cu)
+        cur_c = np.ascontiguousarray(np.delete(cur, stale) if stale else cur)
+        m = len(slots_c)
+        commits = np.zeros(m, dtype=np.int32)
         bs = self.bs
         bp = self.nat._bsp
         st = self.nat.lib.optimus_host_apply(
-            n, self.slots_h.ctypes.data, self.cfg.block_size, cu_c.ctypes.data, tok_pos.ctypes.data,
+            m, slots_c.ctypes.data, self.cfg.block_size, cu_c.ctypes.data, tok_pos.ctypes.data,
             cur_c.ctypes.data, row_pos.ctypes.data, mask.ctypes.data, bp["states"], bs.states.shape[1],
             bp["queue"], bs.qcap, bp["q_head"], bp["q_len"], bp["block_index"], bp["committed"],
             bp["steps_taken"], bp["cached_prefix"], bp["out_len"], commits.ctypes.data)
@@ -219,6 +241,13 @@ class DeviceLoop:
                                    commits=frozenset(row_pos[a:b][mask[a:b].astype(bool)].tolist())))
         return out
 
+    def drain(self) -> None:
+        """Wait for an in-flight lookahead iteration and discard it (its effects on
+        the device state are kept: call only when every request has finished)."""
+        if self._inflight:
+            torch.cuda.current_stream().synchronize()
+            self._inflight = False
+
     def replace(self, i: int, request) -> None:
         """Continuous batching: admit `request` into loop position i, whose request
         finished (released by step()).  The new request's batch-state row and
@@ -231,11 +260,16 @@ class DeviceLoop:
         s = self.nat._slot(request, int(self.slots_h[i]))
         self.dec.tables.ensure(s, request.prompt_tokens + request.output_tokens)
         bs = self.bs
+        # pinned staging + async copies, stream-ordered after any in-flight iteration
+        # (the host caching allocator keeps each staging buffer until its copy ran)
         for k in self.state_keys:
-            self.D[k][s : s + 1].copy_(torch.from_numpy(np.ascontiguousarray(getattr(bs, k)[s : s + 1])))
-        self.Dt[s].copy_(torch.from_numpy(self.dec.tables.table[s]))
+            src = torch.from_numpy(np.ascontiguousarray(getattr(bs, k)[s : s + 1])).pin_memory()
+            self.D[k][s : s + 1].copy_(src, non_blocking=True)
+        self.Dt[s].copy_(torch.from_numpy(self.dec.tables.table[s].copy()).pin_memory(), non_blocking=True)
         self.requests[i] = request
         self.free.discard(i)
+        if self._inflight:
+            self._stale.add(i)
 
     def finished(self) -> bool:
         return all(r.finished for r in self.requests)

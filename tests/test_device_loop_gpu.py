@@ -67,10 +67,13 @@ def test_device_loop_matches_host_native_step(batch, chunk):
         assert np.array_equal(loop.D[k].cpu().numpy(), getattr(loop.bs, k)), k
 
 
-def test_device_loop_continuous_batching_matches_host():
+@pytest.mark.parametrize("lookahead", [False, True])
+def test_device_loop_continuous_batching_matches_host(lookahead):
     """DeviceLoop.replace admits a new request into a finished position (same batch
     slot, state and block-table rows copied into the captured graph's inputs); the
-    closed loop matches the host native step run with the same admissions."""
+    closed loop matches the host native step run with the same admissions.  With
+    lookahead the next iteration is already in flight when the host applies one, so
+    an admission takes effect one iteration later: the host run admits with that lag."""
     batch, chunk = 10, 16
     reqs_h, dec_h = _setup(4, batch, chunk)
     reqs_d, dec_d = _setup(4, batch, chunk)
@@ -85,36 +88,47 @@ def test_device_loop_continuous_batching_matches_host():
 
     spare_h, spare_d = spares(), spares()
     assert len(spare_h) >= 3
-    loop = DeviceLoop(dec_d, reqs_d, chunk)
+    loop = DeviceLoop(dec_d, reqs_d, chunk, lookahead=lookahead)
     pos_h = {r.id: i for i, r in enumerate(reqs_h)}  # host: loop position of each live request
     for i, r in enumerate(reqs_h):  # the host batch takes the device loop's slots (logit rows follow slots)
         dec_h.native()._slot(r, int(loop.slots_h[i]))
     live_h = list(reqs_h)
+    lagged = []  # host admissions waiting one iteration (lookahead)
     steps = admitted = 0
-    while live_h or not loop.finished():
+    while live_h or lagged or not loop.finished():
         sh = dec_h.step(live_h, chunk) if live_h else []
         sd = loop.step()
         by_id = {r.id: s for r, s in zip(live_h, sh)}
         for r, s in zip(loop.requests, sd):
             if r.id in by_id:
                 assert set(s.commits) == set(by_id[r.id].commits), (steps, r.id)
+                assert s.computed == by_id[r.id].computed, (steps, r.id)
+            else:
+                assert s.computed == 0 and not s.commits, (steps, r.id)
         for a in live_h:
             b = loop.requests[pos_h[a.id]]
             assert a.id == b.id and np.array_equal(a.states, b.states), (steps, a.id)
             assert (a.block_index, a.committed, a.steps_taken) == (b.block_index, b.committed, b.steps_taken)
-        # admissions: every finished position takes the next spare, in position order
         done = sorted(pos_h[r.id] for r in live_h if r.finished)
         live_h = [r for r in live_h if not r.finished]
-        assert sorted(loop.free) == sorted(set(loop.free)) and set(done) <= loop.free
-        for i in done:
+        for i, nh in lagged:
+            dec_h.native()._slot(nh, int(loop.slots_h[i]))
+            live_h.append(nh)
+        lagged = []
+        assert set(done) <= loop.free
+        for i in done:  # every finished position takes the next spare, in position order
             if not spare_h:
                 break
             nh, nd = spare_h.pop(0), spare_d.pop(0)
-            dec_h.native()._slot(nh, int(loop.slots_h[i]))
             pos_h[nh.id] = i
-            live_h.append(nh)
             loop.replace(i, nd)
+            if lookahead:
+                lagged.append((i, nh))
+            else:
+                dec_h.native()._slot(nh, int(loop.slots_h[i]))
+                live_h.append(nh)
             admitted += 1
         steps += 1
         assert steps < 5000
+    loop.drain()
     assert admitted >= 3
