@@ -166,3 +166,73 @@ def test_device_work_planner_matches_host_whole_unit_plan(hq, hkv, page, maxq, k
         assert np.array_equal(off.cpu().numpy(), plan.cta_off_host)
         assert np.array_equal(work.cpu().numpy()[: c[0]], plan.work_host)
         assert np.array_equal(groups.cpu().numpy()[: c[1]], plan.groups_host)
+
+
+@pytest.mark.parametrize("hq,hkv,page,maxq,ke_hi", [(32, 8, 64, 33, 3000), (32, 8, 16, 33, 9000), (64, 8, 16, 33, 800),
+                                                    (16, 4, 64, 33, 600), (4, 4, 8, 9, 40000)])
+def test_device_work_planner_cut_mode_invariants(hq, hkv, page, maxq, ke_hi):
+    """allow_cut = 1: every unit's pieces tile [0, key_end) in key order with
+    consecutive partial slots iff cut, groups describe exactly the cut units, the work
+    list is in CTA order, and the planned makespan (half-tile costs) never exceeds the
+    whole-unit plan's by more than the cut overhead, while a dominant long unit is cut."""
+    rng = np.random.default_rng(hq * 7 + page + maxq)
+    L = _lib.load()
+    G = hq // hkv
+    T = 128 // G
+    for it in range(5):
+        n = int(rng.integers(1, 65))
+        counts = rng.integers(0, maxq, n)
+        counts[0] = max(int(counts[0]), 1)
+        cu = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+        ke = rng.integers(1, ke_hi, n).astype(np.int32)
+        if it == 0:
+            ke[0] = ke_hi * 4  # one dominant request
+        grid = 148
+        res = {}
+        for cut in (0, 1):
+            mw, mg = 4096, 1024
+            work = torch.zeros((mw, 8), dtype=torch.int32, device="cuda")
+            off = torch.zeros(grid + 1, dtype=torch.int32, device="cuda")
+            groups = torch.zeros((mg, 8), dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(4, dtype=torch.int32, device="cuda")
+            dcu, dke = _dev(cu), _dev(ke)
+            st = L.optimus_device_attn_plan(n, _p(dcu), _p(dke), hq, hkv, grid, page, cut, _p(work), mw, _p(off),
+                                            _p(groups), mg, _p(cnt), torch.cuda.current_stream().cuda_stream)
+            assert st == 0
+            torch.cuda.synchronize()
+            c = cnt.cpu().tolist()
+            assert c[3] == 0
+            res[cut] = (c, work.cpu().numpy()[: c[0]], off.cpu().numpy(), groups.cpu().numpy()[: c[1]])
+        c, w, o, g = res[1]
+        assert o[0] == 0 and o[-1] == c[0] and np.all(np.diff(o) >= 0)
+        units = {}
+        for x, r in enumerate(w):
+            cta = int(np.searchsorted(o, x, side="right") - 1)
+            units.setdefault((int(r[0]), int(r[1]), int(r[2])), []).append((int(r[4]), int(r[5]), int(r[6]), cta))
+        n_units = sum(hkv * ((int(q) + T - 1) // T) for q in counts if q > 0)
+        assert len(units) == n_units
+        cut_units = 0
+        loads = np.zeros(grid)
+        for (req, head, tok), pcs in units.items():
+            pcs.sort()
+            assert pcs[0][0] == 0 and pcs[-1][1] == ke[req]
+            assert all(pcs[i][1] == pcs[i + 1][0] for i in range(len(pcs) - 1))
+            if len(pcs) > 1:
+                cut_units += 1
+                slots = [p[2] for p in pcs]
+                assert slots == list(range(slots[0], slots[0] + len(pcs)))
+            else:
+                assert pcs[0][2] == -1
+            for a, b, _, cta in pcs:
+                loads[cta] += 2 * ((b - a + 63) // 64) + 5 + (3 if len(pcs) > 1 else 0)
+        assert cut_units == c[1] and sum(int(x[5]) for x in g) == c[2]
+        # makespan vs the whole-unit plan
+        c0, w0, o0, _ = res[0]
+        loads0 = np.zeros(grid)
+        for x, r in enumerate(w0):
+            cta = int(np.searchsorted(o0, x, side="right") - 1)
+            loads0[cta] += 2 * ((r[5] - r[4] + 63) // 64) + 5 + (3 if r[6] >= 0 else 0)
+        assert loads.max() <= loads0.max() + 8
+        hard_cap = 255 * page // 64  # tiles per item (the page cap cuts longer units in both modes)
+        if it == 0 and (ke[0] + 63) // 64 <= hard_cap and 2 * (ke[0] + 63) // 64 > 1.2 * loads0.mean() + 40:
+            assert c[1] > 0 and loads.max() < loads0.max()
