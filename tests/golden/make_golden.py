@@ -13,6 +13,9 @@ Writes (small, committed):
   costmodel.json  seeded (x, latency) profiles and the reference's own fit of
                 each (costmodel.fit, costmodel.py:118-176), serialised with
                 CostModel.to_json (costmodel.py:69-82), plus its profile CSV.
+  trace.json    CommitTrace JSONL recorded from stochastic decodes
+                (commit.py:206-251) and ReplayOracle replays of it, strict and
+                carry-over, under other chunk sizes (commit.py:254-312).
 """
 
 from __future__ import annotations
@@ -26,7 +29,8 @@ import numpy as np
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from dllmsim.costmodel import fit as ref_fit, profile_to_csv  # noqa: E402
-from dllmsim.commit import CommitProfile, StochasticOracle, calibrate_q, commit_step  # noqa: E402
+from dllmsim.commit import (CommitProfile, CommitTrace, ReplayOracle, StochasticOracle,  # noqa: E402
+                            TraceExhausted, calibrate_q, commit_step)
 from dllmsim.core import Request, TokenState, WindowRule  # noqa: E402
 from dllmsim.engine import apply_chunk, ar_step, block_diffusion_step, plan_chunk, prefix_cached_step  # noqa: E402
 from dllmsim.workload import PROFILES, calibrated_profile  # noqa: E402
@@ -124,6 +128,49 @@ def engine_cases() -> list:
     return cases
 
 
+def trace_case(seed: int, outs, rec_chunk: int, replays, block: int = 32) -> dict:
+    """Record a CommitTrace from stochastic decodes of len(outs) requests, then
+    replay it through plan_chunk / apply_chunk with ReplayOracle."""
+    trace = CommitTrace()
+    oracle = StochasticOracle(CommitProfile(q=0.8))
+    for i, out in enumerate(outs):
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(1, i)))
+        req = Request(id=seed * 100 + i, arrival_time=0.0, prompt_tokens=5, output_tokens=out, rng=rng)
+        step = 0
+        while not req.finished:
+            plan = plan_chunk(req, rec_chunk, block, WindowRule.IN_BLOCK)
+            commits = oracle.commits(req, plan.window) if plan.window else set()
+            apply_chunk(req, plan, commits, block)
+            trace.record(req.id, step, commits)
+            step += 1
+    trace.validate({seed * 100 + i: out for i, out in enumerate(outs)})
+    jsonl = trace.to_jsonl()
+    runs = []
+    for chunk, carry in replays:
+        ro = ReplayOracle(CommitTrace.from_jsonl(jsonl), carryover=carry)
+        per_req = []
+        for i, out in enumerate(outs):
+            req = Request(id=seed * 100 + i, arrival_time=0.0, prompt_tokens=5, output_tokens=out,
+                          rng=np.random.default_rng(0))
+            steps = []
+            exhausted = False
+            while not req.finished and len(steps) < 10 * out + 50:
+                plan = plan_chunk(req, chunk, block, WindowRule.IN_BLOCK)
+                try:
+                    commits = ro.commits(req, plan.window) if plan.window else set()
+                except TraceExhausted:
+                    exhausted = True
+                    break
+                apply_chunk(req, plan, commits, block)
+                ro.consume(req, commits)
+                steps.append({"window": list(plan.window), "commits": sorted(commits)})
+            per_req.append({"steps": steps, "final_states": req.states.tolist(), "exhausted": exhausted,
+                            "finished": bool(req.finished)})
+        runs.append({"chunk": chunk, "carryover": carry, "requests": per_req})
+    return {"seed": seed, "outs": list(outs), "rec_chunk": rec_chunk, "block": block, "jsonl": jsonl,
+            "replays": runs}
+
+
 def main() -> None:
     sharegpt = calibrated_profile(PROFILES["sharegpt"], "dense-8b")
     cases = []
@@ -177,7 +224,11 @@ def main() -> None:
         fits.append({"samples": samples, "fit": json.loads(ref_fit(samples).to_json()),
                      "csv": profile_to_csv(samples)})
     (OUT / "costmodel.json").write_text(json.dumps({"fits": fits}))
-    print("wrote", OUT / "control.json", OUT / "commits.json", OUT / "costmodel.json", len(cases), "replays")
+    traces = [trace_case(7, (40, 70, 33), 32, ((32, False), (32, True), (8, True), (4, True), (8, False))),
+              trace_case(8, (97, 12), 16, ((16, False), (6, True), (32, True)))]
+    (OUT / "trace.json").write_text(json.dumps({"cases": traces}))
+    print("wrote", OUT / "control.json", OUT / "commits.json", OUT / "costmodel.json", OUT / "trace.json",
+          len(cases), "replays")
 
 
 if __name__ == "__main__":

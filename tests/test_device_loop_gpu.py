@@ -132,3 +132,48 @@ def test_device_loop_continuous_batching_matches_host(lookahead):
         assert steps < 5000
     loop.drain()
     assert admitted >= 3
+
+
+@pytest.mark.parametrize("path", ["host_step", "device_loop"])
+def test_recorded_gpu_trace_replays_exactly(path):
+    """The B200 path's commit decisions (K3 on the synthetic logits), recorded as a
+    CommitTrace in the reference's JSONL format, replay the same decode through
+    the CPU engine with the strict ReplayOracle: identical windows and commits per
+    step, identical final states."""
+    from paper_2605_24832_b200 import engine as pe
+    from paper_2605_24832_b200.core import Request
+    from paper_2605_24832_b200.trace import CommitTrace, ReplayOracle, TraceRecorder
+
+    batch, chunk = 8, 16
+    staged, dec = _setup(6, batch, chunk)
+    block = dec.cfg.block_size
+    fresh = lambda: [Request(id=r.id, arrival_time=0.0, prompt_tokens=r.prompt_tokens,
+                             output_tokens=min(r.output_tokens, 300)) for r in staged]
+    reqs = fresh()
+    rec = TraceRecorder()
+    loop = DeviceLoop(dec, reqs, chunk) if path == "device_loop" else None
+    gpu_steps = {r.id: [] for r in reqs}
+    n = 0
+    while not all(r.finished for r in reqs):
+        active = list(reqs) if loop is not None else [r for r in reqs if not r.finished]
+        rec.before(active)
+        summ = loop.step() if loop is not None else dec.step(active, chunk)
+        rec.after(active, summ)
+        for r, s in zip(active, summ):
+            if s.computed:
+                gpu_steps[r.id].append(sorted(s.commits))
+        n += 1
+        assert n < 5000
+    text = rec.trace.to_jsonl()
+    trace = CommitTrace.from_jsonl(text)
+    trace.validate({r.id: r.output_tokens for r in reqs})
+    ro = ReplayOracle(trace, carryover=False)
+    for orig, r in zip(reqs, fresh()):
+        replayed = []
+        while not r.finished:
+            plan = pe.plan_chunk(r, chunk, block, "in_block")
+            commits = ro.commits(r, list(plan.window)) if plan.window else set()
+            pe.apply_chunk(r, plan, commits, block)
+            replayed.append(sorted(commits))
+        assert replayed == gpu_steps[r.id], r.id
+        assert np.array_equal(r.states, orig.states) and r.steps_taken == orig.steps_taken
