@@ -369,7 +369,10 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
   // Cutting can only win if even a perfectly balanced cut plan (the mean CTA load)
   // plus the combine launch beats whole units by > 3% (the rule below): otherwise
   // keep candidate A and skip B.
-  const double kCombine = 7.0;
+  // ~12 tiles: measured on the tp30b batch (G = 8), where the cut plan the old 7-tile
+  // figure picked ran 30.5 us against 28.2 us whole; the other workloads keep their plans
+  double kCombine = 12.0;
+  if (const char* e = std::getenv("OPTIMUS_PLAN_KCOMBINE")) kCombine = std::atof(e);  // diagnostics
   double lb = 0;
   for (const Unit& u : units) lb += u.tiles + kItem;
   lb /= grid;
@@ -430,7 +433,7 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
   }
 
   // Prefer whole units unless cutting buys >3% of the makespan, net of the split
-  // combine launch it brings (~5 us ~ 7 tiles, measured).
+  // combine launch and partial traffic it brings (kCombine, measured).
   bool use_b = span_b + kCombine < 0.97 * span_a && static_cast<int>(pb.size()) <= max_work;
   if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE"))  // diagnostics: "whole" | "cut"
     use_b = std::strcmp(f, "cut") == 0 && static_cast<int>(pb.size()) <= max_work;

@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     const long long budget = (total + grid - 1) / grid + 5;
     const long long longest = nu > 0 ? 2LL * u_tiles[static_cast<int>(keys[0] & 0xFFFFFFFFu)] + 5 : 0;
     const int nt_max = static_cast<int>(max(4LL, (budget - 8) / 2));
-    bool cut = allow_cut && 100 * (budget + 14) < 97 * longest;
+    bool cut = allow_cut && 100 * (budget + 24) < 97 * longest;  // + the combine (12 tiles)
     for (int pass = 0; pass < 2; ++pass) {
       int pieces = 0, cut_units = 0;
       for (int u = lane; u < nu; u += 32) {

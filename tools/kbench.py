@@ -27,14 +27,16 @@ a.steps = 1
 dev = torch.device("cuda")
 reqs = bench.workload_requests(a)
 P = a.page
-cfg = DecodeConfig(num_layers=a.layers, page_size=P, max_batch=a.batch,
+spec_model = dict(bench.workload_spec(a.workload)["model"])
+spec_model["num_layers"] = a.layers
+cfg = DecodeConfig(**spec_model, page_size=P, max_batch=a.batch,
                    num_pages=bench.pages_needed(reqs, P) + 64,
                    max_pages_per_req=max((r.prompt_tokens + r.output_tokens + P - 1) // P for r in reqs) + 1)
 fwd = SyntheticForward(cfg, a.batch * a.chunk, a.batch, device=dev)
 dec = StreamingDecoder(cfg, fwd, device=dev)
 for l in range(cfg.num_layers):
     dec.cache.k[l].normal_(); dec.cache.v[l].normal_()
-plans = plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule)
+plans = plan_batch(reqs, bench.step_chunks(a, reqs), cfg.block_size, cfg.window_rule)
 dm = dec.prepare(reqs, plans)
 dec.device_step(dm)
 torch.cuda.synchronize()
