@@ -673,8 +673,10 @@ def run_device_loop(args, dec, world):
     if world != 1 or workload_spec(args.workload)["mixed"] or args.workload == "tp30b":
         return None
     long_ctx = args.workload in ("longbench", "ctx4096")
-    reqs = workload_requests(args, seed_offset=3)
-    spare = workload_requests(args, seed_offset=4, n=16 if long_ctx else None)
+    # the same batch and spare pool as run_e2e (fresh objects): the two e2e numbers
+    # decode the same requests
+    reqs = workload_requests(args, seed_offset=1)
+    spare = workload_requests(args, seed_offset=2, n=16 if long_ctx else None)
     try:
         loop = DeviceLoop(dec, reqs, args.chunk, lookahead=True)
     except (ConfigError, RuntimeError) as e:
