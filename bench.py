@@ -670,7 +670,7 @@ def run_device_loop(args, dec, world):
     import torch
     from paper_2605_24832_b200.device_loop import DeviceLoop
     from paper_2605_24832_b200.errors import ConfigError
-    if world != 1 or workload_spec(args.workload)["mixed"] or args.workload == "tp30b":
+    if world != 1 or args.workload == "tp30b":
         return None
     long_ctx = args.workload in ("longbench", "ctx4096")
     # the same batch and spare pool as run_e2e (fresh objects): the two e2e numbers
@@ -678,7 +678,7 @@ def run_device_loop(args, dec, world):
     reqs = workload_requests(args, seed_offset=1)
     spare = workload_requests(args, seed_offset=2, n=16 if long_ctx else None)
     try:
-        loop = DeviceLoop(dec, reqs, args.chunk, lookahead=True)
+        loop = DeviceLoop(dec, reqs, step_chunks(args, reqs), lookahead=True)
     except (ConfigError, RuntimeError) as e:
         dec.release_all(reqs)
         return {"unavailable": str(e)[:200]}

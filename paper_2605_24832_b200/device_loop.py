@@ -37,7 +37,14 @@ class DeviceLoop:
         if not getattr(decoder.forward, "resident_layers", False) or not hasattr(decoder.forward, "row_src_host"):
             raise ConfigError("DeviceLoop needs a forward with resident per-layer activations and a slot-indexed "
                               "logits table (SyntheticForward)")
-        self.dec, self.cfg, self.chunk = decoder, cfg, int(chunk)
+        self.dec, self.cfg = decoder, cfg
+        # one chunk for the batch, or one per loop position (mixed chunks, the elastic
+        # scheduler's per-request sizes); capacities follow the largest
+        mixed = np.ndim(chunk) > 0
+        self.chunk_h = np.asarray(chunk if mixed else [chunk] * len(requests), dtype=np.int32)
+        if len(self.chunk_h) != len(requests) or self.chunk_h.min() < 2:
+            raise ConfigError("DeviceLoop: one chunk >= 2 per request")
+        self.chunk = int(self.chunk_h.max())
         nat = decoder.native()
         self.nat = nat
         self.requests = list(requests)
@@ -58,6 +65,7 @@ class DeviceLoop:
         self.D = {k: torch.from_numpy(np.ascontiguousarray(getattr(bs, k))).to(dev) for k in self.state_keys}
         self.Dt = torch.from_numpy(np.ascontiguousarray(decoder.tables.table)).to(dev)
         self.slots = torch.from_numpy(self.slots_h).to(dev)
+        self.chunks_d = torch.from_numpy(self.chunk_h).to(dev) if mixed else None
         ct = n * self.chunk
         cr = n * min(self.chunk, cfg.block_size)
         cw = n * (bs.states.shape[1] // 32 + 4)
@@ -107,7 +115,8 @@ class DeviceLoop:
         L = _lib
         rule = 0 if rule_value(cfg.window_rule) == "in_block" else 1
         _lib.check(L.call(
-            "optimus_device_plan", n, p(self.slots), self.chunk, None, cfg.block_size, rule, p(D["states"]),
+            "optimus_device_plan", n, p(self.slots), self.chunk,
+            p(self.chunks_d) if self.chunks_d is not None else None, cfg.block_size, rule, p(D["states"]),
             D["states"].shape[1], p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]),
             p(D["cached_prefix"]), p(D["prompt"]), p(D["out_len"]), p(self.Dt), self.Dt.shape[1],
             p(M["cu_seqlens"]), p(M["tok_req"]), p(M["tok_pos"]), ct, p(M["prompt_len"]), p(M["key_end"]),

@@ -177,3 +177,32 @@ def test_recorded_gpu_trace_replays_exactly(path):
             replayed.append(sorted(commits))
         assert replayed == gpu_steps[r.id], r.id
         assert np.array_equal(r.states, orig.states) and r.steps_taken == orig.steps_taken
+
+
+def test_device_loop_mixed_chunks_matches_host():
+    """Per-position chunk sizes (the elastic scheduler's per-request chunks, BASELINE
+    configs[3]): the device plan reads them from device memory; same decode as the
+    host native step given the same per-request chunks."""
+    batch = 12
+    rng = np.random.default_rng(9)
+    chunks = [int(c) for c in rng.choice([8, 16, 24, 32], batch)]
+    reqs_h, dec_h = _setup(7, batch, 32)
+    reqs_d, dec_d = _setup(7, batch, 32)
+    loop = DeviceLoop(dec_d, reqs_d, chunks)
+    chunk_of = {r.id: c for r, c in zip(reqs_h, chunks)}
+    for i, r in enumerate(reqs_h):
+        dec_h.native()._slot(r, int(loop.slots_h[i]))
+    steps = 0
+    while not all(r.finished for r in reqs_h):
+        active = [r for r in reqs_h if not r.finished]
+        sh = dec_h.step(active, [chunk_of[r.id] for r in active])
+        sd = loop.step()
+        by_id = {r.id: s for r, s in zip(active, sh)}
+        for r, s in zip(reqs_d, sd):
+            if r.id in by_id:
+                assert set(s.commits) == set(by_id[r.id].commits), (steps, r.id)
+                assert s.computed == by_id[r.id].computed
+        for a, b in zip(reqs_h, reqs_d):
+            assert np.array_equal(a.states, b.states), (steps, a.id)
+        steps += 1
+        assert steps < 5000
