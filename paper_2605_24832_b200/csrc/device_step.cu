@@ -634,8 +634,21 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
       load[i] = lane + 32 * i < grid ? 0u : 0xFFFFFFFFu;
       cnt[i] = 0;
     }
+    // the first `grid` pieces land on CTAs 0, 1, ... in order (every load is still
+    // zero when each is placed, ties go to the lowest CTA): place them in parallel
+    const int first = min(npc, grid);
+#pragma unroll
+    for (int i = 0; i < KPER; ++i) {
+      const int c = lane + 32 * i;
+      if (c < first) {
+        load[i] = static_cast<unsigned>(p_cta[c]);
+        cnt[i] = 1;
+        p_cta[c] = c;
+      }
+    }
+    __syncwarp();
 #pragma unroll 4
-    for (int x = 0; x < npc; ++x) {
+    for (int x = first; x < npc; ++x) {
       const unsigned cost = static_cast<unsigned>(p_cta[x]);
       unsigned best = 0xFFFFFFFFu;
       int bi = 0;
