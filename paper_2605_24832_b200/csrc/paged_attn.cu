@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Split-KV combine: merge the (m, l, O) partials of every split query tile.
-// One warp per output row (grid.x = group, grid.y = 8-row slab): lane s reads the
+// One warp per output row (one block per (group, 8-row slab) pair): lane s reads the
 // (m, l) of split s, the warp reduces the merged max / denominator with shuffles,
 // then every lane accumulates a 4-column float4 slice over the splits.
 template <int HD>
@@ -809,9 +809,11 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __rest
   // device-planned steps: the group count is read from device memory and the grid,
   // sized for capacity, strides over the groups
   if (n_groups_dev != nullptr) n_groups = *n_groups_dev;
-  const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
+  constexpr int kSlabs = kBlockM / 8;  // 8-row slabs per group (one warp per row)
   const int lane = threadIdx.x & 31;
-  for (int gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+  for (int idx = blockIdx.x; idx < n_groups * kSlabs; idx += gridDim.x) {
+    const int gi = idx / kSlabs;
+    const int r = (idx - gi * kSlabs) * 8 + (threadIdx.x >> 5);
     const int* gr = groups + 8 * gi;
     const int head = gr[1], tok_begin = gr[2], n_tok = gr[3], slot0 = gr[4], n_split = gr[5];
     if (r >= n_tok * group_sz) continue;
@@ -861,13 +863,15 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const int32_t* __rest
   }
 }
 
-// Launch the combine with PDL after the attention grid; n_groups_dev != nullptr: the
-// count is on the device and the grid covers min(n_groups, 32) groups per pass.
+// Launch the combine with PDL after the attention grid: one block per (group, 8-row
+// slab).  n_groups_dev != nullptr: the count is on the device and a grid of at most
+// 128 blocks strides over the (group, slab) pairs (cheap when there are none).
 template <int HD>
 static int launch_combine_t(const AttnParams& prm, const int32_t* groups, int n_groups,
                             const int32_t* n_groups_dev, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_groups_dev ? (n_groups < 32 ? n_groups : 32) : n_groups, kBlockM / 8);
+  const int pairs = n_groups * (kBlockM / 8);
+  cfg.gridDim = dim3(n_groups_dev ? (pairs < 128 ? pairs : 128) : pairs);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = stream;
