@@ -265,6 +265,20 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
 int optimus_unmask_splits(int n_rows, int vocab);
 
 /*
+ * f3: LM-head GEMM with the unmask partials in its epilogue; the
+ * logits are never written.  hidden: bf16 [n_rows][hidden_stride] (first k_dim used),
+ * weight: bf16 [vocab][weight_stride] (the LM head, row v = token v).  Writes
+ * part[n_rows][optimus_lmhead_splits(vocab)] records in the layout of
+ * optimus_unmask_partials (max logit, sum exp(x - max), lowest argmax + vocab_offset);
+ * finish with optimus_unmask_finalize(part, 1, n_rows, optimus_lmhead_splits(vocab), ...).
+ * tcgen05 (M=128, N=256) with a 4-stage TMA ring; k_dim and strides multiples of 8.
+ */
+int optimus_lmhead_splits(int vocab);
+int optimus_lmhead_unmask_partials(const void* hidden, int64_t hidden_stride, int n_rows, const void* weight,
+                                   int64_t weight_stride, int vocab, int k_dim, int vocab_offset, float* part,
+                                   void* stream);
+
+/*
  * Device twins of optimus_host_plan / optimus_host_apply (device half):
  * the same packed per-slot state and step metadata, all pointers DEVICE pointers,
  * enqueued on `stream`, bit-identical results (tests/test_device_step_gpu.py).

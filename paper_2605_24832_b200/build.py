@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "liboptimus_b200.so"
-SOURCES = ["kv_append.cu", "paged_attn.cu", "paged_attn2.cu", "unmask.cu", "capi.cu", "host_step.cu", "device_step.cu"]
+SOURCES = ["kv_append.cu", "paged_attn.cu", "paged_attn2.cu", "unmask.cu", "capi.cu", "host_step.cu", "device_step.cu", "lmhead_unmask.cu"]
 HEADERS = ["ptx.cuh", "attn.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -33,6 +33,7 @@ int launch_unmask_partials(const void*, int, int64_t, const int32_t*, int, int, 
 int launch_unmask_finalize(const float*, int, int, int, const int32_t*, int, float, int, uint8_t*,
                            int32_t*, float*, const int32_t*, uint8_t*, int32_t*, int64_t,
                            cudaStream_t);
+int launch_lmhead_unmask(const CUtensorMap&, const CUtensorMap&, int, int, int, int, float*, cudaStream_t);
 
 }  // namespace optimus
 
@@ -248,6 +249,36 @@ int optimus_unmask_partials_dev(const void* logits, int logits_dtype, int64_t ro
                                                 vocab, vocab_offset, n_vsplit, part,
                                                 static_cast<cudaStream_t>(stream)),
                      "unmask_partials_dev");
+}
+
+// f3: LM-head GEMM with the unmask partials in its epilogue (lmhead_unmask.cu).
+int optimus_lmhead_splits(int vocab) { return vocab < 1 ? 0 : (vocab + 255) / 256; }
+
+int optimus_lmhead_unmask_partials(const void* hidden, int64_t hidden_stride, int n_rows, const void* weight,
+                                   int64_t weight_stride, int vocab, int k_dim, int vocab_offset, float* part,
+                                   void* stream) {
+  if (n_rows < 0 || vocab < 1 || k_dim < 8 || k_dim % 8) return fail("lmhead: bad sizes (k_dim % 8 == 0)");
+  if (hidden_stride < k_dim || weight_stride < k_dim || hidden_stride % 8 || weight_stride % 8)
+    return fail("lmhead: row strides must be >= k_dim and multiples of 8 elements");
+  if (!hidden || !weight || !part) return fail("lmhead: null pointer");
+  if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(weight)) & 15)
+    return fail("lmhead: hidden / weight must be 16-byte aligned");
+  if (n_rows == 0) return 0;
+  if (int st = check_device()) return st;
+  CUtensorMap th, tw;
+  const uint64_t dh[4] = {static_cast<uint64_t>(k_dim), static_cast<uint64_t>(n_rows), 1, 1};
+  const uint64_t sh[3] = {static_cast<uint64_t>(hidden_stride) * 2, static_cast<uint64_t>(hidden_stride) * 2 * n_rows,
+                          static_cast<uint64_t>(hidden_stride) * 2 * n_rows};
+  const uint32_t bh[4] = {64, 128, 1, 1};
+  if (int st = get_map(hidden, dh, sh, bh, &th)) return st;
+  const uint64_t dw[4] = {static_cast<uint64_t>(k_dim), static_cast<uint64_t>(vocab), 1, 1};
+  const uint64_t sw[3] = {static_cast<uint64_t>(weight_stride) * 2, static_cast<uint64_t>(weight_stride) * 2 * vocab,
+                          static_cast<uint64_t>(weight_stride) * 2 * vocab};
+  const uint32_t bw[4] = {64, 256, 1, 1};
+  if (int st = get_map(weight, dw, sw, bw, &tw)) return st;
+  return cuda_status(launch_lmhead_unmask(th, tw, n_rows, vocab, k_dim, vocab_offset, part,
+                                          static_cast<cudaStream_t>(stream)),
+                     "lmhead_unmask");
 }
 
 int optimus_slot_mapping(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,

@@ -375,6 +375,34 @@ def unmask_partials(
     return part
 
 
+def lmhead_unmask_partials(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    vocab_offset: int = 0,
+    part: Optional[torch.Tensor] = None,
+    stream=None,
+) -> torch.Tensor:
+    """f3: the LM head ``hidden @ weight.T`` reduced straight to the unmask partials
+    (``optimus_lmhead_unmask_partials``); the logits are never materialised.
+    Returns part ``[n_rows, optimus_lmhead_splits(vocab), 3]`` for ``unmask_finalize``."""
+    _cuda(hidden, weight, part)
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise ConfigError("lmhead: hidden and weight must be bf16")
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise ConfigError("lmhead: hidden [rows, K] and weight [vocab, K] must share K")
+    if hidden.stride(-1) != 1 or weight.stride(-1) != 1:
+        raise ConfigError("lmhead: rows must be contiguous")
+    n_rows, k = hidden.shape
+    vocab = weight.shape[0]
+    n_vt = int(_lib.call("optimus_lmhead_splits", vocab))
+    if part is None:
+        part = torch.empty((max(n_rows, 1), n_vt, 3), dtype=torch.float32, device=hidden.device)
+    st = _lib.call("optimus_lmhead_unmask_partials", _ptr(hidden), hidden.stride(0), n_rows, _ptr(weight),
+                   weight.stride(0), vocab, k, vocab_offset, _ptr(part), _stream(stream))
+    _lib.check(st, "optimus_lmhead_unmask_partials")
+    return part
+
+
 def unmask_finalize(
     part: torch.Tensor,
     n_outer: int,
