@@ -274,6 +274,10 @@ int optimus_unmask_splits(int n_rows, int vocab);
  * tcgen05 (M=128, N=256) with a 4-stage TMA ring; k_dim and strides multiples of 8.
  */
 int optimus_lmhead_splits(int vocab);
+/* Merge part[n_rows][n_split] unmask records into out[n_rows][1] (same record layout;
+ * a fixed per-row merge order), e.g. the hundreds of LM-head vocab tiles before
+ * optimus_unmask_finalize(out, 1, n_rows, 1, ...). */
+int optimus_unmask_merge_splits(const float* part, int n_rows, int n_split, float* out, void* stream);
 int optimus_lmhead_unmask_partials(const void* hidden, int64_t hidden_stride, int n_rows, const void* weight,
                                    int64_t weight_stride, int vocab, int k_dim, int vocab_offset, float* part,
                                    void* stream);

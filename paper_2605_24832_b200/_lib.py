@@ -84,6 +84,7 @@ SIGNATURES = {
     "optimus_device_attn_plan": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
                                         _vp, _vp]),
     "optimus_lmhead_splits": (_i32, [_i32]),
+    "optimus_unmask_merge_splits": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "optimus_lmhead_unmask_partials": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
     "optimus_paged_attn_combine_dev": (_i32, [_vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _vp]),
     "optimus_kv_append_dev": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _i32, _i32, _i32, _vp,

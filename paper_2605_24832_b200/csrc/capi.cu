@@ -34,6 +34,7 @@ int launch_unmask_finalize(const float*, int, int, int, const int32_t*, int, flo
                            int32_t*, float*, const int32_t*, uint8_t*, int32_t*, int64_t,
                            cudaStream_t);
 int launch_lmhead_unmask(const CUtensorMap&, const CUtensorMap&, int, int, int, int, float*, cudaStream_t);
+int launch_merge_splits(const float*, int, int, float*, cudaStream_t);
 
 }  // namespace optimus
 
@@ -279,6 +280,14 @@ int optimus_lmhead_unmask_partials(const void* hidden, int64_t hidden_stride, in
   return cuda_status(launch_lmhead_unmask(th, tw, n_rows, vocab, k_dim, vocab_offset, part,
                                           static_cast<cudaStream_t>(stream)),
                      "lmhead_unmask");
+}
+
+int optimus_unmask_merge_splits(const float* part, int n_rows, int n_split, float* out, void* stream) {
+  if (n_rows < 0 || n_split < 1 || (n_rows > 0 && (!part || !out))) return fail("merge_splits: bad args");
+  if (n_rows == 0) return 0;
+  if (int st = check_device()) return st;
+  return cuda_status(launch_merge_splits(part, n_rows, n_split, out, static_cast<cudaStream_t>(stream)),
+                     "merge_splits");
 }
 
 int optimus_slot_mapping(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,

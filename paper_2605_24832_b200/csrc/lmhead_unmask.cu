@@ -146,6 +146,50 @@ __global__ void __launch_bounds__(128, 1) lmhead_unmask_kernel(const __grid_cons
   if (warp == 0) tmem_dealloc<kLmN>(tmem);
 }
 
+// Merge each row's n_split partials into one record (one warp per row: every lane
+// folds splits lane, lane + 32, ... in order, then a fixed xor-tree across lanes), so
+// the finalize step sees n_vsplit = 1 instead of hundreds of vocab tiles.
+__device__ __forceinline__ void lm_merge(float& m, float& s, int& idx, float m2, float s2, int i2) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  if (i2 < 0) return;
+  if (idx < 0 || m2 > m || (m2 == m && i2 < idx)) {
+    s = (idx < 0 || m == -INFINITY) ? s2 : s * fast_exp2((m - m2) * kLog2e) + s2;
+    m = m2;
+    idx = i2;
+  } else {
+    s += (m2 == -INFINITY) ? 0.f : s2 * fast_exp2((m2 - m) * kLog2e);
+  }
+}
+
+__global__ void __launch_bounds__(256) merge_splits_kernel(const LmPart* __restrict__ part, int n_rows,
+                                                           int n_split, LmPart* __restrict__ out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  float m = -INFINITY, s = 0.f;
+  int idx = -1;
+  const LmPart* pr = part + static_cast<int64_t>(row) * n_split;
+  for (int k = lane; k < n_split; k += 32) {
+    const LmPart q = pr[k];
+    lm_merge(m, s, idx, q.m, q.s, q.idx);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float m2 = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+    const float s2 = __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    const int i2 = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
+    lm_merge(m, s, idx, m2, s2, i2);
+  }
+  if (lane == 0) out[row] = LmPart{m, s, idx};
+}
+
+int launch_merge_splits(const float* part, int n_rows, int n_split, float* out, cudaStream_t stream) {
+  if (n_rows <= 0) return 0;
+  merge_splits_kernel<<<(n_rows * 32 + 255) / 256, 256, 0, stream>>>(
+      reinterpret_cast<const LmPart*>(part), n_rows, n_split, reinterpret_cast<LmPart*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
 int lmhead_unmask_smem() { return kLmSmem; }
 
 int launch_lmhead_unmask(const CUtensorMap& tm_h, const CUtensorMap& tm_w, int n_rows, int vocab, int k_dim,

@@ -381,10 +381,13 @@ def lmhead_unmask_partials(
     vocab_offset: int = 0,
     part: Optional[torch.Tensor] = None,
     stream=None,
+    merge: bool = False,
+    merged: Optional[torch.Tensor] = None,
 ) -> torch.Tensor:
     """f3: the LM head ``hidden @ weight.T`` reduced straight to the unmask partials
     (``optimus_lmhead_unmask_partials``); the logits are never materialised.
-    Returns part ``[n_rows, optimus_lmhead_splits(vocab), 3]`` for ``unmask_finalize``."""
+    Returns part ``[n_rows, optimus_lmhead_splits(vocab), 3]`` for ``unmask_finalize``,
+    or with ``merge`` the per-row merge of the vocab tiles, ``[n_rows, 1, 3]``."""
     _cuda(hidden, weight, part)
     if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
         raise ConfigError("lmhead: hidden and weight must be bf16")
@@ -400,7 +403,13 @@ def lmhead_unmask_partials(
     st = _lib.call("optimus_lmhead_unmask_partials", _ptr(hidden), hidden.stride(0), n_rows, _ptr(weight),
                    weight.stride(0), vocab, k, vocab_offset, _ptr(part), _stream(stream))
     _lib.check(st, "optimus_lmhead_unmask_partials")
-    return part
+    if not merge:
+        return part
+    if merged is None:
+        merged = torch.empty((max(n_rows, 1), 1, 3), dtype=torch.float32, device=hidden.device)
+    st = _lib.call("optimus_unmask_merge_splits", _ptr(part), n_rows, n_vt, _ptr(merged), _stream(stream))
+    _lib.check(st, "optimus_unmask_merge_splits")
+    return merged
 
 
 def unmask_finalize(

@@ -36,6 +36,12 @@ def test_lmhead_unmask_matches_fp32_reference(rows, k, vocab, scale):
     tok = res.tokens.cpu().numpy()[:rows]
     ref_tok = logits.argmax(dim=1).cpu().numpy()
     assert np.array_equal(tok[clear], ref_tok[clear])
+    # merged per row first (optimus_unmask_merge_splits): the same decisions
+    mg = ops.lmhead_unmask_partials(H, W, merge=True)
+    res2 = ops.unmask_finalize(mg, 1, rows, 1, cu_rows, 0.9)
+    torch.cuda.synchronize()
+    assert torch.equal(res2.tokens[:rows], res.tokens[:rows])
+    np.testing.assert_allclose(res2.conf.cpu().numpy()[:rows], conf, rtol=1e-5)
     # the raw partials: per-tile max equals the reference tile max
     pm = part[:, :, 0].cpu().numpy()
     lg = logits.float().cpu().numpy()
