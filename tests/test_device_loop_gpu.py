@@ -18,13 +18,13 @@ from paper_2605_24832_b200.synthetic import SyntheticForward
 pytestmark = pytest.mark.gpu
 
 
-def _setup(seed, batch, chunk, page=64, layers=2):
+def _setup(seed, batch, chunk, page=64, layers=2, rule="in_block", block=32):
     class A:
         pass
     a = A()
     a.workload, a.chunk, a.page, a.batch, a.seed, a.steps = "sharegpt", chunk, page, batch, seed, 1
     reqs = bench.workload_requests(a)
-    cfg = DecodeConfig(num_layers=layers, page_size=page, max_batch=batch,
+    cfg = DecodeConfig(num_layers=layers, page_size=page, max_batch=batch, window_rule=rule, block_size=block,
                        num_pages=bench.pages_needed(reqs, page) + 2 * batch + 64,
                        max_pages_per_req=max((r.prompt_tokens + r.output_tokens + page - 1) // page for r in reqs) + 2)
     dev = torch.device("cuda")
@@ -38,10 +38,11 @@ def _setup(seed, batch, chunk, page=64, layers=2):
     return reqs, dec
 
 
-@pytest.mark.parametrize("batch,chunk", [(12, 32), (24, 8)])
-def test_device_loop_matches_host_native_step(batch, chunk):
-    reqs_h, dec_h = _setup(3, batch, chunk)
-    reqs_d, dec_d = _setup(3, batch, chunk)
+@pytest.mark.parametrize("batch,chunk,rule,block", [(12, 32, "in_block", 32), (24, 8, "in_block", 32),
+                                                    (10, 16, "out_block", 32), (8, 8, "in_block", 16)])
+def test_device_loop_matches_host_native_step(batch, chunk, rule, block):
+    reqs_h, dec_h = _setup(3, batch, chunk, rule=rule, block=block)
+    reqs_d, dec_d = _setup(3, batch, chunk, rule=rule, block=block)
     loop = DeviceLoop(dec_d, reqs_d, chunk)
     steps = 0
     while not all(r.finished for r in reqs_h):
