@@ -412,6 +412,26 @@ def lmhead_unmask_partials(
     return merged
 
 
+def lmhead_unmask_commit(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    cu_rows: torch.Tensor,
+    tau: float = 0.9,
+    fallback: str = "earliest",
+    row_pos: Optional[torch.Tensor] = None,
+    state: Optional[torch.Tensor] = None,
+    token_buf: Optional[torch.Tensor] = None,
+    stream=None,
+) -> "UnmaskResult":
+    """K3 from hidden states (f3): fused LM head -> per-row merge -> threshold and
+    progress rule.  Same result contract as ``unmask_commit`` on the logits
+    ``hidden @ weight.T`` (computed here in fp32, never stored)."""
+    n_rows = hidden.shape[0]
+    merged = lmhead_unmask_partials(hidden, weight, merge=True, stream=stream)
+    return unmask_finalize(merged, 1, n_rows, 1, cu_rows, tau, fallback, row_pos=row_pos, state=state,
+                           token_buf=token_buf, stream=stream)
+
+
 def unmask_finalize(
     part: torch.Tensor,
     n_outer: int,

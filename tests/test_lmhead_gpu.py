@@ -70,3 +70,25 @@ def test_lmhead_vocab_offset_and_sharded_merge():
     assert torch.equal(full.tokens[:rows], sh.tokens[:rows])
     torch.testing.assert_close(full.conf[:rows], sh.conf[:rows], rtol=1e-5, atol=1e-7)
     assert torch.equal(full.commit_mask[:rows], sh.commit_mask[:rows])
+
+
+def test_lmhead_unmask_commit_equals_unmask_commit_on_fp32_logits():
+    """One-call f3 API == K3 (`unmask_commit`) on the fp32 logits of the same LM
+    head, per request (progress rule included), away from the tau boundary."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    rows, k, vocab = 260, 1024, 4096
+    H = torch.randn(rows, k, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(vocab, k, device="cuda", generator=g) * 0.08).to(torch.bfloat16)
+    H[::3] *= 4  # sharper rows: a mix of committed and uncommitted positions
+    cu = torch.tensor([0, 7, 40, 41, 120, 260], dtype=torch.int32, device="cuda")
+    a = ops.lmhead_unmask_commit(H, W, cu, 0.9)
+    logits = (H.float() @ W.float().T).contiguous()
+    b = ops.unmask_commit(logits, cu, 0.9)
+    torch.cuda.synchronize()
+    conf = b.conf.cpu().numpy()[:rows]
+    far = np.abs(conf - 0.9) > 1e-3
+    assert far.sum() > rows // 2
+    assert np.array_equal(a.commit_mask.cpu().numpy()[:rows][far], b.commit_mask.cpu().numpy()[:rows][far])
+    assert 0 < int(a.commit_mask[:rows].sum()) < rows
+    np.testing.assert_allclose(a.conf.cpu().numpy()[:rows], conf, rtol=2e-3, atol=1e-6)
