@@ -207,3 +207,25 @@ def test_device_loop_mixed_chunks_matches_host():
             assert np.array_equal(a.states, b.states), (steps, a.id)
         steps += 1
         assert steps < 5000
+
+
+def test_graph_captured_host_step_matches_eager(monkeypatch):
+    """NativeStepper.device_step_graph (the host-planned step replayed as one CUDA
+    graph, counts read on the device) == the eager step, commit for commit."""
+    batch, chunk = 12, 16
+    reqs_e, dec_e = _setup(8, batch, chunk)
+    reqs_g, dec_g = _setup(8, batch, chunk)
+    steps = 0
+    while not all(r.finished for r in reqs_e):
+        ae = [r for r in reqs_e if not r.finished]
+        ag = [r for r in reqs_g if not r.finished]
+        monkeypatch.setenv("OPTIMUS_STEP_GRAPH", "0")
+        se = dec_e.step(ae, chunk)
+        monkeypatch.setenv("OPTIMUS_STEP_GRAPH", "1")
+        sg = dec_g.step(ag, chunk)
+        assert [set(s.commits) for s in se] == [set(s.commits) for s in sg], steps
+        for a, b in zip(reqs_e, reqs_g):
+            assert np.array_equal(a.states, b.states), (steps, a.id)
+        steps += 1
+        assert steps < 5000
+    assert dec_g.native()._graphs  # the graph path ran
