@@ -13,6 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("rows,k,vocab,scale", [(300, 512, 5000, 0.06), (128, 256, 256, 0.2), (77, 4096, 2056, 0.02),
+                                                (150, 200, 1000, 0.1), (513, 1024, 40000, 0.05),
                                                 (1, 64, 700, 0.5)])
 def test_lmhead_unmask_matches_fp32_reference(rows, k, vocab, scale):
     g = torch.Generator(device="cuda")
