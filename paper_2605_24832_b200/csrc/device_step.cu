@@ -31,6 +31,34 @@ constexpr int8_t MASKED = 0, UNCACHED = 1, CACHED = 2;
 constexpr int kWarps = 32;
 constexpr int kMaxOut = 4096;          // planned bitmap capacity per warp (positions)
 constexpr int kMaxReq = 256;           // requests per step (the reference's max_batch, sim.py:62)
+
+// Exclusive prefix sum over a 1024-thread block's values (warp shuffles, then one
+// warp over the 32 warp totals); *total = the sum.  All threads must call it.
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* ws, unsigned* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= o) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  const unsigned pre = (warp ? ws[warp - 1] : 0u) + x - v;
+  *total = ws[31];
+  __syncthreads();  // ws is reused by the next call
+  return pre;
+}
 constexpr int kMaxChunk = 128;
 
 struct PlanArgs {
@@ -77,6 +105,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
   __shared__ int ntok_s[kMaxReq], nrow_s[kMaxReq], nword_s[kMaxReq], nkv_s[kMaxReq];
   __shared__ int ke_s[kMaxReq], vb_s[kMaxReq];
   __shared__ int bad;
+  __shared__ unsigned scan_ws[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
@@ -181,28 +210,33 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
     }
   }
   __syncthreads();
-  // ---- offsets (one thread: n <= 1024, cheap)
-  if (threadIdx.x == 0) {
-    int nt = 0, nr = 0, nw = 0;
-    a.cu_seqlens[0] = 0;
-    a.cu_rows[0] = 0;
-    for (int r = 0; r < a.n; ++r) {
-      a.vis_off[r] = nw;
-      nt += ntok_s[r];
-      nr += nrow_s[r];
-      nw += nword_s[r];
-      a.cu_seqlens[r + 1] = nt;
-      a.cu_rows[r + 1] = nr;
+  // ---- offsets: block scans over the requests (thread r = request r, n <= 256)
+  {
+    const int r = threadIdx.x;
+    const bool live = r < a.n;
+    unsigned tt, tr, tw;
+    const unsigned t_pre = block_exclusive_scan(live ? static_cast<unsigned>(ntok_s[r]) : 0u, scan_ws, &tt);
+    const unsigned r_pre = block_exclusive_scan(live ? static_cast<unsigned>(nrow_s[r]) : 0u, scan_ws, &tr);
+    const unsigned w_pre = block_exclusive_scan(live ? static_cast<unsigned>(nword_s[r]) : 0u, scan_ws, &tw);
+    if (live) {
+      a.vis_off[r] = static_cast<int>(w_pre);
+      a.cu_seqlens[r + 1] = static_cast<int>(t_pre) + ntok_s[r];
+      a.cu_rows[r + 1] = static_cast<int>(r_pre) + nrow_s[r];
       a.prompt_len[r] = a.prompt[a.slots[r]];
       a.key_end[r] = ke_s[r];
       a.vis_base[r] = vb_s[r];
     }
-    a.vis_off[a.n] = nw;
-    if (nt > a.cap_tok || nr > a.cap_rows || nw > a.cap_words) bad = 1;
-    a.counts[0] = nt;
-    a.counts[1] = nr;
-    a.counts[2] = nw;
-    a.counts[3] = bad ? OPTIMUS_EINVAL : 0;
+    if (r == 0) {
+      a.cu_seqlens[0] = 0;
+      a.cu_rows[0] = 0;
+      a.vis_off[a.n] = static_cast<int>(tw);
+      if (static_cast<int>(tt) > a.cap_tok || static_cast<int>(tr) > a.cap_rows || static_cast<int>(tw) > a.cap_words)
+        bad = 1;
+      a.counts[0] = static_cast<int>(tt);
+      a.counts[1] = static_cast<int>(tr);
+      a.counts[2] = static_cast<int>(tw);
+      a.counts[3] = bad ? OPTIMUS_EINVAL : 0;
+    }
   }
   __syncthreads();
   if (bad) return;
@@ -435,33 +469,6 @@ namespace dstep {
 constexpr int kPlanThreads = 1024;
 constexpr int kMaxUnits = 4096;
 
-// Exclusive prefix sum over the block's kPlanThreads values (warp shuffles, then one
-// warp over the 32 warp totals); *total = the sum.  All threads must call it.
-__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* ws, unsigned* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) ws[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned w = ws[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, w, o);
-      if (lane >= o) w += y;
-    }
-    ws[lane] = w;
-  }
-  __syncthreads();
-  const unsigned pre = (warp ? ws[warp - 1] : 0u) + x - v;
-  *total = ws[31];
-  __syncthreads();  // ws is reused by the next call
-  return pre;
-}
 
 template <int KPER>  // CTAs per lane: grid <= 32 * KPER
 __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
