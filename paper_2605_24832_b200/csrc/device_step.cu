@@ -654,8 +654,42 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
       }
     }
     __syncwarp();
+    // when every load fits 22 bits, one reduction of (load << 10 | cta) gives the
+    // least-loaded CTA with the lowest index on ties
+    unsigned sum = 0;
+    for (int x = first + lane; x < npc; x += 32) sum += static_cast<unsigned>(p_cta[x]);
+#pragma unroll
+    for (int i = 0; i < KPER; ++i) sum += lane + 32 * i < first ? load[i] : 0u;
+    sum = __reduce_add_sync(0xFFFFFFFFu, sum);
+    const bool packed = sum < (1u << 22);
+    if (packed) {
+      unsigned key[KPER];
+#pragma unroll
+      for (int i = 0; i < KPER; ++i) {
+        const int c = lane + 32 * i;
+        key[i] = c < grid ? ((load[i] << 10) | static_cast<unsigned>(c)) : 0xFFFFFFFFu;
+      }
 #pragma unroll 4
-    for (int x = first; x < npc; ++x) {
+      for (int x = first; x < npc; ++x) {
+        const unsigned cost = static_cast<unsigned>(p_cta[x]) << 10;
+        unsigned lm = key[0];
+#pragma unroll
+        for (int i = 1; i < KPER; ++i) lm = min(lm, key[i]);
+        const int bc = static_cast<int>(__reduce_min_sync(0xFFFFFFFFu, lm) & 1023u);
+        const int sel = (bc & 31) == lane ? (bc >> 5) : -1;
+        int rank = 0;
+#pragma unroll
+        for (int i = 0; i < KPER; ++i) {
+          const bool hit = i == sel;
+          rank = hit ? cnt[i] : rank;
+          key[i] += hit ? cost : 0u;
+          cnt[i] += hit ? 1 : 0;
+        }
+        if (sel >= 0) p_cta[x] = bc | (rank << 10);
+      }
+    }
+#pragma unroll 4
+    for (int x = packed ? npc : first; x < npc; ++x) {
       const unsigned cost = static_cast<unsigned>(p_cta[x]);
       unsigned best = 0xFFFFFFFFu;
       int bi = 0;
