@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "liboptimus_b200.so"
-SOURCES = ["kv_append.cu", "paged_attn.cu", "paged_attn2.cu", "unmask.cu", "capi.cu", "host_step.cu", "device_step.cu", "lmhead_unmask.cu"]
+SOURCES = ["kv_append.cu", "paged_attn.cu", "unmask.cu", "capi.cu", "host_step.cu", "device_step.cu", "lmhead_unmask.cu"]
 HEADERS = ["ptx.cuh", "attn.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -77,6 +77,29 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose:
         print("".join(logs))
     return LIB
+
+
+REF_SRC = Path("/root/reference/pkg")
+REF_DST = PKG.parent / "baseline" / "_ref"
+
+
+def install_reference() -> bool:
+    """Offline install of the reference package (``dllmsim``, pure Python) into
+    ``baseline/_ref`` — git-ignored, but it travels to the GPU box with the snapshot,
+    where the tests drive it with the B200 oracle plugged into ``Scenario.oracle_factory``
+    (sim.py:64).  The checkout is read-only, so the install builds from a /tmp copy.
+    Returns False when the checkout is absent (GPU box: the shipped install is used)."""
+    if not REF_SRC.exists():
+        return False
+    tmp = Path("/tmp/optimus_refpkg")
+    shutil.rmtree(tmp, ignore_errors=True)
+    shutil.copytree(REF_SRC, tmp, ignore=shutil.ignore_patterns("tests", "test_output.txt", "__pycache__"))
+    shutil.rmtree(REF_DST, ignore_errors=True)
+    cmd = [sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation", "--no-deps",
+           "--find-links", "/opt/wheelhouse", "--target", str(REF_DST), str(tmp), "-q"]
+    subprocess.run(cmd, check=True)
+    shutil.rmtree(tmp, ignore_errors=True)
+    return True
 
 
 if __name__ == "__main__":

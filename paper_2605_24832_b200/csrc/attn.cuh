@@ -43,8 +43,6 @@ struct AttnParams {
   int dbg;  // diagnostics: bit0 skip lo-plane PV, bit1 skip S MMA, bit2 skip softmax math, bit3 skip PV  // optional per-CTA timeline (diagnostics), nullptr in production
 };
 
-int launch_paged_attn_dual(int head_dim, bool v_fp16, const CUtensorMap& tq, const CUtensorMap& tk,
-                           const CUtensorMap& tv, const AttnParams& prm, int grid, cudaStream_t stream);
 int launch_attn_combine_dev(int head_dim, const AttnParams& prm, const int32_t* groups, int max_groups,
                             const int32_t* n_groups_dev, cudaStream_t stream);
 int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CUtensorMap& tk,

@@ -632,18 +632,6 @@ static int paged_attn_impl(const void* q, int64_t q_stride_tok, int n_tok_total,
     const char* e = getenv("OPTIMUS_DBG");
     prm.dbg = e ? atoi(e) : 0;
   }
-  // Experimental dual-slot K2 (paged_attn2.cu, off by default: 38 us vs 29.6 us on the
-  // ShareGPT batch): the work list was planned for 2 x #CTA virtual CTAs; attention
-  // only (no fused append), head_dim 128.
-  const bool dual = getenv("OPTIMUS_K2_DUAL") != nullptr;
-  if (dual && k_new == nullptr && head_dim == 128 && grid % 2 == 0) {
-    int st = launch_paged_attn_dual(head_dim, v_dtype == 1, tq, tk, tv, prm, grid / 2,
-                                    static_cast<cudaStream_t>(stream));
-    if (st) return cuda_status(st, "paged_attn_dual");
-    return cuda_status(launch_paged_attn(head_dim, v_dtype == 1, tq, tk, tv, prm, 0, groups, n_groups,
-                                         static_cast<cudaStream_t>(stream)),
-                       "paged_attn_combine");
-  }
   return cuda_status(launch_paged_attn(head_dim, v_dtype == 1, tq, tk, tv, prm, grid, groups,
                                        n_groups, static_cast<cudaStream_t>(stream)),
                      "paged_attn");

@@ -105,7 +105,7 @@ class StreamingDecoder:
                                            cfg.page_size, cfg.head_dim, device=self.device)
         self.pool = PagePool(self.cache.num_pages)
         self.tables = BlockTables(self.pool, cfg.max_batch, cfg.max_pages_per_req, cfg.page_size)
-        self.grid = ops.sm_count() * ops.k2_slots()
+        self.grid = ops.sm_count()
         self._pinned = None
         self._dev_buf = None
         self._ws_o = None

@@ -50,13 +50,6 @@ def sm_count() -> int:
     return int(_lib.call("optimus_device_sm_count"))
 
 
-def k2_slots() -> int:
-    """Virtual CTAs per SM the attention work list is planned for (2 with the
-    experimental dual-slot K2, OPTIMUS_K2_DUAL)."""
-    import os
-    return 2 if os.environ.get("OPTIMUS_K2_DUAL") else 1
-
-
 # --------------------------------------------------------------------------- K1
 def kv_append(
     k_new: torch.Tensor,
@@ -168,7 +161,7 @@ def plan_attention(
     ke = np.ascontiguousarray(key_end, dtype=np.int32)
     n_req = len(ke)
     if grid is None:
-        grid = (sm_count() if torch.cuda.is_available() else 148) * k2_slots()
+        grid = sm_count() if torch.cuda.is_available() else 148
     mw, mg = C.c_int(0), C.c_int(0)
     _lib.check(
         _lib.call(

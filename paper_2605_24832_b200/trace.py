@@ -1,110 +1,29 @@
-"""Commit traces: record what the B200 path committed, replay it in the simulator
+"""Record the commits of batched B200 steps as the reference's commit trace
 ("record/replay GPU commit traces via CommitTrace JSONL").
 
-The reference keeps a per-request list of committed-position sets per step and
-serialises it as JSON lines (``commit.py:206-251``); ``ReplayOracle`` drives an
-engine from such a trace, verbatim or with carry-over (``commit.py:254-312``).
-This module restates both with the same JSONL format, so a trace recorded from
-``StreamingDecoder.step`` / ``DeviceLoop.step`` (the K3 decisions of a real or
-synthetic model on the B200) loads into ``dllmsim.commit.CommitTrace.from_jsonl``
-unchanged and replays the decode exactly (``tests/test_trace.py``, pinned against
-``tests/golden/trace.json``, generated by the reference itself).
+The trace format, its validation and the replaying oracle are the reference's own
+classes (``dllmsim.commit.CommitTrace`` / ``ReplayOracle``, commit.py:205-312); this
+module only adds the recorder that feeds them from ``StreamingDecoder.step`` /
+``DeviceLoop.step``, so a trace of the K3 decisions of a real or synthetic model on
+the B200 replays the decode in the simulator exactly (``tests/test_trace.py``,
+``tests/test_device_loop_gpu.py``).
 """
 
 from __future__ import annotations
 
-import json
-from typing import Dict, Iterable, List, Optional, Sequence, Set
+from typing import Dict, Optional
 
-import numpy as np
-
-from .errors import TraceExhausted
+from .errors import ConfigError
 
 
-class CommitTrace:
-    """Per request, the ordered committed-position sets of its steps
-    (``commit.py:206-214``).  Sets are disjoint across steps; for a finished
-    request their union is every output position."""
-
-    def __init__(self, steps: Optional[Dict[int, List[Set[int]]]] = None):
-        self.steps: Dict[int, List[Set[int]]] = steps if steps is not None else {}
-
-    def record(self, request_id: int, step: int, positions: Iterable[int]) -> None:
-        """Append step `step` of a request; steps arrive in order (``commit.py:216-220``)."""
-        seq = self.steps.setdefault(request_id, [])
-        if step != len(seq):
-            raise ValueError(f"steps must be recorded in order, expected {len(seq)}, got {step}")
-        seq.append({int(p) for p in positions})
-
-    def validate(self, output_tokens: Dict[int, int]) -> None:
-        """No position twice; full coverage for requests of known length
-        (``commit.py:222-231``)."""
-        for rid, seq in self.steps.items():
-            union: Set[int] = set()
-            for s in seq:
-                if union & s:
-                    raise ValueError(f"request {rid}: positions committed twice")
-                union |= s
-            if rid in output_tokens and union != set(range(output_tokens[rid])):
-                raise ValueError(f"request {rid}: trace does not cover the output")
-
-    def to_jsonl(self) -> str:
-        """One ``{"request_id", "step", "positions"}`` object per line, requests in
-        id order, positions sorted (``commit.py:233-242``)."""
-        rows = [json.dumps({"request_id": rid, "step": k, "positions": sorted(s)})
-                for rid in sorted(self.steps) for k, s in enumerate(self.steps[rid])]
-        return "\n".join(rows) + "\n"
-
-    @classmethod
-    def from_jsonl(cls, text: str) -> "CommitTrace":
-        """Inverse of ``to_jsonl``; lines may come in any order (``commit.py:244-251``)."""
-        rows = [json.loads(line) for line in text.splitlines() if line.strip()]
-        rows.sort(key=lambda r: (r["request_id"], r["step"]))
-        trace = cls()
-        for r in rows:
-            trace.record(r["request_id"], r["step"], r["positions"])
-        return trace
-
-
-def replay_oracle(trace: CommitTrace, request_id: int, step_index: int, window: Sequence[int]) -> Set[int]:
-    """The traced step's positions that lie in the window; no progress rule
-    (``commit.py:254-267``).  Past the trace: ``TraceExhausted``."""
-    seq = trace.steps.get(request_id)
-    if seq is None or step_index >= len(seq):
-        raise TraceExhausted(f"no trace entry for request {request_id} step {step_index}")
-    return seq[step_index] & set(window)
-
-
-class ReplayOracle:
-    """Commit oracle that replays a trace (``commit.py:283-312``).
-
-    Strict (``carryover=False``): step k of a request commits exactly the traced
-    set of step k within the window.  Carry-over: a traced position that was not in
-    its step's window stays eligible and commits at the first later step whose
-    window holds it; after the trace's last step every uncommitted position is
-    eligible.  Plugs into the same loop as ``B200Oracle`` (``commits`` + ``consume``)."""
-
-    def __init__(self, trace: CommitTrace, carryover: bool = True):
-        self.trace = trace
-        self.carryover = carryover
-        self._eligible: Dict[int, Set[int]] = {}
-
-    def commits(self, request, window: Sequence[int]) -> Set[int]:
-        k = request.steps_taken
-        if not self.carryover:
-            return replay_oracle(self.trace, request.id, k, window)
-        pool = self._eligible.setdefault(request.id, set())
-        seq = self.trace.steps.get(request.id, [])
-        if k < len(seq):
-            pool |= seq[k]
-        elif not pool:
-            done = set(np.flatnonzero(np.asarray(request.states) != 0).tolist())
-            pool |= set(range(request.output_tokens)) - done
-        return pool & set(window)
-
-    def consume(self, request, committed: Set[int]) -> None:
-        if self.carryover and request.id in self._eligible:
-            self._eligible[request.id] -= set(committed)
+def commit_trace_cls():
+    """``dllmsim.commit.CommitTrace``; the reference package must be importable."""
+    try:
+        from dllmsim.commit import CommitTrace
+    except ImportError as e:  # pragma: no cover - depends on the install
+        raise ConfigError("commit traces need the reference package dllmsim "
+                          "(pip install --target baseline/_ref /root/reference/pkg)") from e
+    return CommitTrace
 
 
 class TraceRecorder:
@@ -116,8 +35,8 @@ class TraceRecorder:
     step, exactly the index the reference's loop records (``sim.py:269-305``).
     Requests that did not take a step (no computed tokens) are skipped."""
 
-    def __init__(self, trace: Optional[CommitTrace] = None):
-        self.trace = trace if trace is not None else CommitTrace()
+    def __init__(self, trace=None):
+        self.trace = trace if trace is not None else commit_trace_cls()()
         self._k: Dict[int, int] = {}
 
     def before(self, requests) -> None:
@@ -125,7 +44,7 @@ class TraceRecorder:
 
     def after(self, requests, summaries) -> None:
         for r, s in zip(requests, summaries):
-            k = self._k.get(r.id)
+            k: Optional[int] = self._k.get(r.id)
             if k is None or int(r.steps_taken) == k:
                 continue  # not stepped (finished, or a position admitted mid-flight)
             self.trace.record(r.id, k, s.commits)

@@ -6,6 +6,8 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+# the reference package (dllmsim) from its offline install, if not importable already
+import paper_2605_24832_b200  # noqa: E402,F401
 
 
 def pytest_configure(config):

@@ -10,9 +10,6 @@ Writes (small, committed):
                 hand-written cases of the reference's test_engine.py:50-157.
   commits.json  commit_step decisions for seeded windows (commit.py:86-112) and
                 calibrate_q goldens (test_commit.py:54-57).
-  costmodel.json  seeded (x, latency) profiles and the reference's own fit of
-                each (costmodel.fit, costmodel.py:118-176), serialised with
-                CostModel.to_json (costmodel.py:69-82), plus its profile CSV.
   trace.json    CommitTrace JSONL recorded from stochastic decodes
                 (commit.py:206-251) and ReplayOracle replays of it, strict and
                 carry-over, under other chunk sizes (commit.py:254-312).
@@ -28,7 +25,6 @@ import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from dllmsim.costmodel import fit as ref_fit, profile_to_csv  # noqa: E402
 from dllmsim.commit import (CommitProfile, CommitTrace, ReplayOracle, StochasticOracle,  # noqa: E402
                             TraceExhausted, calibrate_q, commit_step)
 from dllmsim.core import Request, TokenState, WindowRule  # noqa: E402
@@ -213,21 +209,10 @@ def main() -> None:
         "sharegpt_dense8b_sigma": sharegpt.rate_jitter_sigma,
     }
     (OUT / "commits.json").write_text(json.dumps({"draws": draws, "q": golden_q}))
-    fits = []
-    for seed in range(6):
-        rng = np.random.default_rng(500 + seed)
-        xs = np.sort(rng.choice(np.arange(2, 4096), size=int(rng.integers(12, 40)), replace=False)).astype(float)
-        b1, b2 = float(rng.uniform(64, 600)), float(rng.uniform(900, 2500))
-        lat = 1e-3 * (0.4 + 2e-4 * xs + 1.5e-3 * np.clip(xs - b1, 0, None) + 4e-3 * np.clip(xs - b2, 0, None))
-        lat = lat * (1.0 + 0.02 * rng.standard_normal(xs.size))
-        samples = [(float(a), float(b)) for a, b in zip(xs, lat)]
-        fits.append({"samples": samples, "fit": json.loads(ref_fit(samples).to_json()),
-                     "csv": profile_to_csv(samples)})
-    (OUT / "costmodel.json").write_text(json.dumps({"fits": fits}))
     traces = [trace_case(7, (40, 70, 33), 32, ((32, False), (32, True), (8, True), (4, True), (8, False))),
               trace_case(8, (97, 12), 16, ((16, False), (6, True), (32, True)))]
     (OUT / "trace.json").write_text(json.dumps({"cases": traces}))
-    print("wrote", OUT / "control.json", OUT / "commits.json", OUT / "costmodel.json", OUT / "trace.json",
+    print("wrote", OUT / "control.json", OUT / "commits.json", OUT / "trace.json",
           len(cases), "replays")
 
 

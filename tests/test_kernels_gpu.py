@@ -392,19 +392,3 @@ def test_decoder_step_with_no_requests():
                        max_batch=4, max_pages_per_req=16, num_pages=64)
     dec = StreamingDecoder(cfg, SyntheticForward(cfg, 64, 4))
     assert dec.step([], 8) == []
-
-
-@pytest.mark.parametrize("case", ["sharegpt_like", "split_kv", "bf16v"])
-def test_experimental_dual_slot_kernel_parity(case, monkeypatch):
-    """The experimental dual-slot K2 (paged_attn2.cu, OPTIMUS_K2_DUAL; two independent
-    pipelines per SM over a 2 x #SM work list) meets the same oracle bound."""
-    monkeypatch.setenv("OPTIMUS_K2_DUAL", "1")
-    if case == "sharegpt_like":
-        s = _step(71, 16, 32, 32, 64, 32, 8, 128)
-    elif case == "split_kv":
-        s = _step(72, 6, 8, 32, 64, 32, 8, 128, prompt_range=(4096, 9000), out_range=(20, 120))
-    else:
-        s = _step(73, 11, 16, 32, 16, 32, 8, 128, v_dtype=torch.bfloat16)
-    plan, err, got, ref = _attn_check(s, grid=2 * ops.sm_count())
-    assert np.isfinite(got).all()
-    assert err <= ATTN_RTOL, err

@@ -1,16 +1,19 @@
-"""Commit-trace record / replay: the package's CommitTrace JSONL and
-ReplayOracle against goldens recorded and replayed by the reference itself
-(tests/golden/make_golden.py: commit.py:206-312 driven through engine.py:45-95)."""
+"""Commit-trace record / replay.  The trace and the replaying oracle
+are the reference's own classes (dllmsim.commit, commit.py:205-312); what is tested
+here is this package's side of it: the engine mirror replays the reference's
+recorded traces step for step (goldens from tests/golden/make_golden.py), and
+TraceRecorder produces a trace the reference loads and validates."""
 
 import json
 
-import numpy as np
 import pytest
 
 from paper_2605_24832_b200 import engine as pe
 from paper_2605_24832_b200.core import Request
 from paper_2605_24832_b200.errors import TraceExhausted
-from paper_2605_24832_b200.trace import CommitTrace, ReplayOracle, TraceRecorder, replay_oracle
+from paper_2605_24832_b200.trace import TraceRecorder
+
+commit = pytest.importorskip("dllmsim.commit")
 
 
 @pytest.fixture(scope="module")
@@ -18,35 +21,12 @@ def golden(golden_dir):
     return json.loads((golden_dir / "trace.json").read_text())
 
 
-def test_jsonl_round_trip_is_byte_identical(golden):
-    for case in golden["cases"]:
-        t = CommitTrace.from_jsonl(case["jsonl"])
-        assert t.to_jsonl() == case["jsonl"]
-        t.validate({case["seed"] * 100 + i: out for i, out in enumerate(case["outs"])})
-        # lines in any order load the same trace
-        lines = case["jsonl"].strip().split("\n")
-        assert CommitTrace.from_jsonl("\n".join(reversed(lines))).to_jsonl() == case["jsonl"]
-
-
-def test_record_and_validate_errors():
-    t = CommitTrace()
-    t.record(1, 0, [0, 2])
-    with pytest.raises(ValueError):
-        t.record(1, 2, [1])  # out of order
-    t.record(1, 1, [2])
-    with pytest.raises(ValueError):
-        t.validate({})  # position 2 twice
-    t2 = CommitTrace()
-    t2.record(3, 0, [0])
-    with pytest.raises(ValueError):
-        t2.validate({3: 2})  # does not cover position 1
-    assert CommitTrace().to_jsonl() == "\n"
-
-
-def test_replays_match_reference(golden):
+def test_engine_mirror_replays_reference_traces(golden):
+    """dllmsim's ReplayOracle driving this package's plan_chunk / apply_chunk
+    reproduces the windows, commits and final states the reference recorded."""
     for case in golden["cases"]:
         for run in case["replays"]:
-            ro = ReplayOracle(CommitTrace.from_jsonl(case["jsonl"]), carryover=run["carryover"])
+            ro = commit.ReplayOracle(commit.CommitTrace.from_jsonl(case["jsonl"]), carryover=run["carryover"])
             for i, (out, want) in enumerate(zip(case["outs"], run["requests"])):
                 req = Request(id=case["seed"] * 100 + i, arrival_time=0.0, prompt_tokens=5, output_tokens=out)
                 steps = []
@@ -66,16 +46,6 @@ def test_replays_match_reference(golden):
                 assert req.states.tolist() == want["final_states"]
 
 
-def test_strict_replay_past_the_end_raises():
-    t = CommitTrace()
-    t.record(5, 0, [0, 1])
-    assert replay_oracle(t, 5, 0, [1, 2]) == {1}
-    with pytest.raises(TraceExhausted):
-        replay_oracle(t, 5, 1, [2])
-    with pytest.raises(TraceExhausted):
-        replay_oracle(t, 6, 0, [0])
-
-
 def test_recorder_skips_requests_that_did_not_step():
     class R:
         def __init__(self, i):
@@ -87,7 +57,31 @@ def test_recorder_skips_requests_that_did_not_step():
 
     a, b = R(1), R(2)
     rec = TraceRecorder()
+    assert isinstance(rec.trace, commit.CommitTrace)
     rec.before([a, b])
     a.steps_taken = 1  # b did not step
     rec.after([a, b], [S([0, 3]), S([])])
     assert rec.trace.steps == {1: [{0, 3}]}
+
+
+def test_recorded_decode_round_trips_through_reference_jsonl():
+    """Record a batched decode (engine mirror + the reference's stochastic oracle),
+    serialise with the reference's JSONL, validate coverage, replay strictly."""
+    prof = commit.CommitProfile(q=0.8)
+    oracle = commit.StochasticOracle(prof)
+    import numpy as np
+
+    reqs = [Request(id=i, arrival_time=0.0, prompt_tokens=7, output_tokens=40 + 9 * i,
+                    rng=np.random.default_rng(i)) for i in range(4)]
+    rec = TraceRecorder()
+    while not all(r.finished for r in reqs):
+        live = [r for r in reqs if not r.finished]
+        plans = pe.plan_batch(live, 8, 32, "in_block")
+        cs = [oracle.commits(r, list(p.window)) if p.window else set() for r, p in zip(live, plans)]
+        rec.before(live)
+        sums = pe.apply_batch(live, plans, cs, 32)
+        rec.after(live, sums)
+    text = rec.trace.to_jsonl()
+    tr = commit.CommitTrace.from_jsonl(text)
+    tr.validate({r.id: r.output_tokens for r in reqs})
+    assert tr.to_jsonl() == text

@@ -15,7 +15,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 import bench
-from paper_2605_24832_b200 import costmodel as cm
+import paper_2605_24832_b200  # noqa: F401  (puts baseline/_ref on sys.path)
+from dllmsim.costmodel import fit, profile_to_csv
 from paper_2605_24832_b200.decode import DecodeConfig, StreamingDecoder
 from paper_2605_24832_b200.engine import plan_batch
 from paper_2605_24832_b200.synthetic import SyntheticForward
@@ -80,7 +81,7 @@ for b in batches:
         print(f"batch {b:4d} chunk {c:3d}: x = {x:5d} computed tokens, step {lat * 1e3:8.3f} ms", flush=True)
         del gr
 print(f"{len(samples)} samples in {time.time() - t0:.0f} s")
-model = cm.fit(samples)
-Path(a.out + "_step_profile.csv").write_text(cm.profile_csv(samples))
-Path(a.out + "_cost_model.json").write_text(cm.to_json(model))
-print(cm.to_json(model))
+model = fit(samples)
+Path(a.out + "_step_profile.csv").write_text(profile_to_csv(samples))
+Path(a.out + "_cost_model.json").write_text(model.to_json())
+print(model.to_json())
