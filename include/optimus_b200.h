@@ -224,7 +224,9 @@ int optimus_unmask_partials(const void* logits, int logits_dtype, int64_t row_st
  *       fallback_mode 0 ("earliest"): the first window row always commits
  *                       (exactly commit.py:103);
  *       fallback_mode 1 ("top1"): if no row passes, the highest-confidence row
- *                       commits (ties -> earliest).
+ *                       commits (ties -> earliest);
+ *       fallback_mode 2 ("none"): threshold only (a step may commit nothing,
+ *                       as a ReplayOracle step can, commit.py:254-267).
  *     Optional state mirror update (pass NULL to skip): for committed row i of
  *     request r at output position row_pos[i]:
  *       state[r*state_stride + pos] = 1 (DECODED_UNCACHED), token_buf[same] = tok.

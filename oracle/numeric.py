@@ -140,7 +140,7 @@ def unmask(logits, cu_rows, tau: float = 0.9, fallback: str = "earliest"):
             continue
         if fallback == "earliest":
             commit[a] = True
-        elif not commit[a:b].any():
+        elif fallback == "top1" and not commit[a:b].any():
             commit[a + int(np.argmax(conf[a:b]))] = True
     return commit, tok, conf
 

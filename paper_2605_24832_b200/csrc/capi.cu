@@ -790,7 +790,7 @@ int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vs
                             const int32_t* row_pos, uint8_t* state, int32_t* token_buf,
                             int64_t state_stride, void* stream) {
   if (n_outer < 1 || n_rows < 0 || n_vsplit < 1 || n_req < 0) return fail("unmask: bad sizes");
-  if (fallback_mode != 0 && fallback_mode != 1) return fail("unmask: fallback_mode must be 0 or 1");
+  if (fallback_mode < 0 || fallback_mode > 2) return fail("unmask: fallback_mode must be 0, 1 or 2");
   if (n_req == 0) return 0;
   if (!part || !cu_rows || !commit_mask || !tok || !conf) return fail("unmask: null pointer");
   if (state && !row_pos) return fail("unmask: state update needs row_pos");

@@ -239,7 +239,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
     }
   }
   __syncthreads();
-  if (bad) return;
+  if (bad) {
+    // rejected: an empty step for every consumer that reads the counts / offsets
+    // (K1, K3, the work planner, apply), so a captured graph that keeps running
+    // cannot act on half-written metadata; counts[3] tells the host
+    for (int i = threadIdx.x; i <= a.n; i += blockDim.x) {
+      a.cu_seqlens[i] = 0;
+      a.cu_rows[i] = 0;
+      a.vis_off[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+      a.counts[0] = 0;
+      a.counts[1] = 0;
+      a.counts[2] = 0;
+    }
+    return;
+  }
   // ---- pass 2: layouts, visibility words, block tables
   for (int r = warp; r < a.n; r += kWarps) {
     const int s = a.slots[r];
@@ -325,11 +340,39 @@ struct ApplyArgs {
   int32_t* status;
 };
 
+// Validation pass (one thread per request, no writes but *status): the KV plan pops
+// the FIFO in order and every committed row is MASKED (engine.py:70-76,85-88).  The
+// apply kernel runs after it on the same stream and does nothing when *status is
+// set, so an illegal step leaves the whole batch unchanged (the reference checks
+// before it mutates, engine.py:83).  *status is sticky: the caller zeroes it (the
+// device loop shares it with the plan's counts[3], so a rejected plan skips apply).
+__global__ void __launch_bounds__(128) apply_validate_kernel(const ApplyArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n) return;
+  const int s = a.slots[r];
+  const int out = a.out_len[s];
+  if (a.committed[s] >= out) return;
+  const int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
+  const int32_t* q = a.queue + static_cast<int64_t>(s) * a.qcap;
+  const int nkv = (a.cu_seqlens[r + 1] - a.cu_seqlens[r]) - (a.cu_rows[r + 1] - a.cu_rows[r]);
+  const int head = a.q_head[s], len = a.q_len[s];
+  bool ok = nkv >= 0 && nkv <= len;
+  for (int i = 0; i < nkv && ok; ++i) ok = q[(head + i) % a.qcap] == a.tok_pos[a.cu_seqlens[r] + i];
+  int k = 0;
+  for (int i = a.cu_rows[r]; i < a.cu_rows[r + 1] && ok; ++i) {
+    if (!a.commit_mask[i]) continue;
+    const int p = a.row_pos[i];
+    ok = p >= 0 && p < out && st[p] == MASKED;
+    ++k;
+  }
+  if (!ok || len - nkv + k > a.qcap) *a.status = OPTIMUS_EINVAL;
+}
+
 // One warp per request (lane 0 walks the FIFO; the rest scan in parallel).
 __global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (r >= a.n) return;
+  if (r >= a.n || *a.status != 0) return;
   const int s = a.slots[r];
   int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
   int32_t* q = a.queue + static_cast<int64_t>(s) * a.qcap;
@@ -338,44 +381,29 @@ __global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
     if (lane == 0) a.commits_out[r] = 0;
     return;
   }
-  int ok = 1;
-  if (lane == 0) {
+  if (lane == 0) {  // validated: pop the KV plan, push the commits
     const int nkv = (a.cu_seqlens[r + 1] - a.cu_seqlens[r]) - (a.cu_rows[r + 1] - a.cu_rows[r]);
     int head = a.q_head[s], len = a.q_len[s];
-    for (int i = 0; i < nkv && ok; ++i) {
-      const int p = a.tok_pos[a.cu_seqlens[r] + i];
-      if (len == 0 || q[head] != p) {
-        ok = 0;  // KV plan out of order
-        break;
-      }
+    for (int i = 0; i < nkv; ++i) {
+      st[a.tok_pos[a.cu_seqlens[r] + i]] = CACHED;
       head = (head + 1) % a.qcap;
       --len;
-      st[p] = CACHED;
     }
     int k = 0;
-    for (int i = a.cu_rows[r]; i < a.cu_rows[r + 1] && ok; ++i) {
+    for (int i = a.cu_rows[r]; i < a.cu_rows[r + 1]; ++i) {
       if (!a.commit_mask[i]) continue;
       const int p = a.row_pos[i];
-      if (st[p] != MASKED || len >= a.qcap) {
-        ok = 0;
-        break;
-      }
       st[p] = UNCACHED;
       q[(head + len) % a.qcap] = p;
       ++len;
       ++k;
     }
-    if (ok) {
-      a.q_head[s] = head;
-      a.q_len[s] = len;
-      a.commits_out[r] = k;
-      a.committed[s] += k;
-      a.steps[s] += 1;
-    } else {
-      *a.status = OPTIMUS_EINVAL;
-    }
+    a.q_head[s] = head;
+    a.q_len[s] = len;
+    a.commits_out[r] = k;
+    a.committed[s] += k;
+    a.steps[s] += 1;
   }
-  if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return;
   __syncwarp();
   // advance_blocks: skip blocks without MASKED positions
   int bi = a.block_index[s];
@@ -448,6 +476,7 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
   ApplyArgs a{n, slots, block, cu_seqlens, tok_pos, cu_rows, row_pos, commit_mask, states, state_stride, queue,
               qcap, q_head, q_len, block_index, committed, steps_taken, cached_prefix, out_len, commits_out,
               status};
+  apply_validate_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   apply_kernel<<<(n * 32 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
@@ -494,6 +523,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
   __shared__ unsigned scan_ws[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) bad = 0;
+  __syncthreads();
   // 1. units: per request hkv * ceil(nq / T), request-major then head then token group
   unsigned n_units_req = 0;
   if (tid < n_req) {

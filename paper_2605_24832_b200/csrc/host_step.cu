@@ -172,6 +172,9 @@ int optimus_host_plan(int n, const int32_t* slots, int chunk, const int32_t* chu
 // Apply one step: kv positions -> DECODED_CACHED (FIFO pops), committed window rows
 // (commit_mask in row order) -> DECODED_UNCACHED appended to the ring, counters,
 // advance_blocks.  commits_out[r] receives the number of commits of batch row r.
+// Like the reference (_check_commits before any state change, engine.py:70-83),
+// every request of the batch is validated first; on OPTIMUS_EINVAL no state has
+// changed.
 int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu_seqlens,
                        const int32_t* tok_pos, const int32_t* cu_rows, const int32_t* row_pos,
                        const uint8_t* commit_mask, int8_t* states, int64_t state_stride,
@@ -179,6 +182,26 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
                        int32_t* block_index, int32_t* committed, int32_t* steps_taken,
                        int32_t* cached_prefix, const int32_t* out_len, int32_t* commits_out) {
   if (n < 0 || block < 1) return OPTIMUS_EINVAL;
+  // pass 1: validate (no writes)
+  for (int r = 0; r < n; ++r) {
+    const int s = slots[r];
+    if (committed[s] >= out_len[s]) continue;
+    const int8_t* st = states + static_cast<int64_t>(s) * state_stride;
+    const int32_t* q = queue + static_cast<int64_t>(s) * qcap;
+    const int nkv = (cu_seqlens[r + 1] - cu_seqlens[r]) - (cu_rows[r + 1] - cu_rows[r]);
+    if (nkv < 0 || nkv > q_len[s]) return OPTIMUS_EINVAL;
+    for (int i = 0; i < nkv; ++i)  // KV plan must pop the FIFO in order (engine.py:85-88)
+      if (q[(q_head[s] + i) % qcap] != tok_pos[cu_seqlens[r] + i]) return OPTIMUS_EINVAL;
+    int k = 0;
+    for (int i = cu_rows[r]; i < cu_rows[r + 1]; ++i) {
+      if (!commit_mask[i]) continue;
+      const int p = row_pos[i];
+      if (p < 0 || p >= out_len[s] || st[p] != MASKED) return OPTIMUS_EINVAL;  // IllegalCommit
+      ++k;
+    }
+    if (q_len[s] - nkv + k > qcap) return OPTIMUS_EINVAL;
+  }
+  // pass 2: apply
   for (int r = 0; r < n; ++r) {
     const int s = slots[r];
     if (committed[s] >= out_len[s]) {  // finished: not stepped (sim.py:307-313)
@@ -189,17 +212,14 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
     int32_t* q = queue + static_cast<int64_t>(s) * qcap;
     const int nkv = (cu_seqlens[r + 1] - cu_seqlens[r]) - (cu_rows[r + 1] - cu_rows[r]);
     for (int i = 0; i < nkv; ++i) {
-      const int p = tok_pos[cu_seqlens[r] + i];
-      if (q_len[s] == 0 || q[q_head[s]] != p) return OPTIMUS_EINVAL;  // KV plan out of order
+      st[tok_pos[cu_seqlens[r] + i]] = CACHED;
       q_head[s] = (q_head[s] + 1) % qcap;
       --q_len[s];
-      st[p] = CACHED;
     }
     int k = 0;
     for (int i = cu_rows[r]; i < cu_rows[r + 1]; ++i) {
       if (!commit_mask[i]) continue;
       const int p = row_pos[i];
-      if (st[p] != MASKED || q_len[s] >= qcap) return OPTIMUS_EINVAL;
       st[p] = UNCACHED;
       q[(q_head[s] + q_len[s]) % qcap] = p;
       ++q_len[s];

@@ -368,30 +368,100 @@ class StreamingDecoder:
 class B200Oracle:
     """The reference's commit-oracle protocol served by the B200 decode step.
 
-    ``commits(request, window)`` (commit.py:279-280 signature) runs the device
-    step for the batch that ``prime(requests, plans)`` / ``commits_batch``
-    announced, or — used standalone inside ``dllmsim``'s ``_Loop`` — for the
-    single request it is asked about.  ``consume`` is a no-op kept for protocol
-    parity (commit.py:310-312).
+    Plugs into ``Scenario.oracle_factory`` (sim.py:64,128-132) unchanged:
+    ``commits(request, window)`` (commit.py:279-280 signature) runs one device step
+    (K1 -> K2 per layer -> K3) for that request; ``commits_batch(requests, plans)``
+    runs ONE device step for a whole batch (the batched twin of the loop, see
+    ``sim_bridge.BatchedLoop``).  ``consume`` (commit.py:310-312) is forwarded to the
+    forward when it wants it (reference-oracle-driven logits).
+
+    KV bookkeeping.  The reference calls the oracle only when the plan's window is
+    non-empty (sim.py:278), yet ``apply_chunk`` still marks that plan's kv positions
+    DECODED_CACHED (engine.py:84-88): a step whose backlog filled the whole chunk
+    (engine.py:58-59) never reaches the device.  So the oracle keeps, per request,
+    the positions it committed in commit order (the device's view of the FIFO) and
+    how many of them the device has recomputed; every device step recomputes the
+    missed ones first, then the plan's own kv positions (rule K: each committed
+    position's final KV is computed exactly once, with its committed token).  A
+    request's pages are released when the commits returned finish it.
     """
 
     def __init__(self, decoder: StreamingDecoder, mode: str = "stream"):
         self.decoder = decoder
         self.mode = mode  # "stream" (chunked), or the block baselines "bd" / "prefix"
         self._cache: dict = {}
+        self._fifo: dict = {}   # request id -> positions committed through this oracle, in order
+        self._sent: dict = {}   # request id -> how many of them the device has recomputed
+        self.recomputed: dict = {}  # request id -> positions recomputed as kv rows, in order (diagnostics)
+        self.device_steps = 0
 
+    # ------------------------------------------------------------------ bookkeeping
+    def _track(self, req):
+        if req.id not in self._fifo:  # first sight: the current backlog is what is pending
+            self._fifo[req.id] = [int(p) for p in req.uncached_queue]
+            self._sent[req.id] = 0
+            self.recomputed[req.id] = []
+        return self._fifo[req.id]
+
+    def _device_plan(self, req, plan: ChunkPlan) -> tuple:
+        """(kv rows the device recomputes this step, index past them in the fifo)."""
+        fifo = self._track(req)
+        sent = self._sent[req.id]
+        queue = [int(p) for p in req.uncached_queue]
+        pending = fifo[sent:]
+        if queue and queue != pending[len(pending) - len(queue):]:
+            raise ConfigError(f"B200Oracle: request {req.id}'s uncached queue is not the tail of the positions "
+                              f"this oracle committed (was it committed by another oracle?)")
+        kv = tuple(int(p) for p in plan.kv_positions)
+        if tuple(queue[: len(kv)]) != kv:
+            raise ConfigError(f"B200Oracle: request {req.id}'s kv positions are not its FIFO head (engine.py:58)")
+        end = sent + (len(pending) - len(queue)) + len(kv)  # missed kv-only steps, then this plan's kv
+        return tuple(fifo[sent:end]), end
+
+    def _finish(self, req, committed) -> None:
+        self._fifo[req.id].extend(sorted(int(p) for p in committed))
+        if req.committed + len(committed) >= req.output_tokens:  # apply_chunk will finish it
+            if self.decoder.tables.slot(req.id) is not None:
+                self.decoder.release(req)
+            for d in (self._fifo, self._sent, self.recomputed):
+                d.pop(req.id, None)
+
+    # ------------------------------------------------------------------ protocol
     def commits_batch(self, requests: Sequence, plans: Sequence[ChunkPlan]) -> list:
-        idx = [i for i, p in enumerate(plans) if p.kv_positions or p.window]
-        sub_r = [requests[i] for i in idx]
-        sub_p = [plans[i] for i in idx]
         result = [set() for _ in requests]
+        if self.mode in ("bd", "prefix"):
+            idx = [i for i, p in enumerate(plans) if p.kv_positions or p.window]
+            dev_plans = [plans[i] for i in idx]
+            ends = None
+        else:
+            idx, dev_plans, ends = [], [], []
+            for i, (req, plan) in enumerate(zip(requests, plans)):
+                kv, end = self._device_plan(req, plan)
+                if kv or plan.window:
+                    idx.append(i)
+                    dev_plans.append(ChunkPlan(kv_positions=kv, window=tuple(plan.window)))
+                    ends.append(end)
+        sub_r = [requests[i] for i in idx]
         if sub_r:
-            dm = self.decoder.prepare(sub_r, sub_p)
+            dm = self.decoder.prepare(sub_r, dev_plans)
             res = self.decoder.device_step(dm)
+            self.device_steps += 1
             for i, c in zip(idx, self.decoder.fetch_commits(dm, res)):
                 result[i] = c
+        if ends is not None:
+            for i, dp, end in zip(idx, dev_plans, ends):
+                req = requests[i]
+                self.recomputed[req.id].extend(dp.kv_positions)
+                self._sent[req.id] = end
+        for req, c in zip(requests, result):
+            if self.mode in ("bd", "prefix"):
+                if req.committed + len(c) >= req.output_tokens and self.decoder.tables.slot(req.id) is not None:
+                    self.decoder.release(req)
+            else:
+                self._finish(req, c)
         for req, plan, c in zip(requests, plans, result):
-            self._cache[(req.id, tuple(plan.window))] = c
+            if plan.window:  # the reference never asks about an empty window (sim.py:278)
+                self._cache[(req.id, tuple(plan.window))] = c
         return result
 
     def commits(self, request, window) -> set:
@@ -412,7 +482,9 @@ class B200Oracle:
         return c
 
     def consume(self, request, committed) -> None:
-        return None
+        fn = getattr(self.decoder.forward, "consume", None)
+        if fn is not None:
+            fn(request, committed)
 
 
 def run_decode_batched(decoder: StreamingDecoder, batch: Sequence, chunk_size: int) -> tuple:

@@ -32,6 +32,14 @@ from .errors import ConfigError
 
 
 class DeviceLoop:
+    MAX_REQ, MAX_CHUNK, MAX_OUT, MAX_UNITS = 256, 128, 4096, 4096
+
+    @classmethod
+    def _check_request(cls, r, nat) -> None:
+        if r.output_tokens > min(cls.MAX_OUT, nat.bs.states.shape[1]):
+            raise ConfigError(f"DeviceLoop: request {r.id} has {r.output_tokens} output tokens > "
+                              f"{min(cls.MAX_OUT, nat.bs.states.shape[1])}")
+
     def __init__(self, decoder, requests, chunk: int, lookahead: bool = False):
         cfg = decoder.cfg
         if not getattr(decoder.forward, "resident_layers", False) or not hasattr(decoder.forward, "row_src_host"):
@@ -46,6 +54,18 @@ class DeviceLoop:
             raise ConfigError("DeviceLoop: one chunk >= 2 per request")
         self.chunk = int(self.chunk_h.max())
         nat = decoder.native()
+        # the device planners' hard limits (csrc/device_step.cu): checked here so a
+        # captured graph never runs a step they would reject
+        if len(requests) > self.MAX_REQ:
+            raise ConfigError(f"DeviceLoop: {len(requests)} requests > {self.MAX_REQ}")
+        if self.chunk > self.MAX_CHUNK:
+            raise ConfigError(f"DeviceLoop: chunk {self.chunk} > {self.MAX_CHUNK}")
+        for r in requests:
+            self._check_request(r, nat)
+        G = cfg.num_q_heads // cfg.num_kv_heads
+        units = len(requests) * cfg.num_kv_heads * -(-self.chunk // max(1, 128 // G))
+        if units > self.MAX_UNITS:
+            raise ConfigError(f"DeviceLoop: {units} attention units > {self.MAX_UNITS}")
         self.nat = nat
         self.requests = list(requests)
         self.n = n = len(self.requests)
@@ -73,7 +93,7 @@ class DeviceLoop:
         z = lambda m, dt=torch.int32: torch.zeros(max(m, 1), dtype=dt, device=dev)
         M = dict(cu_seqlens=z(n + 1), tok_req=z(ct), tok_pos=z(ct), prompt_len=z(n), key_end=z(n), vis_base=z(n),
                  vis_off=z(n + 1), vis_words=z(cw), cu_rows=z(n + 1), row_tok=z(cr), row_pos=z(cr), row_req=z(cr),
-                 counts=z(4), row_src=z(cr), commits=z(n), status=z(1))
+                 counts=z(4), row_src=z(cr), commits=z(n))
         M["block_tables"] = torch.zeros((n, max_pages), dtype=torch.int32, device=dev)
         G = cfg.num_q_heads // cfg.num_kv_heads
         T = 128 // G
@@ -163,8 +183,8 @@ class DeviceLoop:
             "optimus_device_apply", n, p(self.slots), cfg.block_size, p(M["cu_seqlens"]), p(M["tok_pos"]),
             p(M["cu_rows"]), p(M["row_pos"]), p(self.res.commit_mask), p(D["states"]), D["states"].shape[1],
             p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
-            p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["status"]), stream),
-            "device_apply")
+            p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["counts"][3:]),
+            stream), "device_apply")  # apply's status = the plan's counts[3]: a rejected plan skips apply
         for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
             self.H[k].copy_(M[k], non_blocking=True)
         self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
@@ -206,7 +226,8 @@ class DeviceLoop:
         n = self.n
         n_tok, n_rows = int(H["counts"][0]), int(H["counts"][1])
         if int(H["counts"][3]) != 0:
-            raise ConfigError("device plan rejected the step (capacity or chunk bounds)")
+            raise ConfigError("device step rejected (plan capacity / chunk bounds, or an illegal commit); "
+                              "the device state was left unchanged")
         if int(H["wcounts"][3]) != 0:
             raise ConfigError("device attention planner rejected the step (work / group capacity)")
         cu = H["cu_seqlens"].numpy()[: n + 1].copy()
@@ -264,6 +285,7 @@ class DeviceLoop:
         itself is unchanged (it reads the slot map and the state by pointer)."""
         if i not in self.free:
             raise ConfigError(f"DeviceLoop.replace: position {i} still holds a live request")
+        self._check_request(request, self.nat)
         # the position keeps its batch slot: another free position's slot map still
         # points at its own (finished, idle) slot
         s = self.nat._slot(request, int(self.slots_h[i]))

@@ -108,6 +108,7 @@ class BlockTables:
         s = self._slot_of.pop(request_id)
         n = int(self.n_pages[s])
         self.pool.free(self.table[s, :n].tolist())
+        self.table[s, :n] = 0  # no stale page ids survive in a free slot's row
         self.n_pages[s] = 0
         self._free_slots.append(s)
 

@@ -166,10 +166,11 @@ class NativeStepper:
         for i, req in enumerate(requests):
             slots[i] = self._slot(req)
         bs = self.bs
-        # pages for every position this step can touch (current block, +2 for OUT_BLOCK)
-        ahead = 3 if rule_value(cfg.window_rule) == "out_block" else 1
+        # pages for the current block up front (the common case needs no re-gather);
+        # positions the plan reaches beyond them (OUT_BLOCK windows can lie in any
+        # later block) are allocated from the exact plan below
         sl = slots.astype(np.int64)
-        reach = np.minimum(bs.out_len[sl], (bs.block_index[sl] + ahead) * cfg.block_size)
+        reach = np.minimum(bs.out_len[sl], (bs.block_index[sl] + 1) * cfg.block_size)
         need = (bs.prompt[sl] + reach + cfg.page_size - 1) // cfg.page_size
         tables = self.dec.tables
         for i in np.flatnonzero(need > tables.n_pages[sl]):
@@ -189,6 +190,7 @@ class NativeStepper:
             A.hptr("block_tables"), A.hptr("counts"))
         _lib.check(st, "optimus_host_plan")
         n_tok, n_rows, n_words = (int(x) for x in A.h("counts", 3))
+        self._cover_planned(n, sl, A, n_tok)
         # attention work list straight into the arena
         ng, npart = C.c_int(0), C.c_int(0)
         mw, mg = C.c_int(0), C.c_int(0)
@@ -222,6 +224,27 @@ class NativeStepper:
                            row_src_host=A.h("row_src"))
         return dm
 
+    def _cover_planned(self, n, sl, A, n_tok) -> None:
+        """Every planned position must have a page before K1 writes it: allocate the
+        pages the plan reaches beyond the current block and re-gather those requests'
+        block-table rows into the arena."""
+        if not n_tok:
+            return
+        cfg, tables, bs = self.cfg, self.dec.tables, self.bs
+        cu = A.h("cu_seqlens", n + 1)
+        pos = A.h("tok_pos", n_tok)
+        nz = np.flatnonzero(cu[1:] > cu[:-1])
+        hi = np.full(n, -1, dtype=np.int64)
+        hi[nz] = np.maximum.reduceat(pos, cu[:-1][nz])
+        need = (bs.prompt[sl] + hi + cfg.page_size) // cfg.page_size
+        short = np.flatnonzero((hi >= 0) & (need > tables.n_pages[sl]))
+        if short.size:
+            MP = cfg.max_pages_per_req
+            bt = A.h("block_tables", n * MP).reshape(n, MP)
+            for i in short:
+                tables.ensure(int(sl[i]), int(bs.prompt[sl[i]] + hi[i] + 1))
+                bt[i] = tables.table[sl[i]]
+
     def upload(self, dm) -> None:
         A = self.arena
         plan = dm.__dict__["attn_plan"]
@@ -243,7 +266,9 @@ class NativeStepper:
             self.mask_host[:n_rows].copy_(res.commit_mask[:n_rows], non_blocking=True)
             if want_tok:
                 self.tok_host[:n_rows].copy_(res.tokens[:n_rows], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        # always: the next plan() rewrites the pinned arena this step's non-blocking
+        # upload reads from, so that upload must have completed (even with no rows)
+        torch.cuda.current_stream().synchronize()
         self.d2h_bytes = n_rows * (5 if want_tok else 1)
         if want_tok and n_rows:
             fwd.on_commit(dm, self.mask_host.numpy()[:n_rows].astype(bool), self.tok_host.numpy()[:n_rows])

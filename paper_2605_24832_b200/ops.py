@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from .errors import ConfigError
 
-FALLBACK_MODES = {"earliest": 0, "top1": 1}
+FALLBACK_MODES = {"earliest": 0, "top1": 1, "none": 2}
 
 
 def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:

@@ -240,6 +240,10 @@ class OracleDrivenForward(Forward):
                 u = req.rng.random(n - 1)
                 dec += [bool(uj < min(1.0, m * self.q ** j)) for j, uj in enumerate(u, start=1)]
             confs += [self.t_hi if d else self.t_lo for d in dec]
+        return self._peaked(confs), None
+
+    def _peaked(self, confs):
+        """Window-row logits with max-softmax confidence confs[i] (SURVEY §8c recipe)."""
         n_rows = len(confs)
         V = self.cfg.vocab
         x = torch.randn((max(n_rows, 1), V), generator=self.gen, device=self.device, dtype=torch.float32)
@@ -249,7 +253,41 @@ class OracleDrivenForward(Forward):
             lse = torch.logsumexp(x, dim=1)
             c = torch.as_tensor(confs, device=self.device, dtype=torch.float32)
             x.scatter_(1, tok[:, None], (lse + torch.log(c / (1 - c)))[:, None])
-        return x.to(self.cfg.logits_dtype), None
+        return x.to(self.cfg.logits_dtype)
+
+
+class ReferenceOracleForward(OracleDrivenForward):
+    """Stand-in model whose logits encode ANY reference commit oracle's decisions
+    (``StochasticOracle``, ``ReplayOracle``, a test's custom oracle: the duck-typed
+    protocol of engine.py:105-110).  For every request with window rows in the step,
+    ``inner.commits(request, window)`` is asked once and each row's logits get
+    confidence 0.97 (committed) or 0.80 (held); with tau = 0.9 and fallback "none"
+    the B200 unmask reproduces the inner oracle's sets exactly.  ``consume`` is
+    forwarded, so carry-over replay keeps working.  This is how the B200 oracle is
+    driven inside dllmsim's own loop (``Scenario.oracle_factory``, sim.py:64,128-132)
+    without a model checkpoint."""
+
+    def __init__(self, cfg: DecodeConfig, inner, max_tokens: int, device="cuda", seed: int = 0, **kw):
+        super().__init__(cfg, max_tokens, 0.0, device=device, seed=seed, **kw)
+        self.inner = inner
+
+    def logits(self, dm: DeviceMeta):
+        reqs = dm.__dict__["requests"]
+        cu_rows, row_pos = dm.host.cu_rows, dm.host.row_pos
+        confs = []
+        for r, req in enumerate(reqs):
+            a, b = int(cu_rows[r]), int(cu_rows[r + 1])
+            if b == a:
+                continue
+            window = [int(p) for p in row_pos[a:b]]
+            got = self.inner.commits(req, window)
+            confs += [self.t_hi if p in got else self.t_lo for p in window]
+        return self._peaked(confs), None
+
+    def consume(self, request, committed) -> None:
+        fn = getattr(self.inner, "consume", None)
+        if fn is not None:
+            fn(request, committed)
 
 
 class TPForward(SyntheticForward):

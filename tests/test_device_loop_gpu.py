@@ -143,7 +143,9 @@ def test_recorded_gpu_trace_replays_exactly(path):
     step, identical final states."""
     from paper_2605_24832_b200 import engine as pe
     from paper_2605_24832_b200.core import Request
-    from paper_2605_24832_b200.trace import CommitTrace, ReplayOracle, TraceRecorder
+    from dllmsim.commit import CommitTrace, ReplayOracle
+
+    from paper_2605_24832_b200.trace import TraceRecorder
 
     batch, chunk = 8, 16
     staged, dec = _setup(6, batch, chunk)
@@ -229,3 +231,17 @@ def test_graph_captured_host_step_matches_eager(monkeypatch):
         steps += 1
         assert steps < 5000
     assert dec_g.native()._graphs  # the graph path ran
+
+
+def test_device_loop_rejects_what_the_device_planners_cannot_run():
+    """Limits of csrc/device_step.cu are checked before capture (chunk <= 128,
+    out_len <= 4096 / the packed state's capacity, <= 256 requests)."""
+    from paper_2605_24832_b200.core import Request
+    from paper_2605_24832_b200.errors import ConfigError
+
+    reqs, dec = _setup(4, 4, 8)
+    with pytest.raises(ConfigError):
+        DeviceLoop(dec, reqs, 130)
+    big = Request(id=999, arrival_time=0.0, prompt_tokens=10, output_tokens=5000)
+    with pytest.raises(ConfigError):
+        DeviceLoop(dec, reqs[:3] + [big], 8)

@@ -133,6 +133,44 @@ def test_device_apply_rejects_out_of_order_kv():
     assert st == 0
     torch.cuda.synchronize()
     assert int(status.item()) == -1
+    for k in ("states", "q_head", "q_len", "committed", "steps_taken"):  # nothing applied
+        assert np.array_equal(D[k].cpu().numpy(), getattr(bs, k)), k
+
+
+def test_device_apply_is_atomic_over_the_batch():
+    """An illegal commit in the last request leaves every request unchanged
+    (validation pass before the apply kernel; engine.py:70-83 checks first)."""
+    bs = BatchState(3, 64, qcap=8)
+    reqs = make_requests(6, 3, (3, 10), (20, 30), 8, 16, "in_block")
+    for r in reqs:
+        r.states[:] = 0
+        r.uncached_queue.clear()
+        r.committed = r.block_index = r.steps_taken = 0
+    for i, r in enumerate(reqs):
+        bs.bind(r, i)
+    bs.states[2, 1] = 1  # request 2 position 1 is already decoded
+    L = _lib.load()
+    # each request: no kv, window rows (0, 1); all rows commit -> request 2 row 1 is illegal
+    cu = _dev(np.array([0, 2, 4, 6], np.int32))
+    tok = _dev(np.array([0, 1, 0, 1, 0, 1], np.int32))
+    cur = _dev(np.array([0, 2, 4, 6], np.int32))
+    rp = _dev(np.array([0, 1, 0, 1, 0, 1], np.int32))
+    mask = _dev(np.ones(6, np.uint8))
+    D = {k: _dev(getattr(bs, k)) for k in ("states", "queue", "q_head", "q_len", "block_index", "committed",
+                                            "steps_taken", "cached_prefix", "out_len")}
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sl = _dev(np.array([0, 1, 2], np.int32))
+    c0 = torch.zeros(3, dtype=torch.int32, device="cuda")
+    st = L.optimus_device_apply(
+        3, _p(sl), 16, _p(cu), _p(tok), _p(cur), _p(rp), _p(mask),
+        _p(D["states"]), D["states"].shape[1], _p(D["queue"]), bs.qcap, _p(D["q_head"]), _p(D["q_len"]),
+        _p(D["block_index"]), _p(D["committed"]), _p(D["steps_taken"]), _p(D["cached_prefix"]), _p(D["out_len"]),
+        _p(c0), _p(status), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    assert int(status.item()) != 0
+    for k in ("states", "q_head", "q_len", "committed", "steps_taken", "block_index"):
+        assert np.array_equal(D[k].cpu().numpy(), getattr(bs, k)), k
 
 
 @pytest.mark.parametrize("hq,hkv,page,maxq,ke_hi", [(32, 8, 64, 33, 3000), (32, 8, 16, 33, 9000), (64, 8, 16, 33, 800),

@@ -123,3 +123,37 @@ def test_bound_requests_work_with_reference_functions_and_unbind():
         assert np.array_equal(back.states, twin[i].states)
         assert list(back.uncached_queue) == list(twin[i].uncached_queue)
         assert back.committed == twin[i].committed and back.block_index == twin[i].block_index
+
+
+def test_illegal_commit_leaves_every_request_unchanged():
+    """optimus_host_apply validates the whole batch before it changes anything
+    (the reference checks commits before mutating, engine.py:70-83): an illegal
+    commit in the LAST request leaves the earlier requests' state untouched too."""
+    reqs = make_requests(5, 3, (1, 50), (40, 60), 8, 32, "in_block")
+    bs = BatchState(4, 128, qcap=32)
+    for i, r in enumerate(reqs):
+        bs.bind(r, i)
+    tables = np.arange(4 * 8, dtype=np.int32).reshape(4, 8)
+    idx = [0, 1, 2]
+    out, counts = _native_plan(bs, idx, 8, 32, "in_block", tables)
+    n_rows = int(counts[1])
+    mask = np.ones(n_rows, np.uint8)
+    before = {k: getattr(bs, k).copy() for k in ("states", "queue", "q_head", "q_len", "block_index", "committed",
+                                                  "steps_taken", "cached_prefix")}
+    # corrupt the last request's last row: point it at an already-decoded position
+    last = int(out["cu_rows"][3]) - 1
+    bs.states[2, 0] = 1
+    before["states"][2, 0] = 1
+    out["row_pos"][last] = 0
+    commits = np.zeros(3, np.int32)
+    m = np.ascontiguousarray(mask)
+    sl = np.asarray(idx, dtype=np.int32)
+    st = _lib.load().optimus_host_apply(
+        3, sl.ctypes.data, 32, out["cu_seqlens"].ctypes.data, out["tok_pos"].ctypes.data,
+        out["cu_rows"].ctypes.data, out["row_pos"].ctypes.data, m.ctypes.data, bs.states.ctypes.data,
+        bs.states.shape[1], bs.queue.ctypes.data, bs.qcap, bs.q_head.ctypes.data, bs.q_len.ctypes.data,
+        bs.block_index.ctypes.data, bs.committed.ctypes.data, bs.steps_taken.ctypes.data,
+        bs.cached_prefix.ctypes.data, bs.out_len.ctypes.data, commits.ctypes.data)
+    assert st != 0
+    for k, v in before.items():
+        assert np.array_equal(getattr(bs, k), v), k
