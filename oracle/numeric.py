@@ -90,7 +90,7 @@ def gather_keys(cache: np.ndarray, block_table, n_keys: int, page_size: int) -> 
 
 def paged_attention(q, k_cache, v_cache, cu_seqlens, q_pos, prompt_len, vis_out_list,
                     block_tables, block_size: int, page_size: int, sm_scale=None,
-                    dtype=np.float32) -> np.ndarray:
+                    dtype=np.float32, workers: int = 1) -> np.ndarray:
     """Reference output [n_tok, Hq, d] for the decode step.
 
     ``vis_out_list[r]`` is the boolean visibility of request r's output positions
@@ -102,10 +102,11 @@ def paged_attention(q, k_cache, v_cache, cu_seqlens, q_pos, prompt_len, vis_out_
     G = hq // hkv
     scale = (1.0 / np.sqrt(d)) if sm_scale is None else sm_scale
     out = np.zeros((n_tok, hq, d), dtype=np.float32)
-    for r in range(len(cu_seqlens) - 1):
+
+    def one(r):
         t0, t1 = int(cu_seqlens[r]), int(cu_seqlens[r + 1])
         if t1 == t0:
-            continue
+            return
         prompt = int(prompt_len[r])
         vis_out = vis_out_list[r]
         n_keys = prompt + len(vis_out)
@@ -123,16 +124,40 @@ def paged_attention(q, k_cache, v_cache, cu_seqlens, q_pos, prompt_len, vis_out_
             P /= P.sum(axis=1, keepdims=True)
             O = P @ V[:, h, :]
             out[t0:t1, h * G:(h + 1) * G, :] = O.reshape(nq, G, d)
+
+    _for_each(one, range(len(cu_seqlens) - 1), workers)
     return out
 
 
-def unmask(logits, cu_rows, tau: float = 0.9, fallback: str = "earliest"):
+def _for_each(fn, items, workers: int) -> None:
+    """Run fn over items, on `workers` threads when > 1 (numpy releases the GIL in
+    its array kernels; requests / row blocks are independent)."""
+    items = list(items)
+    if workers <= 1:
+        for i in items:
+            fn(i)
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(workers) as ex:
+        for _ in ex.map(fn, items):
+            pass
+
+
+def unmask(logits, cu_rows, tau: float = 0.9, fallback: str = "earliest", workers: int = 1):
     """Rule U -> (commit_mask bool[n], tok int64[n], conf float64[n])."""
-    x = np.asarray(logits, dtype=np.float64)
+    x = np.asarray(logits)
     n = x.shape[0]
-    tok = np.argmax(x, axis=1) if n else np.zeros(0, dtype=np.int64)
-    m = x.max(axis=1, keepdims=True) if n else np.zeros((0, 1))
-    conf = 1.0 / np.exp(x - m).sum(axis=1) if n else np.zeros(0)
+    tok = np.zeros(n, dtype=np.int64)
+    conf = np.zeros(n, dtype=np.float64)
+
+    def rows(a):
+        b = min(n, a + 16)
+        xb = np.asarray(x[a:b], dtype=np.float64)
+        tok[a:b] = np.argmax(xb, axis=1)
+        conf[a:b] = 1.0 / np.exp(xb - xb.max(axis=1, keepdims=True)).sum(axis=1)
+
+    _for_each(rows, range(0, n, 16), workers)
     commit = conf >= tau
     for r in range(len(cu_rows) - 1):
         a, b = int(cu_rows[r]), int(cu_rows[r + 1])

@@ -91,6 +91,25 @@ def make_batch(seed: int, batch: int, chunk: int, block: int = 32, rule: str = "
     return reqs
 
 
+def logit_recipe(seed: int, n_versions: int, max_slots: int, rows_per_slot: int, vocab: int, q: float,
+                 sigma: float, t_hi: float = 0.97, t_lo: float = 0.80):
+    """The logit table's decisions (SURVEY §8c recipe): per (version, slot, window
+    rank) whether the row commits (rank 0 always; rank j w.p. min(1, m q^j), m the
+    slot's rate multiplier — commit_step's rule, commit.py:103-111), its peak's
+    max-softmax confidence (t_hi / t_lo around tau = 0.9) and its peak token.
+    Shared by the GPU table (SyntheticForward) and the CPU reference arm (bench.py),
+    which therefore take the same decisions on the same rows."""
+    rng = np.random.default_rng(seed + 17)
+    mult = np.array([rate_multiplier(rng, sigma) for _ in range(max_slots)])
+    rank = np.arange(rows_per_slot)
+    p = np.minimum(1.0, mult[None, :, None] * q ** rank[None, None, :])
+    commit = rng.random((n_versions, max_slots, rows_per_slot)) < p
+    commit[..., 0] = True
+    conf = np.where(commit, t_hi, t_lo)
+    tok = rng.integers(0, vocab, n_versions * max_slots * rows_per_slot).reshape(commit.shape)
+    return commit, conf, tok
+
+
 class SyntheticForward(Forward):
     """Random activations at the decode shape plus oracle-driven logits."""
 
@@ -122,18 +141,12 @@ class SyntheticForward(Forward):
 
     def _make_logits(self, g, seed, q, sigma, t_hi, t_lo, v0, v1):
         cfg = self.cfg
-        rng = np.random.default_rng(seed + 17)
         n = self.n_versions * self.max_slots * self.rows_per_slot
         width = v1 - v0
         out = torch.empty((n, width), dtype=cfg.logits_dtype, device=self.device)
-        # decide per (version, slot, rank) whether the row commits, then place the peak
-        mult = np.array([rate_multiplier(rng, sigma) for _ in range(self.max_slots)])
-        rank = np.arange(self.rows_per_slot)
-        p = np.minimum(1.0, mult[None, :, None] * q ** rank[None, None, :])
-        commit = rng.random((self.n_versions, self.max_slots, self.rows_per_slot)) < p
-        commit[..., 0] = True
-        conf = np.where(commit, t_hi, t_lo).reshape(-1)
-        tok = rng.integers(0, cfg.vocab, n)
+        commit, conf, tok = logit_recipe(seed, self.n_versions, self.max_slots, self.rows_per_slot, cfg.vocab, q,
+                                         sigma, t_hi, t_lo)
+        conf = conf.reshape(-1)
         chunk = 256
         V = cfg.vocab
         lg = torch.Generator(device=self.device)
@@ -141,7 +154,7 @@ class SyntheticForward(Forward):
             b = min(n, a + chunk)
             lg.manual_seed(seed * 1000003 + a)
             x = torch.randn((b - a, V), generator=lg, device=self.device, dtype=torch.float32)
-            t = torch.as_tensor(tok[a:b], device=self.device)
+            t = torch.as_tensor(tok.reshape(-1)[a:b], device=self.device)
             x.scatter_(1, t[:, None], -float("inf"))
             lse = torch.logsumexp(x, dim=1)
             c = torch.as_tensor(conf[a:b], device=self.device, dtype=torch.float32)
