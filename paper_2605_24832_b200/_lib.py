@@ -118,6 +118,8 @@ def load(path: os.PathLike | None = None):
     except OSError as exc:  # pragma: no cover - environment specific
         raise ExtensionMissing(f"cannot load {p}: {exc}") from exc
     for name, (res, args) in SIGNATURES.items():
+        if path is not None and not hasattr(lib, name):
+            continue  # another build (tools/ab_lib.py): type what it exports
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

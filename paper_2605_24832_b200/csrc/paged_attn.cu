@@ -108,11 +108,7 @@ struct AttnSmem {
   static_assert(TM_Q + HD / 2 <= TM_O && TM_O + 2 * HD <= TMEM_COLS, "TMEM budget");
 };
 
-// INF > 0: a producer issues tile t only once tile t - INF of its ring has landed, so
-// at most INF tiles per ring are in flight in DRAM while up to KST / VST landed tiles
-// wait in shared memory (a consumer stall at an item boundary keeps the loads going
-// without deepening the DRAM queues).  INF = 0: in flight = ring depth.
-template <int HD, int KST, int VST, bool VF16, int INF = 0>
+template <int HD, int KST, int VST, bool VF16>
 __global__ void __launch_bounds__(kThreads, 1)
     paged_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_k,
@@ -267,10 +263,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           // this tile holds rows appended in this step: wait for the append once
           mbar_wait(append_done, 0);
           need_append = false;
-        }
-        if (INF > 0 && tile_ctr >= INF) {
-          const int tl = tile_ctr - INF;  // in-flight cap: that tile has landed
-          mbar_wait(&full[tl % NST], (tl / NST) & 1);
         }
         mbar_wait(&empty[st], ((tile_ctr / NST) & 1) ^ 1);
         if (lane == 0) trace(p, is_k ? 4 : 10, tile_ctr);
@@ -901,14 +893,14 @@ int launch_attn_combine_dev(int head_dim, const AttnParams& prm, const int32_t* 
                          : launch_combine_t<64>(prm, groups, max_groups, n_groups_dev, stream);
 }
 
-template <int HD, int KST, int VST, bool VF16, int INF = 0>
+template <int HD, int KST, int VST, bool VF16>
 static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          const AttnParams& prm, int grid, const int32_t* groups, int n_groups,
                          cudaStream_t stream) {
   using L = AttnSmem<HD, KST, VST>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, KST, VST, VF16, INF>,
+    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, KST, VST, VF16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC);
     if (e != cudaSuccess) return static_cast<int>(e);
     configured = true;
@@ -927,7 +919,7 @@ static int launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, paged_attn_kernel<HD, KST, VST, VF16, INF>, tq, tk, tv, prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, paged_attn_kernel<HD, KST, VST, VF16>, tq, tk, tv, prm);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (n_groups > 0) {
@@ -957,14 +949,6 @@ int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CU
     if (rings == 56)
       return v_fp16 ? launch_attn_t<128, 5, 6, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
                     : launch_attn_t<128, 5, 6, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
-    if (rings == 563 && v_fp16)  // 5 K / 6 V stages, 3 tiles in flight per ring
-      return launch_attn_t<128, 5, 6, true, 3>(tq, tk, tv, prm, grid, groups, n_groups, stream);
-    if (rings == 564 && v_fp16)
-      return launch_attn_t<128, 5, 6, true, 4>(tq, tk, tv, prm, grid, groups, n_groups, stream);
-    if (rings == 443 && v_fp16)
-      return launch_attn_t<128, 4, 4, true, 3>(tq, tk, tv, prm, grid, groups, n_groups, stream);
-    if (rings == 553 && v_fp16)
-      return launch_attn_t<128, 5, 5, true, 3>(tq, tk, tv, prm, grid, groups, n_groups, stream);
     return v_fp16 ? launch_attn_t<128, 3, 3, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
                   : launch_attn_t<128, 3, 3, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
   }

@@ -92,11 +92,16 @@ if a.ab:
     os.environ.pop("OPTIMUS_PLAN_FORCE")
     graphs = []
     for name, pl, dbg in variants:
-        os.environ["OPTIMUS_DBG"] = dbg.split(":")[0]
-        if ":" in dbg:
-            os.environ["OPTIMUS_K2_RINGS"] = dbg.split(":")[1]
+        parts = dbg.split(":")
+        os.environ["OPTIMUS_DBG"] = parts[0]
+        if len(parts) > 1 and parts[1]:
+            os.environ["OPTIMUS_K2_RINGS"] = parts[1]
         else:
             os.environ.pop("OPTIMUS_K2_RINGS", None)
+        if len(parts) > 2:  # "kernel": the separate split-KV combine kernel
+            os.environ["OPTIMUS_K2_COMBINE"] = parts[2]
+        else:
+            os.environ.pop("OPTIMUS_K2_COMBINE", None)
         plan = pl
         out = dec._workspaces(pl, m.n_tok)
         s_ = torch.cuda.Stream(); s_.wait_stream(torch.cuda.current_stream())
