@@ -44,6 +44,10 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
   const int page = __ldg(block_tables + static_cast<int64_t>(r) * max_pages + s / page_size);
   const int off = s % page_size;
   const int64_t src = static_cast<int64_t>(t) * new_stride_vec + i;
+  // PDL: the slot computation above overlapped the preceding grid's tail; the rows
+  // (its outputs in a model) and the pages (a preceding attention grid may still read
+  // them) are touched only after it completed
+  grid_dep_wait();
   const uint4 kv = __ldg(k_new + src);
   const uint4 vv = __ldg(v_new + src);
   const int64_t dst =
@@ -64,6 +68,27 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
   if (i == 0 && slot_out != nullptr) slot_out[t] = static_cast<int64_t>(page) * page_size + off;
 }
 
+// K1 launches with programmatic stream serialization: its blocks start on the SMs the
+// preceding grid (the previous layer's attention) releases, and wait in-kernel.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int blocks, int threads, cudaStream_t stream,
+                              Args... args) {
+  static const bool pdl = [] {
+    const char* e = getenv("OPTIMUS_K1_PDL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_tok,
                      const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
                      const int32_t* block_tables, int max_pages, int n_tok, int hkv, int head_dim,
@@ -74,11 +99,11 @@ int launch_kv_append(const void* k_new, const void* v_new, int64_t new_stride_to
   const int64_t total = static_cast<int64_t>(n_tok) * hkv * vec_per_head;
   const int threads = 256;
   const int blocks = static_cast<int>((total + threads - 1) / threads);
-  kv_append_kernel<<<blocks, threads, 0, stream>>>(
-      static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
-      tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok, hkv, vec_per_head, page_size,
-      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), slot_out, v_fp16, nullptr);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(launch_pdl(
+      kv_append_kernel, blocks, threads, stream, static_cast<const uint4*>(k_new),
+      static_cast<const uint4*>(v_new), new_stride_tok / 8, tok_req, tok_pos, prompt_len, block_tables,
+      max_pages, n_tok, hkv, vec_per_head, page_size, static_cast<uint4*>(k_cache),
+      static_cast<uint4*>(v_cache), slot_out, v_fp16, static_cast<const int32_t*>(nullptr)));
 }
 
 // Same, with the token count read from device memory (n_tok_cap sizes the grid).
@@ -91,11 +116,11 @@ int launch_kv_append_dev(const void* k_new, const void* v_new, int64_t new_strid
   const int vec_per_head = head_dim / 8;
   const int64_t total = static_cast<int64_t>(n_tok_cap) * hkv * vec_per_head;
   const int blocks = static_cast<int>((total + 255) / 256);
-  kv_append_kernel<<<blocks, 256, 0, stream>>>(
-      static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
-      tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok_cap, hkv, vec_per_head, page_size,
-      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), nullptr, v_fp16, n_tok_dev);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(launch_pdl(
+      kv_append_kernel, blocks, 256, stream, static_cast<const uint4*>(k_new),
+      static_cast<const uint4*>(v_new), new_stride_tok / 8, tok_req, tok_pos, prompt_len, block_tables,
+      max_pages, n_tok_cap, hkv, vec_per_head, page_size, static_cast<uint4*>(k_cache),
+      static_cast<uint4*>(v_cache), static_cast<int64_t*>(nullptr), v_fp16, n_tok_dev));
 }
 
 // K1 over a precomputed per-step slot map (optimus_slot_mapping): one round trip
@@ -114,6 +139,7 @@ __global__ void __launch_bounds__(256) kv_append_slots_kernel(
   const int c = i - h * vec_per_head;
   const int slot = __ldg(slot_abs + t).y;
   const int64_t src = static_cast<int64_t>(t) * new_stride_vec + i;
+  grid_dep_wait();
   const uint4 kv = __ldg(k_new + src);
   const uint4 vv = __ldg(v_new + src);
   const int64_t dst = ((static_cast<int64_t>(slot >> page_shift) * hkv + h) * page_size +
@@ -140,12 +166,11 @@ int launch_kv_append_slots(const void* k_new, const void* v_new, int64_t new_str
   const int vec_per_head = head_dim / 8;
   const int64_t total = static_cast<int64_t>(n_tok) * hkv * vec_per_head;
   const int blocks = static_cast<int>((total + 255) / 256);
-  kv_append_slots_kernel<<<blocks, 256, 0, stream>>>(
-      static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), new_stride_tok / 8,
-      reinterpret_cast<const int2*>(slot_abs), n_tok, hkv, vec_per_head, page_size,
-      __builtin_ctz(static_cast<unsigned>(page_size)), static_cast<uint4*>(k_cache),
-      static_cast<uint4*>(v_cache), v_fp16);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(launch_pdl(
+      kv_append_slots_kernel, blocks, 256, stream, static_cast<const uint4*>(k_new),
+      static_cast<const uint4*>(v_new), new_stride_tok / 8, reinterpret_cast<const int2*>(slot_abs), n_tok,
+      hkv, vec_per_head, page_size, __builtin_ctz(static_cast<unsigned>(page_size)),
+      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), v_fp16));
 }
 
 // Per-step slot map for the fused append (K2 with k_new): out[t] = {prompt + pos,

@@ -190,6 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace(p, 6, 1);
+  // Every CTA of this grid is resident (one per SM, grid <= #SM): let the next
+  // PDL-launched kernel take each SM as soon as this CTA leaves it, so its prologue
+  // (and a K1's index math) fills this grid's tail.  Dependents read nothing this grid
+  // writes before their griddepcontrol.wait, which waits for this grid's completion.
+  if (!(p.dbg & 128)) grid_dep_launch();
   const uint32_t tm_s0 = tmem_base;           // S/P buffers
   const uint32_t tm_qt = tmem_base + L::TM_Q; // Q tile (MMA A operand)
   const uint32_t tm_o0 = tmem_base + L::TM_O; // O accumulators

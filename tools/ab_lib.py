@@ -26,6 +26,7 @@ ap.add_argument("--chunk", type=int, default=32)
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--tp", type=int, default=1, help="rank 0's KV-head shard of tp ranks")
 ap.add_argument("--rounds", type=int, default=12)
+ap.add_argument("--step", action="store_true", help="also A/B the whole device step (L x (K1, K2) + K3)")
 a = ap.parse_args()
 a.page, a.seed, a.steps = 64, 0, 1
 a.batch = a.batch or (128 if a.workload == "llada" else 64)
@@ -39,6 +40,7 @@ dm = dec.prepare(W.reqs, plans)
 m = dm.host
 k2b = bench.algorithmic_bytes(dm, cfg)[0]
 graphs = {}
+steps = {}
 for name, lib in (("A", lib_a), ("B", lib_b)):
     _lib._LIB = lib
     plan = ops.plan_attention(m.cu_seqlens, m.key_end, cfg.num_q_heads, cfg.num_kv_heads, grid=dec.grid,
@@ -66,6 +68,15 @@ for name, lib in (("A", lib_a), ("B", lib_b)):
     torch.cuda.synchronize()
     ref = out[: m.n_tok].clone()
     graphs[name] = (g, plan, ref)
+    if a.step:
+        gs = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            dec.device_step(dm)
+            s.synchronize()
+            with torch.cuda.graph(gs, stream=s):
+                dec.device_step(dm)
+        torch.cuda.synchronize()
+        steps[name] = gs
     print(f"{name}: work {plan.n_work} groups {plan.n_groups}", flush=True)
 _lib._LIB = lib_b
 d = (graphs["A"][2].float() - graphs["B"][2].float()).norm() / graphs["A"][2].float().norm()
@@ -80,6 +91,17 @@ for _ in range(a.rounds):
         e1.record()
         torch.cuda.synchronize()
         res[name].append(e0.elapsed_time(e1) * 1e3 / cfg.num_layers)
+st = {k: [] for k in steps}
+for _ in range(a.rounds):
+    for name, g in steps.items():
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        st[name].append(e0.elapsed_time(e1) * 1e3)
+for name, v in st.items():
+    v = np.array(v[2:])
+    print(f"{name}: whole step us median {np.median(v):8.1f} min {v.min():8.1f}")
 hbm, _ = bench.peaks()
 for name, v in res.items():
     v = np.array(v[2:])
