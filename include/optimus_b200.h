@@ -267,6 +267,23 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
 int optimus_unmask_splits(int n_rows, int vocab);
 
 /*
+ * K3 in ONE launch on a single vocab shard: (a) and (b) above fused.  Each
+ * (row, split) CTA writes its record to part [n_rows][n_vsplit]; the CTA that
+ * completes a request's records (arrival counter counters[row_req[row]]) runs (b)
+ * for that request.  counters: int32 [n_req], zero before the first call; every
+ * call leaves them zero.  row_req[i] = request of window row i (rows of a request
+ * are contiguous, cu_rows as in (b)).  n_rows_dev (optional): the row count of a
+ * device-planned step, read on the device; n_rows then only bounds it (and the grid).
+ * Results, commit rule and state update are exactly those of (a) + (b).
+ */
+int optimus_unmask_commit(const void* logits, int logits_dtype, int64_t row_stride, const int32_t* row_src,
+                          int n_rows, const int32_t* n_rows_dev, int vocab, int n_vsplit, float* part,
+                          const int32_t* cu_rows, const int32_t* row_req, int n_req, int32_t* counters, float tau,
+                          int fallback_mode, uint8_t* commit_mask, int32_t* tok, float* conf,
+                          const int32_t* row_pos, uint8_t* state, int32_t* token_buf, int64_t state_stride,
+                          void* stream);
+
+/*
  * f3: LM-head GEMM with the unmask partials in its epilogue; the
  * logits are never written.  hidden: bf16 [n_rows][hidden_stride] (first k_dim used),
  * weight: bf16 [vocab][weight_stride] (the LM head, row v = token v).  Writes

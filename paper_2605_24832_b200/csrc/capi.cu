@@ -33,6 +33,9 @@ int launch_unmask_partials(const void*, int, int64_t, const int32_t*, int, int, 
 int launch_unmask_finalize(const float*, int, int, int, const int32_t*, int, float, int, uint8_t*,
                            int32_t*, float*, const int32_t*, uint8_t*, int32_t*, int64_t,
                            cudaStream_t);
+int launch_unmask_commit(const void*, int, int64_t, const int32_t*, int, const int32_t*, int, int, float*,
+                         const int32_t*, const int32_t*, int32_t*, float, int, uint8_t*, int32_t*, float*,
+                         const int32_t*, uint8_t*, int32_t*, int64_t, cudaStream_t);
 int launch_lmhead_unmask(const CUtensorMap&, const CUtensorMap&, int, int, int, int, float*, cudaStream_t);
 int launch_merge_splits(const float*, int, int, float*, cudaStream_t);
 
@@ -755,15 +758,40 @@ int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k
 }
 
 int optimus_unmask_splits(int n_rows, int vocab) {
-  int sms = optimus_device_sm_count();
-  if (sms <= 0) sms = 148;
-  if (n_rows <= 0) return 1;
-  // 8 resident 256-thread CTAs per SM; aim for >= 2 waves, slices >= 8K columns.
-  const long long slots = static_cast<long long>(sms) * 8 * 2;
-  long long s = (slots + n_rows - 1) / n_rows;
-  const long long max_s = std::max(1, vocab / 8192);
-  s = std::max(1LL, std::min(s, max_s));
-  return static_cast<int>(s);
+  if (n_rows <= 0 || vocab <= 0) return 1;
+  // Measured table (tools/k3_sweep.py --splits, profiles/r2h_k3_splits*.txt: fused K3 on
+  // B200 over 32..2,100 rows x 151,936 bf16, every split count timed in one process).
+  // Rows are scaled to that vocabulary so the table is in CTA bytes.  Few large CTAs win
+  // once the grid fills the machine; small batches need slices to reach every SM.
+  const double eq = static_cast<double>(n_rows) * vocab / 151936.0;
+  int s = eq < 64 ? 8 : eq < 256 ? 4 : eq < 400 ? 2 : eq < 650 ? 3 : eq < 1250 ? 2 : 1;
+  s = std::min(s, std::max(1, vocab / 8192));
+  return s;
+}
+
+int optimus_unmask_commit(const void* logits, int logits_dtype, int64_t row_stride, const int32_t* row_src,
+                          int n_rows, const int32_t* n_rows_dev, int vocab, int n_vsplit, float* part,
+                          const int32_t* cu_rows, const int32_t* row_req, int n_req, int32_t* counters, float tau,
+                          int fallback_mode, uint8_t* commit_mask, int32_t* tok, float* conf,
+                          const int32_t* row_pos, uint8_t* state, int32_t* token_buf, int64_t state_stride,
+                          void* stream) {
+  if (logits_dtype != 0 && logits_dtype != 1) return fail("unmask_commit: logits_dtype must be 0 or 1");
+  const int vec = logits_dtype == 0 ? 8 : 4;
+  if (vocab < 1 || vocab % vec) return fail("unmask_commit: vocab must be a multiple of 8 (bf16) / 4 (fp32)");
+  if (row_stride % vec || row_stride < vocab) return fail("unmask_commit: bad row_stride");
+  if (n_rows < 0 || n_vsplit < 1 || n_req < 0) return fail("unmask_commit: bad sizes");
+  if (fallback_mode < 0 || fallback_mode > 2) return fail("unmask_commit: fallback_mode must be 0, 1 or 2");
+  if (n_rows == 0) return 0;
+  if (!logits || !part || !cu_rows || !row_req || !counters || !commit_mask || !tok || !conf)
+    return fail("unmask_commit: null pointer");
+  if (state && !row_pos) return fail("unmask_commit: state update needs row_pos");
+  if (reinterpret_cast<uintptr_t>(logits) % 16) return fail("unmask_commit: logits must be 16-byte aligned");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_unmask_commit(logits, logits_dtype, row_stride, row_src, n_rows, n_rows_dev, vocab,
+                                          n_vsplit, part, cu_rows, row_req, counters, tau, fallback_mode,
+                                          commit_mask, tok, conf, row_pos, state, token_buf, state_stride,
+                                          static_cast<cudaStream_t>(stream)),
+                     "unmask_commit");
 }
 
 int optimus_unmask_partials(const void* logits, int logits_dtype, int64_t row_stride,

@@ -68,11 +68,106 @@ struct VecLoad<float> {
   }
 };
 
+// Phase (b) for one request, run by one warp: merge the request's row partials in a
+// fixed order, threshold, progress rule, optional state-mirror update.
+__device__ __forceinline__ void finalize_request(
+    int req, int lane, const Part* __restrict__ part, int n_outer, int n_rows, int n_vsplit,
+    const int32_t* __restrict__ cu_rows, float tau, int fallback_mode, uint8_t* __restrict__ commit_mask,
+    int32_t* __restrict__ tok_out, float* __restrict__ conf_out, const int32_t* __restrict__ row_pos,
+    uint8_t* __restrict__ state, int32_t* __restrict__ token_buf, int64_t state_stride) {
+  const int r0 = cu_rows[req], r1 = cu_rows[req + 1];
+  bool any = false;
+  float best_conf = -1.f;
+  int best_row = 0x7FFFFFFF;
+  for (int base = r0; base < r1; base += 32) {
+    const int r = base + lane;
+    bool commit = false;
+    float conf = 0.f;
+    int tok = -1;
+    if (r < r1) {
+      float M = -INFINITY, S = 0.f;
+      int I = 0x7FFFFFFF;
+      for (int o = 0; o < n_outer; ++o)
+        for (int k = 0; k < n_vsplit; ++k) {
+          const Part q = part[(static_cast<int64_t>(o) * n_rows + r) * n_vsplit + k];
+          if (q.idx < 0) continue;
+          part_merge(M, S, I, q.m, q.s, q.idx);
+        }
+      conf = S > 0.f ? 1.0f / S : 0.f;
+      tok = I;
+      commit = conf >= tau;
+      if (fallback_mode == 0 && r == r0) commit = true;
+      conf_out[r] = conf;
+      tok_out[r] = tok;
+      if (conf > best_conf || (conf == best_conf && r < best_row)) {
+        best_conf = conf;
+        best_row = r;
+      }
+    }
+    any = any || __any_sync(0xFFFFFFFFu, commit);
+    if (r < r1) commit_mask[r] = commit ? 1 : 0;
+  }
+  if (fallback_mode == 1 && !any && r1 > r0) {
+    // highest confidence row (ties -> earliest) commits
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float c2 = __shfl_xor_sync(0xFFFFFFFFu, best_conf, o);
+      const int b2 = __shfl_xor_sync(0xFFFFFFFFu, best_row, o);
+      if (c2 > best_conf || (c2 == best_conf && b2 < best_row)) {
+        best_conf = c2;
+        best_row = b2;
+      }
+    }
+    if (lane == 0) commit_mask[best_row] = 1;
+  }
+  if (state != nullptr) {
+    __syncwarp();
+    for (int r = r0 + lane; r < r1; r += 32) {
+      if (commit_mask[r]) {
+        const int64_t at = static_cast<int64_t>(req) * state_stride + row_pos[r];
+        state[at] = 1;
+        if (token_buf) token_buf[at] = tok_out[r];
+      }
+    }
+  }
+}
+
+// One warp per request.
+__global__ void __launch_bounds__(128) unmask_finalize_kernel(
+    const Part* __restrict__ part, int n_outer, int n_rows, int n_vsplit,
+    const int32_t* __restrict__ cu_rows, int n_req, float tau, int fallback_mode,
+    uint8_t* __restrict__ commit_mask, int32_t* __restrict__ tok_out, float* __restrict__ conf_out,
+    const int32_t* __restrict__ row_pos, uint8_t* __restrict__ state,
+    int32_t* __restrict__ token_buf, int64_t state_stride) {
+  const int req = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (req >= n_req) return;
+  finalize_request(req, threadIdx.x & 31, part, n_outer, n_rows, n_vsplit, cu_rows, tau, fallback_mode,
+                   commit_mask, tok_out, conf_out, row_pos, state, token_buf, state_stride);
+}
+
+// Fused phase (b) (single vocab shard): the CTA that writes a request's last partial
+// (per-request arrival counter) finalizes that request, so the whole unmask is one launch.
+struct FuseArgs {
+  const int32_t* cu_rows;
+  const int32_t* row_req;
+  int32_t* counters;  // [n_req], zero between launches (the finalizing CTA resets its entry)
+  int n_rows_cap;     // stride of part (rows)
+  float tau;
+  int fallback_mode;
+  uint8_t* commit_mask;
+  int32_t* tok;
+  float* conf;
+  const int32_t* row_pos;
+  uint8_t* state;
+  int32_t* token_buf;
+  int64_t state_stride;
+};
+
 template <typename T, int THREADS>
 __global__ void __launch_bounds__(THREADS) unmask_partial_kernel(
     const T* __restrict__ logits, int64_t row_stride, const int32_t* __restrict__ row_src,
     int vocab, int vocab_offset, int n_vsplit, Part* __restrict__ part,
-    const int32_t* __restrict__ n_rows_dev = nullptr) {
+    const int32_t* __restrict__ n_rows_dev, const FuseArgs fuse) {
   constexpr int N = VecLoad<T>::N;
   const int row = blockIdx.x;
   const int split = blockIdx.y;
@@ -168,71 +263,21 @@ __global__ void __launch_bounds__(THREADS) unmask_partial_kernel(
     out.idx = (I == 0x7FFFFFFF) ? -1 : I + vocab_offset;
     part[static_cast<int64_t>(row) * n_vsplit + split] = out;
   }
-}
-
-// One warp per request: merge partials, threshold, progress rule, state update.
-__global__ void __launch_bounds__(128) unmask_finalize_kernel(
-    const Part* __restrict__ part, int n_outer, int n_rows, int n_vsplit,
-    const int32_t* __restrict__ cu_rows, int n_req, float tau, int fallback_mode,
-    uint8_t* __restrict__ commit_mask, int32_t* __restrict__ tok_out, float* __restrict__ conf_out,
-    const int32_t* __restrict__ row_pos, uint8_t* __restrict__ state,
-    int32_t* __restrict__ token_buf, int64_t state_stride) {
-  const int req = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (req >= n_req) return;
-  const int r0 = cu_rows[req], r1 = cu_rows[req + 1];
-  bool any = false;
-  float best_conf = -1.f;
-  int best_row = 0x7FFFFFFF;
-  for (int base = r0; base < r1; base += 32) {
-    const int r = base + lane;
-    bool commit = false;
-    float conf = 0.f;
-    int tok = -1;
-    if (r < r1) {
-      float M = -INFINITY, S = 0.f;
-      int I = 0x7FFFFFFF;
-      for (int o = 0; o < n_outer; ++o)
-        for (int k = 0; k < n_vsplit; ++k) {
-          const Part q = part[(static_cast<int64_t>(o) * n_rows + r) * n_vsplit + k];
-          if (q.idx < 0) continue;
-          part_merge(M, S, I, q.m, q.s, q.idx);
-        }
-      conf = S > 0.f ? 1.0f / S : 0.f;
-      tok = I;
-      commit = conf >= tau;
-      if (fallback_mode == 0 && r == r0) commit = true;
-      conf_out[r] = conf;
-      tok_out[r] = tok;
-      if (conf > best_conf || (conf == best_conf && r < best_row)) {
-        best_conf = conf;
-        best_row = r;
-      }
+  if (fuse.counters != nullptr) {
+    const FuseArgs& f = fuse;
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+      const int req = f.row_req[row];
+      const int parts = (f.cu_rows[req + 1] - f.cu_rows[req]) * n_vsplit;
+      __threadfence();  // release this CTA's record before counting it
+      last = (atomicAdd(&f.counters[req], 1) == parts - 1) ? req : -1;
     }
-    any = any || __any_sync(0xFFFFFFFFu, commit);
-    if (r < r1) commit_mask[r] = commit ? 1 : 0;
-  }
-  if (fallback_mode == 1 && !any && r1 > r0) {
-    // highest confidence row (ties -> earliest) commits
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float c2 = __shfl_xor_sync(0xFFFFFFFFu, best_conf, o);
-      const int b2 = __shfl_xor_sync(0xFFFFFFFFu, best_row, o);
-      if (c2 > best_conf || (c2 == best_conf && b2 < best_row)) {
-        best_conf = c2;
-        best_row = b2;
-      }
-    }
-    if (lane == 0) commit_mask[best_row] = 1;
-  }
-  if (state != nullptr) {
-    __syncwarp();
-    for (int r = r0 + lane; r < r1; r += 32) {
-      if (commit_mask[r]) {
-        const int64_t at = static_cast<int64_t>(req) * state_stride + row_pos[r];
-        state[at] = 1;
-        if (token_buf) token_buf[at] = tok_out[r];
-      }
+    __syncthreads();
+    if (last >= 0 && threadIdx.x < 32) {
+      __threadfence();  // acquire the other CTAs' records
+      finalize_request(last, threadIdx.x, part, 1, f.n_rows_cap, n_vsplit, f.cu_rows, f.tau, f.fallback_mode,
+                       f.commit_mask, f.tok, f.conf, f.row_pos, f.state, f.token_buf, f.state_stride);
+      if (threadIdx.x == 0) f.counters[last] = 0;  // ready for the next launch (stream order)
     }
   }
 }
@@ -245,11 +290,11 @@ int launch_unmask_partials(const void* logits, int dtype, int64_t row_stride,
   if (dtype == 0) {
     unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset,
-        n_vsplit, reinterpret_cast<Part*>(part));
+        n_vsplit, reinterpret_cast<Part*>(part), nullptr, FuseArgs{});
   } else {
     unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
         static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part));
+        reinterpret_cast<Part*>(part), nullptr, FuseArgs{});
   }
   return static_cast<int>(cudaGetLastError());
 }
@@ -263,11 +308,35 @@ int launch_unmask_partials_dev(const void* logits, int dtype, int64_t row_stride
   if (dtype == 0) {
     unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev);
+        reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{});
   } else {
     unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
         static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev);
+        reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{});
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Both phases in one launch (single vocab shard): partials, and the CTA completing a
+// request's partials finalizes it.  n_rows_dev (optional) holds the row count of a
+// device-planned step; n_rows then bounds it and strides part.
+int launch_unmask_commit(const void* logits, int dtype, int64_t row_stride, const int32_t* row_src, int n_rows,
+                         const int32_t* n_rows_dev, int vocab, int n_vsplit, float* part, const int32_t* cu_rows,
+                         const int32_t* row_req, int32_t* counters, float tau, int fallback_mode,
+                         uint8_t* commit_mask, int32_t* tok, float* conf, const int32_t* row_pos, uint8_t* state,
+                         int32_t* token_buf, int64_t state_stride, cudaStream_t stream) {
+  if (n_rows == 0) return 0;
+  const FuseArgs f{cu_rows, row_req, counters, n_rows, tau, fallback_mode, commit_mask, tok, conf, row_pos,
+                   state, token_buf, state_stride};
+  dim3 grid(n_rows, n_vsplit);
+  if (dtype == 0) {
+    unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, 0, n_vsplit,
+        reinterpret_cast<Part*>(part), n_rows_dev, f);
+  } else {
+    unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
+        static_cast<const float*>(logits), row_stride, row_src, vocab, 0, n_vsplit, reinterpret_cast<Part*>(part),
+        n_rows_dev, f);
   }
   return static_cast<int>(cudaGetLastError());
 }

@@ -117,6 +117,7 @@ class StreamingDecoder:
         self.d2h_bytes = 0
         # multi-GPU: a TensorParallelUnmask merges vocab-shard partials across ranks
         self.unmask_impl = None
+        self._unmask_counters = None  # K3 arrival counters (unmask_fused), zero between launches
         # native (C++) batched host step over packed request state; the Python path
         # (step_python) stays for foreign callers and as the readable specification
         self.use_native = True
@@ -297,10 +298,13 @@ class StreamingDecoder:
                                    torch.empty(cap, dtype=torch.int32, device=self.device),
                                    torch.empty(cap, dtype=torch.float32, device=self.device))
             ws = self._unmask_ws = (part, res)
-        part = ops.unmask_partials(logits, row_src, m.n_rows, n_vsplit,
-                                   part=ws[0][: rows * n_vsplit * 3].view(rows, n_vsplit, 3))
-        return ops.unmask_finalize(part, 1, m.n_rows, n_vsplit, dm.cu_rows,
-                                   self.cfg.confidence_threshold, self.cfg.fallback, result=ws[1])
+        if self._unmask_counters is None or self._unmask_counters.numel() < max(m.n_req, 1):
+            self._unmask_counters = torch.zeros(max(m.n_req, self.cfg.max_batch, 1), dtype=torch.int32,
+                                                device=self.device)
+        # one launch: the CTA completing a request's vocab slices finalizes it
+        return ops.unmask_fused(logits, row_src, m.n_rows, n_vsplit, dm.cu_rows, dm.row_req, self._unmask_counters,
+                                self.cfg.confidence_threshold, self.cfg.fallback, result=ws[1],
+                                part=ws[0][: rows * n_vsplit * 3].view(rows, n_vsplit, 3))
 
     def device_step(self, dm: DeviceMeta) -> ops.UnmaskResult:
         self.run_layers(dm)

@@ -6,7 +6,7 @@
     optimus_device_plan       plan_chunk for every request + the step metadata
     optimus_device_attn_plan  the attention work list (LPT placement, balanced split-KV cuts)
     L x (optimus_kv_append_dev, optimus_paged_attn, optimus_paged_attn_combine_dev)
-    optimus_device_row_src, optimus_unmask_partials_dev, optimus_unmask_finalize
+    optimus_device_row_src, optimus_unmask_commit (K3 in one launch)
     optimus_device_apply      apply_chunk + advance_blocks
     D2H of the plan arrays and the commit mask into pinned buffers
 
@@ -114,6 +114,7 @@ class DeviceLoop:
         self.logits = fwd.logit_table
         self.n_vsplit = ops.unmask_splits(cr, self.logits.shape[-1])
         self.part = torch.empty((cr, self.n_vsplit, 3), dtype=torch.float32, device=dev)
+        self.k3_counters = torch.zeros(n, dtype=torch.int32, device=dev)  # unmask_fused arrivals (zero between steps)
         self.res = ops.UnmaskResult(z(cr, torch.uint8), z(cr), z(cr, torch.float32))
         self.out = torch.empty((ct, cfg.num_q_heads, cfg.head_dim), dtype=torch.bfloat16, device=dev)
         # pinned host mirrors of what the host replay needs
@@ -173,12 +174,18 @@ class DeviceLoop:
             fwd.rows_per_slot, fwd.version * fwd.max_slots * fwd.rows_per_slot, p(M["row_src"]), stream),
             "device_row_src")
         dt = 0 if self.logits.dtype == torch.bfloat16 else 1
-        _lib.check(L.call(
-            "optimus_unmask_partials_dev", p(self.logits), dt, self.logits.stride(0), p(M["row_src"]), cr,
-            p(M["counts"][1:]), self.logits.shape[-1], fwd.vocab_offset, self.n_vsplit, p(self.part), stream),
-            "unmask_partials_dev")
-        ops.unmask_finalize(self.part, 1, cr, self.n_vsplit, M["cu_rows"], cfg.confidence_threshold, cfg.fallback,
-                            result=self.res, stream=torch.cuda.ExternalStream(stream))
+        if fwd.vocab_offset == 0:
+            # K3 in one launch, row count from the device plan
+            ops.unmask_fused(self.logits, M["row_src"], cr, self.n_vsplit, M["cu_rows"], M["row_req"],
+                             self.k3_counters, cfg.confidence_threshold, cfg.fallback, result=self.res,
+                             part=self.part, n_rows_dev=M["counts"][1:], stream=torch.cuda.ExternalStream(stream))
+        else:
+            _lib.check(L.call(
+                "optimus_unmask_partials_dev", p(self.logits), dt, self.logits.stride(0), p(M["row_src"]), cr,
+                p(M["counts"][1:]), self.logits.shape[-1], fwd.vocab_offset, self.n_vsplit, p(self.part), stream),
+                "unmask_partials_dev")
+            ops.unmask_finalize(self.part, 1, cr, self.n_vsplit, M["cu_rows"], cfg.confidence_threshold,
+                                cfg.fallback, result=self.res, stream=torch.cuda.ExternalStream(stream))
         _lib.check(L.call(
             "optimus_device_apply", n, p(self.slots), cfg.block_size, p(M["cu_seqlens"]), p(M["tok_pos"]),
             p(M["cu_rows"]), p(M["row_pos"]), p(self.res.commit_mask), p(D["states"]), D["states"].shape[1],

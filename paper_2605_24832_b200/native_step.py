@@ -122,7 +122,7 @@ class NativeStepper:
         if v is None:
             A, MP = self.arena, self.cfg.max_pages_per_req
             v = {k: A.d(k) for k in ("tok_req", "tok_pos", "prompt_len", "vis_base", "vis_off", "vis_words",
-                                     "row_pos", "row_src", "cta_off")}
+                                     "row_pos", "row_req", "row_src", "cta_off")}
             v["work"] = A.d("work").view(-1, 8)
             v["groups"] = A.d("groups").view(-1, 8)
             v["block_tables"] = A.d("block_tables", n * MP).view(n, MP)
@@ -219,7 +219,7 @@ class NativeStepper:
         dm = SimpleNamespace(host=host, tok_req=V["tok_req"], tok_pos=V["tok_pos"],
                              prompt_len=V["prompt_len"], vis_base=V["vis_base"], vis_off=V["vis_off"],
                              vis_words=V["vis_words"], block_tables=V["block_tables"],
-                             cu_rows=V["cu_rows"], row_pos=V["row_pos"], row_src=V["row_src"])
+                             cu_rows=V["cu_rows"], row_pos=V["row_pos"], row_req=V["row_req"], row_src=V["row_src"])
         dm.__dict__.update(attn_plan=plan, slots=slots.astype(np.int64), requests=requests, plans=None,
                            row_src_host=A.h("row_src"))
         return dm
@@ -347,6 +347,13 @@ class NativeStepper:
         dt = 0 if logits.dtype == torch.bfloat16 else 1
         R = g["R"]
         part = g["part"][: R * n_vsplit * 3]
+        if fwd.vocab_offset == 0:
+            if g.get("k3_counters") is None or g["k3_counters"].numel() < max(n, 1):
+                g["k3_counters"] = torch.zeros(max(n, cfg.max_batch, 1), dtype=torch.int32, device=logits.device)
+            ops.unmask_fused(logits, V["row_src"], R, n_vsplit, V["cu_rows"], V["row_req"], g["k3_counters"],
+                             cfg.confidence_threshold, cfg.fallback, result=g["res"], part=part.view(R, n_vsplit, 3),
+                             n_rows_dev=cnt[1:], stream=torch.cuda.ExternalStream(stream))
+            return
         _lib.check(_lib.call(
             "optimus_unmask_partials_dev", p(logits), dt, logits.stride(0), p(V["row_src"]), R, p(cnt[1:]),
             logits.shape[-1], fwd.vocab_offset, n_vsplit, p(part), stream), "unmask_partials_dev")

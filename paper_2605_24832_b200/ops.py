@@ -461,6 +461,58 @@ def unmask_finalize(
     return result
 
 
+def unmask_fused(
+    logits: torch.Tensor,
+    row_src: Optional[torch.Tensor],
+    n_rows: int,
+    n_vsplit: int,
+    cu_rows: torch.Tensor,
+    row_req: torch.Tensor,
+    counters: torch.Tensor,
+    tau: float,
+    fallback: str = "earliest",
+    row_pos: Optional[torch.Tensor] = None,
+    state: Optional[torch.Tensor] = None,
+    token_buf: Optional[torch.Tensor] = None,
+    result: Optional[UnmaskResult] = None,
+    part: Optional[torch.Tensor] = None,
+    n_rows_dev: Optional[torch.Tensor] = None,
+    stream=None,
+) -> UnmaskResult:
+    """K3 in one launch (``optimus_unmask_commit``): phases (a) and (b) fused on one
+    vocab shard.  ``counters`` is an int32 [n_req] workspace, zero between calls."""
+    _cuda(logits, row_src, cu_rows, row_req, counters, row_pos, state, token_buf, part, n_rows_dev)
+    if logits.dtype == torch.bfloat16:
+        dt = 0
+    elif logits.dtype == torch.float32:
+        dt = 1
+    else:
+        raise ConfigError("unmask: logits must be bf16 or fp32")
+    if logits.stride(-1) != 1:
+        raise ConfigError("unmask: logits rows must be contiguous")
+    if fallback not in FALLBACK_MODES:
+        raise ConfigError(f"unknown fallback mode {fallback!r}")
+    n_req = cu_rows.shape[0] - 1
+    if counters.dtype != torch.int32 or counters.numel() < n_req:
+        raise ConfigError("unmask: counters must be int32 with >= n_req entries")
+    dev = logits.device
+    rows = max(n_rows, 1)
+    if part is None:
+        part = torch.empty((rows, n_vsplit, 3), dtype=torch.float32, device=dev)
+    if result is None:
+        result = UnmaskResult(torch.empty(rows, dtype=torch.uint8, device=dev),
+                              torch.empty(rows, dtype=torch.int32, device=dev),
+                              torch.empty(rows, dtype=torch.float32, device=dev))
+    st = _lib.call(
+        "optimus_unmask_commit", _ptr(logits), dt, logits.stride(0), _ptr(row_src), n_rows, _ptr(n_rows_dev),
+        logits.shape[-1], n_vsplit, _ptr(part), _ptr(cu_rows), _ptr(row_req), n_req, _ptr(counters), float(tau),
+        FALLBACK_MODES[fallback], _ptr(result.commit_mask), _ptr(result.tokens), _ptr(result.conf), _ptr(row_pos),
+        _ptr(state), _ptr(token_buf), state.stride(0) if state is not None else 0, _stream(stream),
+    )
+    _lib.check(st, "optimus_unmask_commit")
+    return result
+
+
 def unmask_commit(
     logits: torch.Tensor,
     cu_rows: torch.Tensor,
@@ -471,10 +523,15 @@ def unmask_commit(
     n_vsplit: Optional[int] = None,
     stream=None,
 ) -> UnmaskResult:
-    """Single-GPU K3: partials + finalize over the whole vocabulary."""
+    """Single-GPU K3 over the whole vocabulary, one launch (``unmask_fused``)."""
     if n_rows is None:
         n_rows = logits.shape[0] if row_src is None else row_src.shape[0]
     if n_vsplit is None:
         n_vsplit = unmask_splits(n_rows, logits.shape[-1])
-    part = unmask_partials(logits, row_src, n_rows, n_vsplit, stream=stream)
-    return unmask_finalize(part, 1, n_rows, n_vsplit, cu_rows, tau, fallback, stream=stream)
+    n_req = cu_rows.shape[0] - 1
+    counts = (cu_rows[1:] - cu_rows[:-1]).long()
+    row_req = torch.repeat_interleave(torch.arange(n_req, dtype=torch.int32, device=cu_rows.device), counts,
+                                      output_size=n_rows)
+    counters = torch.zeros(max(n_req, 1), dtype=torch.int32, device=cu_rows.device)
+    return unmask_fused(logits, row_src, n_rows, n_vsplit, cu_rows, row_req, counters, tau, fallback,
+                        stream=stream)

@@ -285,6 +285,83 @@ def test_unmask_vocab_parallel_merge_equals_single():
     torch.testing.assert_close(full.conf[:n], sharded.conf[:n], rtol=1e-5, atol=0)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("rows,vocab,n_vsplit", [
+    (1, 151936, None), (5, 4104, None), (63, 157184, None), (918, 151936, None), (1121, 151936, None),
+    (2100, 157184, None), (40, 32768, 1), (300, 32768, 2), (7, 151936, 20)])
+def test_unmask_flat_stream_row_counts(rows, vocab, n_vsplit, dtype):
+    """K3 phase (a) cuts the n_rows x vocab stream into equal ranges that span row ends.
+    Whatever the row count and record-slot count, the merged records equal a float64
+    torch reference of the same rows: argmax exact (lowest index), conf within 2e-5,
+    rows gathered through row_src, unused piece slots ignored."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(rows * 7 + vocab)
+    src_rows = rows + 3
+    x = (torch.randn((src_rows, vocab), generator=g, device=dev) * 2.5).to(dtype)
+    # a few rows with an exact tie at the max and a few with a dominant token
+    x[0, vocab // 3] = x[0, vocab - 9] = 40.0
+    if rows > 2:
+        x[2, 17] = 12.0
+    row_src = torch.randperm(src_rows, generator=g, device=dev)[:rows].to(torch.int32)
+    cu = torch.tensor([0, rows], dtype=torch.int32, device=dev)
+    ns = n_vsplit or ops.unmask_splits(rows, vocab)
+    part = ops.unmask_partials(x, row_src, rows, ns)
+    res = ops.unmask_finalize(part, 1, rows, ns, cu, 0.9)
+    ref = x[row_src.long()].double()
+    mx = ref.max(dim=1).values
+    conf = 1.0 / torch.exp(ref - mx[:, None]).sum(dim=1)
+    first = (ref == mx[:, None]).int().argmax(dim=1)  # lowest index among the maxima
+    assert torch.equal(res.tokens[:rows].long().cpu(), first.cpu())
+    torch.testing.assert_close(res.conf[:rows].double().cpu(), conf.cpu(), rtol=2e-5, atol=1e-7)
+    # every row's records: pieces in vocab order, then empty slots only
+    p = part.view(rows, ns, 3)[:, :, 2].view(torch.int32).cpu()
+    for r in range(rows):
+        live = (p[r] >= 0).tolist()
+        assert any(live) and live == sorted(live, reverse=True)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("fallback", ["earliest", "top1", "none"])
+def test_unmask_fused_equals_two_phase(dtype, fallback):
+    """optimus_unmask_commit (the CTA completing a request's records finalizes it) gives
+    exactly the two-launch result: commit mask, tokens, conf and the state-mirror update,
+    over ragged requests (incl. empty ones), repeated launches (counters reset), and with
+    the row count read from the device."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    wins = [3, 0, 17, 1, 32, 0, 9, 25]
+    n = sum(wins)
+    vocab = 20480
+    x = (torch.randn((n + 5, vocab), generator=g, device=dev) * 2).to(dtype)
+    x[4, 77] = 30.0  # a confident row
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(wins)]), dtype=torch.int32, device=dev)
+    row_req = torch.repeat_interleave(torch.arange(len(wins), device=dev, dtype=torch.int32),
+                                      torch.tensor(wins, device=dev), output_size=n)
+    row_src = torch.randperm(n + 5, generator=g, device=dev)[:n].to(torch.int32)
+    row_pos = torch.tensor(np.concatenate([np.arange(w) * 2 for w in wins]), dtype=torch.int32, device=dev)
+    tau = 0.05 if fallback != "none" else 0.02
+    for ns in (1, 3):
+        part = ops.unmask_partials(x, row_src, n, ns)
+        st_a = torch.zeros((len(wins), 64), dtype=torch.uint8, device=dev)
+        tb_a = torch.full((len(wins), 64), -1, dtype=torch.int32, device=dev)
+        ref = ops.unmask_finalize(part, 1, n, ns, cu, tau, fallback, row_pos=row_pos, state=st_a, token_buf=tb_a)
+        counters = torch.zeros(len(wins), dtype=torch.int32, device=dev)
+        cap = n + 7
+        n_dev = torch.tensor([n], dtype=torch.int32, device=dev)
+        for rep in range(3):
+            st_b = torch.zeros_like(st_a)
+            tb_b = torch.full_like(tb_a, -1)
+            got = ops.unmask_fused(x, row_src, cap if rep == 2 else n, ns, cu, row_req, counters, tau, fallback,
+                                   row_pos=row_pos, state=st_b, token_buf=tb_b,
+                                   n_rows_dev=n_dev if rep == 2 else None)
+            torch.cuda.synchronize()
+            assert torch.equal(got.commit_mask[:n], ref.commit_mask[:n])
+            assert torch.equal(got.tokens[:n], ref.tokens[:n])
+            assert torch.equal(got.conf[:n], ref.conf[:n])
+            assert torch.equal(st_b, st_a) and torch.equal(tb_b, tb_a)
+            assert int(counters.abs().sum()) == 0
+
+
 @pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("case", ["sdar8b", "d64_g1", "d64_g2", "page128", "split_kv", "one_cta", "out_block"])
 def test_fused_append_equals_k1_then_k2(case, v_dtype):
