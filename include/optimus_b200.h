@@ -227,8 +227,8 @@ int optimus_unmask_partials(const void* logits, int logits_dtype, int64_t row_st
  *                       commits (ties -> earliest);
  *       fallback_mode 2 ("none"): threshold only (a step may commit nothing,
  *                       as a ReplayOracle step can, commit.py:254-267).
- *     Optional state mirror update (pass NULL to skip): for committed row i of
- *     request r at output position row_pos[i]:
+ *     Optional state mirror / token update (pass NULL to skip either): for
+ *     committed row i of request r at output position row_pos[i]:
  *       state[r*state_stride + pos] = 1 (DECODED_UNCACHED), token_buf[same] = tok.
  */
 int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vsplit,

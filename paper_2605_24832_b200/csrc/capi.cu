@@ -784,7 +784,7 @@ int optimus_unmask_commit(const void* logits, int logits_dtype, int64_t row_stri
   if (n_rows == 0) return 0;
   if (!logits || !part || !cu_rows || !row_req || !counters || !commit_mask || !tok || !conf)
     return fail("unmask_commit: null pointer");
-  if (state && !row_pos) return fail("unmask_commit: state update needs row_pos");
+  if ((state || token_buf) && !row_pos) return fail("unmask_commit: state / token update needs row_pos");
   if (reinterpret_cast<uintptr_t>(logits) % 16) return fail("unmask_commit: logits must be 16-byte aligned");
   if (int st = check_device()) return st;
   return cuda_status(launch_unmask_commit(logits, logits_dtype, row_stride, row_src, n_rows, n_rows_dev, vocab,
@@ -821,7 +821,7 @@ int optimus_unmask_finalize(const float* part, int n_outer, int n_rows, int n_vs
   if (fallback_mode < 0 || fallback_mode > 2) return fail("unmask: fallback_mode must be 0, 1 or 2");
   if (n_req == 0) return 0;
   if (!part || !cu_rows || !commit_mask || !tok || !conf) return fail("unmask: null pointer");
-  if (state && !row_pos) return fail("unmask: state update needs row_pos");
+  if ((state || token_buf) && !row_pos) return fail("unmask: state / token update needs row_pos");
   if (int st = check_device()) return st;
   return cuda_status(
       launch_unmask_finalize(part, n_outer, n_rows, n_vsplit, cu_rows, n_req, tau, fallback_mode,

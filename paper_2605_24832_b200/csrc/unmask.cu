@@ -120,12 +120,12 @@ __device__ __forceinline__ void finalize_request(
     }
     if (lane == 0) commit_mask[best_row] = 1;
   }
-  if (state != nullptr) {
+  if (state != nullptr || token_buf != nullptr) {
     __syncwarp();
     for (int r = r0 + lane; r < r1; r += 32) {
       if (commit_mask[r]) {
         const int64_t at = static_cast<int64_t>(req) * state_stride + row_pos[r];
-        state[at] = 1;
+        if (state) state[at] = 1;
         if (token_buf) token_buf[at] = tok_out[r];
       }
     }

@@ -15,7 +15,13 @@ so no host round trip sits between steps.  The host keeps the reference-facing
 ``optimus_host_apply`` from the copied plan (bit-identical to the device's; see
 tests/test_device_loop_gpu.py, which also checks the whole loop against the host
 native step).  The batch is fixed for the loop's lifetime (finished requests plan
-zero tokens); every request's pages are allocated up front.
+zero tokens, ``replace`` refills a finished position); every request's pages are
+allocated up front.
+
+The chunk is elastic: the device plan always reads a per-position chunk array, so
+``step(chunk=c)`` / ``set_chunk`` change it between iterations without a re-capture
+(one chunk for the batch, as ElasticChunk picks it every iteration, sim.py:219-232,
+270-272, or one per position).  Capacities are sized for ``max_chunk``.
 """
 
 from __future__ import annotations
@@ -40,11 +46,16 @@ class DeviceLoop:
             raise ConfigError(f"DeviceLoop: request {r.id} has {r.output_tokens} output tokens > "
                               f"{min(cls.MAX_OUT, nat.bs.states.shape[1])}")
 
-    def __init__(self, decoder, requests, chunk: int, lookahead: bool = False):
+    def __init__(self, decoder, requests, chunk, lookahead: bool = False, max_chunk: int = None):
         cfg = decoder.cfg
-        if not getattr(decoder.forward, "resident_layers", False) or not hasattr(decoder.forward, "row_src_host"):
-            raise ConfigError("DeviceLoop needs a forward with resident per-layer activations and a slot-indexed "
-                              "logits table (SyntheticForward)")
+        fwd = decoder.forward
+        # two kinds of forward: a model with loop hooks (loop_setup / loop_begin / loop_qkv /
+        # loop_post_attn / loop_unmask, capacity-shaped and graph-capturable: TinyDLLM), or
+        # resident per-layer activations with a slot-indexed logits table (SyntheticForward)
+        self.model = bool(getattr(fwd, "loop_model", False))
+        if not self.model and (not getattr(fwd, "resident_layers", False) or not hasattr(fwd, "row_src_host")):
+            raise ConfigError("DeviceLoop needs a forward with loop hooks (loop_model) or resident per-layer "
+                              "activations and a slot-indexed logits table (SyntheticForward)")
         self.dec, self.cfg = decoder, cfg
         # one chunk for the batch, or one per loop position (mixed chunks, the elastic
         # scheduler's per-request sizes); capacities follow the largest
@@ -52,7 +63,8 @@ class DeviceLoop:
         self.chunk_h = np.asarray(chunk if mixed else [chunk] * len(requests), dtype=np.int32)
         if len(self.chunk_h) != len(requests) or self.chunk_h.min() < 2:
             raise ConfigError("DeviceLoop: one chunk >= 2 per request")
-        self.chunk = int(self.chunk_h.max())
+        # capacity chunk: the largest chunk any later iteration may ask for
+        self.chunk = max(int(self.chunk_h.max()), int(max_chunk or 0))
         nat = decoder.native()
         # the device planners' hard limits (csrc/device_step.cu): checked here so a
         # captured graph never runs a step they would reject
@@ -85,7 +97,10 @@ class DeviceLoop:
         self.D = {k: torch.from_numpy(np.ascontiguousarray(getattr(bs, k))).to(dev) for k in self.state_keys}
         self.Dt = torch.from_numpy(np.ascontiguousarray(decoder.tables.table)).to(dev)
         self.slots = torch.from_numpy(self.slots_h).to(dev)
-        self.chunks_d = torch.from_numpy(self.chunk_h).to(dev) if mixed else None
+        # per-position chunks, read by the device plan every replay (elastic chunk)
+        self.chunks_d = torch.from_numpy(self.chunk_h).to(dev)
+        self._chunks_pin = torch.from_numpy(self.chunk_h.copy()).pin_memory()
+        self._chunks_ev = None  # the last staging copy (the pinned buffer is reused)
         ct = n * self.chunk
         cr = n * min(self.chunk, cfg.block_size)
         cw = n * (bs.states.shape[1] // 32 + 4)
@@ -110,9 +125,10 @@ class DeviceLoop:
         self.ws_ml = torch.empty(self.max_work * 128 * 2, dtype=torch.float32, device=dev)
         M["wcounts"] = z(4)
         self.M = M
-        fwd = decoder.forward
-        self.logits = fwd.logit_table
-        self.n_vsplit = ops.unmask_splits(cr, self.logits.shape[-1])
+        vocab = cfg.vocab if self.model else fwd.logit_table.shape[-1]
+        self.logits = None if self.model else fwd.logit_table
+        # vocab slices for about half the row capacity (window rows vary step to step)
+        self.n_vsplit = ops.unmask_splits(max(cr // 2, 1), vocab)
         self.part = torch.empty((cr, self.n_vsplit, 3), dtype=torch.float32, device=dev)
         self.k3_counters = torch.zeros(n, dtype=torch.int32, device=dev)  # unmask_fused arrivals (zero between steps)
         self.res = ops.UnmaskResult(z(cr, torch.uint8), z(cr), z(cr, torch.float32))
@@ -127,6 +143,9 @@ class DeviceLoop:
         self.lookahead = bool(lookahead)
         self._inflight = False  # a lookahead iteration was launched and not yet consumed
         self._stale = set()  # positions refilled while an iteration was in flight
+        self._last = (np.zeros(n + 1, np.int32), np.zeros(1, np.int32), np.zeros(1, np.uint8))
+        if self.model:
+            fwd.loop_setup(self)
 
     # ------------------------------------------------------------------ device
     def _enqueue(self, stream) -> None:
@@ -136,8 +155,8 @@ class DeviceLoop:
         L = _lib
         rule = 0 if rule_value(cfg.window_rule) == "in_block" else 1
         _lib.check(L.call(
-            "optimus_device_plan", n, p(self.slots), self.chunk,
-            p(self.chunks_d) if self.chunks_d is not None else None, cfg.block_size, rule, p(D["states"]),
+            "optimus_device_plan", n, p(self.slots), self.chunk, p(self.chunks_d), cfg.block_size, rule,
+            p(D["states"]),
             D["states"].shape[1], p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]),
             p(D["cached_prefix"]), p(D["prompt"]), p(D["out_len"]), p(self.Dt), self.Dt.shape[1],
             p(M["cu_seqlens"]), p(M["tok_req"]), p(M["tok_pos"]), ct, p(M["prompt_len"]), p(M["key_end"]),
@@ -150,17 +169,24 @@ class DeviceLoop:
         fwd = self.dec.forward
         scale = 1.0 / float(cfg.head_dim) ** 0.5
         v_dtype = ops._v_dtype(self.dec.cache.v)
+        if self.model:
+            fwd.loop_begin(self, M)
         for layer in range(cfg.num_layers):
-            q, k, v = fwd.qkv_buf[layer][:, : cfg.num_q_heads], None, None
-            buf = fwd.qkv_buf[layer]
             hq, hkv = cfg.num_q_heads, cfg.num_kv_heads
+            if self.model:
+                q, k, v = fwd.loop_qkv(self, layer, M)  # capacity rows, bf16, unit inner strides
+                if k.stride(0) != v.stride(0):
+                    raise ConfigError("DeviceLoop: the model's K and V rows must share a row stride")
+            else:
+                buf = fwd.qkv_buf[layer]
+                q, k, v = buf, buf[:, hq], buf[:, hq + hkv]
             kc, vc = self.dec.cache.layer(layer)
             _lib.check(L.call(
-                "optimus_kv_append_dev", p(buf[:, hq]), p(buf[:, hq + hkv]), buf.stride(0), p(M["tok_req"]),
+                "optimus_kv_append_dev", p(k), p(v), k.stride(0), p(M["tok_req"]),
                 p(M["tok_pos"]), p(M["prompt_len"]), p(M["block_tables"]), M["block_tables"].shape[1], ct,
                 p(M["counts"]), hkv, cfg.head_dim, cfg.page_size, p(kc), p(vc), v_dtype, stream), "kv_append_dev")
             _lib.check(L.call(
-                "optimus_paged_attn", p(buf), buf.stride(0), buf.shape[0], p(kc), p(vc), kc.shape[0],
+                "optimus_paged_attn", p(q), q.stride(0), q.shape[0], p(kc), p(vc), kc.shape[0],
                 p(M["tok_pos"]), p(M["prompt_len"]), p(M["vis_base"]), p(M["vis_off"]), p(M["vis_words"]),
                 p(M["block_tables"]), M["block_tables"].shape[1], p(M["work"]), p(M["cta_off"]), self.grid,
                 p(M["groups"]), 0, cfg.block_size, hq, hkv, cfg.head_dim, cfg.page_size, scale, p(self.out),
@@ -169,6 +195,26 @@ class DeviceLoop:
                 "optimus_paged_attn_combine_dev", p(M["groups"]), p(M["wcounts"][1:]), M["groups"].shape[0],
                 p(self.ws_o), p(self.ws_ml), hq, hkv, cfg.head_dim, p(self.out), self.out.stride(0), stream),
                 "paged_attn_combine_dev")
+            if self.model:
+                fwd.loop_post_attn(self, layer, self.out, M)
+        if self.model:
+            fwd.loop_unmask(self, M)  # LM head on the window rows -> K3 into self.res
+        else:
+            self._unmask_synthetic(M, stream)
+        _lib.check(L.call(
+            "optimus_device_apply", n, p(self.slots), cfg.block_size, p(M["cu_seqlens"]), p(M["tok_pos"]),
+            p(M["cu_rows"]), p(M["row_pos"]), p(self.res.commit_mask), p(D["states"]), D["states"].shape[1],
+            p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
+            p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["counts"][3:]),
+            stream), "device_apply")  # apply's status = the plan's counts[3]: a rejected plan skips apply
+        for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
+            self.H[k].copy_(M[k], non_blocking=True)
+        self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
+
+    def _unmask_synthetic(self, M, stream) -> None:
+        cfg, fwd, cr = self.cfg, self.dec.forward, self.caps[1]
+        p = lambda t: t.data_ptr()
+        L = _lib
         _lib.check(L.call(
             "optimus_device_row_src", p(M["counts"]), p(self.slots), p(M["cu_rows"]), p(M["row_req"]), cr,
             fwd.rows_per_slot, fwd.version * fwd.max_slots * fwd.rows_per_slot, p(M["row_src"]), stream),
@@ -186,15 +232,6 @@ class DeviceLoop:
                 "unmask_partials_dev")
             ops.unmask_finalize(self.part, 1, cr, self.n_vsplit, M["cu_rows"], cfg.confidence_threshold,
                                 cfg.fallback, result=self.res, stream=torch.cuda.ExternalStream(stream))
-        _lib.check(L.call(
-            "optimus_device_apply", n, p(self.slots), cfg.block_size, p(M["cu_seqlens"]), p(M["tok_pos"]),
-            p(M["cu_rows"]), p(M["row_pos"]), p(self.res.commit_mask), p(D["states"]), D["states"].shape[1],
-            p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
-            p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["counts"][3:]),
-            stream), "device_apply")  # apply's status = the plan's counts[3]: a rejected plan skips apply
-        for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
-            self.H[k].copy_(M[k], non_blocking=True)
-        self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
 
     def capture(self) -> None:
         s = torch.cuda.Stream(device=self.dev)
@@ -214,16 +251,39 @@ class DeviceLoop:
         torch.cuda.synchronize()
 
     # ------------------------------------------------------------------ host
-    def step(self, summaries: bool = True):
+    def set_chunk(self, chunk) -> None:
+        """Chunk size(s) for the next launched iteration: one int for the batch (the
+        elastic scheduler's per-iteration choice) or one per loop position.  Stream-
+        ordered before the next replay; no re-capture."""
+        c = np.asarray(chunk if np.ndim(chunk) else [chunk] * self.n, dtype=np.int32)
+        if c.shape != (self.n,) or c.min() < 2 or c.max() > self.chunk:
+            raise ConfigError(f"DeviceLoop.set_chunk: chunks must be in [2, {self.chunk}] (the capacity chunk), "
+                              f"one per position")
+        if np.array_equal(c, self.chunk_h):
+            return
+        if self._chunks_ev is not None:
+            self._chunks_ev.synchronize()  # the previous staging copy has read the pinned buffer
+        self._chunks_pin.numpy()[:] = c
+        self.chunks_d.copy_(self._chunks_pin, non_blocking=True)
+        self._chunks_ev = torch.cuda.Event()
+        self._chunks_ev.record()
+        self.chunk_h = c
+
+    def step(self, summaries: bool = True, chunk=None):
         """One iteration: replay the graph, then replay the same transitions on the
         host mirror (Request objects) from the copied plan and commit mask.
 
+        ``chunk`` (optional) sets the chunk size(s) first (``set_chunk``).
+
         With ``lookahead`` the next iteration's graph is launched before the host
         apply of this one (the device state is already advanced), so the host work
-        overlaps the GPU; a request admitted by ``replace`` then enters one
-        iteration later (the in-flight iteration planned nothing for its position)."""
+        overlaps the GPU; a request admitted by ``replace`` — and a chunk given here —
+        then takes effect one iteration later (the in-flight iteration was planned
+        with the previous state)."""
         if self.graph is None:
             self.capture()
+        if chunk is not None:
+            self.set_chunk(chunk)
         t0 = time.perf_counter()
         if not self._inflight:
             self.graph.replay()
@@ -265,6 +325,7 @@ class DeviceLoop:
             bp["queue"], bs.qcap, bp["q_head"], bp["q_len"], bp["block_index"], bp["committed"],
             bp["steps_taken"], bp["cached_prefix"], bp["out_len"], commits.ctypes.data)
         _lib.check(st, "optimus_host_apply")
+        self._last = (cur, row_pos, mask)
         for i, r in enumerate(self.requests):  # finished: release pages and slot (it plans nothing)
             if i not in self.free and r.finished:
                 self.nat.release(r)
@@ -276,6 +337,18 @@ class DeviceLoop:
             a, b = int(cur[r]), int(cur[r + 1])
             out.append(StepSummary(computed=int(cu[r + 1] - cu[r]),
                                    commits=frozenset(row_pos[a:b][mask[a:b].astype(bool)].tolist())))
+        return out
+
+    def window_observations(self) -> list:
+        """(window size, committed window ranks) of every position that had a window in
+        the last iteration, in position order: what ElasticChunk's estimator folds in
+        per request-step (sim.py:289-293, ``CommitEstimator.observe``)."""
+        cur, row_pos, mask = self._last
+        out = []
+        for r in range(self.n):
+            a, b = int(cur[r]), int(cur[r + 1])
+            if b > a:
+                out.append((b - a, set(np.flatnonzero(mask[a:b]).tolist())))
         return out
 
     def drain(self) -> None:

@@ -455,7 +455,7 @@ def unmask_finalize(
         "optimus_unmask_finalize", _ptr(part), n_outer, n_rows, n_vsplit, _ptr(cu_rows), n_req,
         float(tau), FALLBACK_MODES[fallback], _ptr(result.commit_mask), _ptr(result.tokens),
         _ptr(result.conf), _ptr(row_pos), _ptr(state), _ptr(token_buf),
-        state.stride(0) if state is not None else 0, _stream(stream),
+        (state if state is not None else token_buf).stride(0) if (state is not None or token_buf is not None) else 0, _stream(stream),
     )
     _lib.check(st, "optimus_unmask_finalize")
     return result
@@ -507,7 +507,7 @@ def unmask_fused(
         "optimus_unmask_commit", _ptr(logits), dt, logits.stride(0), _ptr(row_src), n_rows, _ptr(n_rows_dev),
         logits.shape[-1], n_vsplit, _ptr(part), _ptr(cu_rows), _ptr(row_req), n_req, _ptr(counters), float(tau),
         FALLBACK_MODES[fallback], _ptr(result.commit_mask), _ptr(result.tokens), _ptr(result.conf), _ptr(row_pos),
-        _ptr(state), _ptr(token_buf), state.stride(0) if state is not None else 0, _stream(stream),
+        _ptr(state), _ptr(token_buf), (state if state is not None else token_buf).stride(0) if (state is not None or token_buf is not None) else 0, _stream(stream),
     )
     _lib.check(st, "optimus_unmask_commit")
     return result

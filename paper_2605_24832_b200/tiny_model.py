@@ -96,16 +96,28 @@ def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor
 
 
 class TinyDLLM(Forward):
-    """The tiny dLLM as the decoder's Forward; keeps each slot's committed token ids."""
+    """The tiny dLLM as the decoder's Forward; keeps each slot's committed token ids.
+
+    It also runs inside ``DeviceLoop`` (``loop_model``): the loop hooks below compute
+    the same forward over the loop's capacity-sized token and row buffers from the
+    device plan (graph-capturable, no host round trip), with the committed token ids
+    kept on the device (written by K3's finalize).  ``lm_head="f3"`` makes the loop's
+    LM head the fused LM-head + unmask kernel (optimus_lmhead_unmask_partials, bf16
+    operands, logits never written) instead of an fp32 GEMM followed by K3."""
 
     needs_tokens = True
+    loop_model = True
 
-    def __init__(self, cfg: TinyConfig, max_slots: int, max_out: int, device="cuda"):
+    def __init__(self, cfg: TinyConfig, max_slots: int, max_out: int, device="cuda", lm_head: str = "torch"):
         torch.backends.cuda.matmul.allow_tf32 = False
+        if lm_head not in ("torch", "f3"):
+            raise ValueError(f"lm_head must be 'torch' or 'f3', got {lm_head!r}")
         self.cfg = cfg
         self.device = torch.device(device)
         self.w = {k: torch.from_numpy(v).to(self.device) for k, v in tiny_weights(cfg).items()}
         self.tokens = np.full((max_slots, max_out), cfg.mask_id, dtype=np.int64)  # committed ids
+        self.max_out = max_out
+        self.lm_head = lm_head
         self.prompt_ids = {}
         self.x = None
 
@@ -194,3 +206,69 @@ class TinyDLLM(Forward):
         slots = dm.__dict__["slots"]
         rows = np.flatnonzero(mask[: m.n_rows])
         self.tokens[slots[m.row_req[rows]], m.row_pos[rows]] = tokens[rows]
+
+    # -------------------------------------------------------------- DeviceLoop hooks
+    def loop_setup(self, loop) -> None:
+        """Capacity buffers of the graph-captured loop: committed token ids per loop
+        position on the device (K3's finalize writes them), and the f3 weight."""
+        cfg = self.cfg
+        self.loop_tok = torch.full((loop.n, self.max_out), cfg.mask_id, dtype=torch.int32, device=self.device)
+        for i, req in enumerate(loop.requests):  # tokens committed before the loop started
+            s = loop.slots_h[i]
+            self.loop_tok[i] = torch.from_numpy(self.tokens[s, : self.max_out].astype(np.int32))
+        if self.lm_head == "f3":
+            # logits = rmsnorm(x) (W_lm * scale): the scale folds into the bf16 weight [vocab, hidden]
+            self.loop_w_lm = (self.w["lm"].t() * cfg.logit_scale).to(torch.bfloat16).contiguous()
+            self.loop_merged = torch.empty((max(loop.caps[1], 1), 1, 3), dtype=torch.float32, device=self.device)
+        self.loop_counters = torch.zeros(loop.n, dtype=torch.int32, device=self.device)
+
+    def loop_begin(self, loop, M) -> None:
+        """Token ids (kv rows: their committed token; window rows: MASK) and RoPE
+        tables for the loop's capacity tokens, from the device plan."""
+        cfg = self.cfg
+        ct = loop.caps[0]
+        r = M["tok_req"][:ct].long()
+        pos = M["tok_pos"][:ct].long().clamp(0, self.max_out - 1)
+        cu, cur = M["cu_seqlens"].long(), M["cu_rows"].long()
+        win_start = cu[r + 1] - (cur[r + 1] - cur[r])  # ChunkPlan order: kv rows, then the window
+        is_win = torch.arange(ct, device=self.device) >= win_start
+        ids = torch.where(is_win, torch.full_like(pos, cfg.mask_id), self.loop_tok[r, pos].long())
+        self.x = self.w["emb"][ids]
+        self.cos, self.sin = rope_tables(M["prompt_len"][r].long() + M["tok_pos"][:ct].long(), cfg.head_dim,
+                                         cfg.rope_theta)
+
+    def loop_qkv(self, loop, layer: int, M):
+        cfg = self.cfg
+        ct = loop.caps[0]
+        d, hq, hkv = cfg.head_dim, cfg.heads, cfg.kv_heads
+        h = rmsnorm(self.x, self.w[f"ln1.{layer}"])
+        qkv = (h @ self.w[f"qkv.{layer}"]).view(ct, hq + 2 * hkv, d)
+        q = apply_rope(qkv[:, :hq], self.cos, self.sin).to(torch.bfloat16).contiguous()
+        k = apply_rope(qkv[:, hq:hq + hkv], self.cos, self.sin).to(torch.bfloat16).contiguous()
+        v = qkv[:, hq + hkv:].to(torch.bfloat16).contiguous()
+        return q, k, v
+
+    def loop_post_attn(self, loop, layer: int, attn_out: torch.Tensor, M) -> None:
+        cfg = self.cfg
+        ct = loop.caps[0]
+        att = attn_out[:ct].float().reshape(ct, cfg.heads * cfg.head_dim)
+        self.x = self.x + att @ self.w[f"o.{layer}"]
+        h = rmsnorm(self.x, self.w[f"ln2.{layer}"])
+        self.x = self.x + (F.silu(h @ self.w[f"g.{layer}"]) * (h @ self.w[f"u.{layer}"])) @ self.w[f"d.{layer}"]
+
+    def loop_unmask(self, loop, M) -> None:
+        """LM head on the window rows, then K3 into loop.res; committed tokens land in
+        loop_tok (the next iterations' kv-row inputs)."""
+        dcfg = loop.cfg
+        cr = loop.caps[1]
+        xw = rmsnorm(self.x[M["row_tok"][:cr].long()], self.w["ln_f"])
+        if self.lm_head == "f3":
+            merged = ops.lmhead_unmask_partials(xw.to(torch.bfloat16), self.loop_w_lm, merge=True,
+                                                merged=self.loop_merged)
+            ops.unmask_finalize(merged, 1, cr, 1, M["cu_rows"], dcfg.confidence_threshold, dcfg.fallback,
+                                row_pos=M["row_pos"], token_buf=self.loop_tok, result=loop.res)
+        else:
+            logits = (xw @ self.w["lm"]) * self.cfg.logit_scale
+            ops.unmask_fused(logits, None, cr, loop.n_vsplit, M["cu_rows"], M["row_req"], self.loop_counters,
+                             dcfg.confidence_threshold, dcfg.fallback, row_pos=M["row_pos"], token_buf=self.loop_tok,
+                             result=loop.res, part=loop.part, n_rows_dev=M["counts"][1:])

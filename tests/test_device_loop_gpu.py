@@ -211,6 +211,61 @@ def test_device_loop_mixed_chunks_matches_host():
         assert steps < 5000
 
 
+def test_device_loop_elastic_chunk_matches_host():
+    """ElasticChunk on the device loop: every iteration the reference's scheduler
+    (dllmsim.scheduler.select_chunk over a CommitEstimator fed with each step's windows
+    and commits, sim.py:219-232,270-293) picks the chunk for the batch, and
+    DeviceLoop.step(chunk=c) runs it from the same captured graph.  Same decode as the
+    host native step given the same chunk sequence, and the estimator fed from the
+    loop's own window observations stays equal to the host one.  (The calibrated B200
+    cost model makes select_chunk pick the largest candidate at this batch; a steeper
+    model makes the chunk move, which is what this exercises.)"""
+    sched = pytest.importorskip("dllmsim.scheduler")
+    costmodel = pytest.importorskip("dllmsim.costmodel")
+    from paper_2605_24832_b200 import engine as pe
+
+    Seg = costmodel.Segment
+    cost = costmodel.CostModel((Seg(0, 2e-6, 2e-4), Seg(64, 4e-6, 2e-4 + 64 * 2e-6),
+                                Seg(256, 8e-6, 2e-4 + 64 * 2e-6 + 192 * 4e-6)))
+    batch, block = 12, 32
+    reqs_h, dec_h = _setup(11, batch, 32)
+    reqs_d, dec_d = _setup(11, batch, 32)
+    loop = DeviceLoop(dec_d, reqs_d, 32, max_chunk=32)
+    for i, r in enumerate(reqs_h):
+        dec_h.native()._slot(r, int(loop.slots_h[i]))
+    mk = lambda: sched.CommitEstimator(window_size=block, alpha=0.95, prior_q=0.8, min_observations=8)
+    est_h, est_d = mk(), mk()
+    prev, seq, steps = None, [], 0
+    while not all(r.finished for r in reqs_h):
+        active = [r for r in reqs_h if not r.finished]
+        c = 32 if est_h.observations < 32 else sched.select_chunk(est_h, cost, len(active),
+                                                                 tuple(range(2, 33, 2)), prev, 0.05)
+        prev = c
+        seq.append(c)
+        windows = [pe.plan_chunk(r, c, block, "in_block").window for r in active]
+        sh = dec_h.step(active, c)
+        sd = loop.step(chunk=c)
+        by_id = {r.id: s for r, s in zip(active, sh)}
+        for r, s in zip(reqs_d, sd):
+            if r.id in by_id:
+                assert set(s.commits) == set(by_id[r.id].commits), (steps, r.id, c)
+                assert s.computed == by_id[r.id].computed
+            else:
+                assert s.computed == 0 and not s.commits
+        for a, b in zip(reqs_h, reqs_d):
+            assert np.array_equal(a.states, b.states), (steps, a.id)
+        for w, s in zip(windows, sh):
+            if w:
+                rank = {p: i for i, p in enumerate(w)}
+                est_h.observe(len(w), {rank[p] for p in s.commits})
+        for n_w, ranks in loop.window_observations():
+            est_d.observe(n_w, ranks)
+        assert est_d.observations == est_h.observations and np.array_equal(est_d.hist, est_h.hist)
+        steps += 1
+        assert steps < 5000
+    assert len(set(seq)) >= 3, seq  # the chunk really changed between iterations
+
+
 def test_graph_captured_host_step_matches_eager(monkeypatch):
     """NativeStepper.device_step_graph (the host-planned step replayed as one CUDA
     graph, counts read on the device) == the eager step, commit for commit."""
