@@ -475,16 +475,71 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     for (double l : loads) span_b = std::max(span_b, l);
   }
 
+  // ---- candidate C: one flat stream.  The units' tiles, in unit order, are cut into
+  // grid equal contiguous ranges (one per CTA), so every CTA streams the same number
+  // of tiles and a unit is cut only where a range ends (few units split, each at most
+  // into ceil(tiles / range) + 1 pieces).  A boundary that would leave a piece under
+  // min_split_tiles moves to the unit's end.
+  std::vector<Piece> pc_;
+  double span_c = 1e300;
+  if (!a_good) {
+    long long total = 0;
+    for (const Unit& u : units) total += u.tiles;
+    const long long E = std::max<long long>(1, (total + grid - 1) / grid);
+    pc_.reserve(nu + 2 * grid + 16);
+    std::vector<double> loads(grid, 0.0);
+    std::vector<char> cutc(nu, 0);
+    int cta = 0;
+    long long room = E;  // tiles left in the current CTA's range
+    for (int ui = 0; ui < nu; ++ui) {
+      int t0 = 0, left = units[ui].tiles;
+      while (left > 0) {
+        if (room <= 0 && cta + 1 < grid) {
+          ++cta;
+          room = E;
+        }
+        const long long here = cta == grid - 1 ? static_cast<long long>(left) : std::max<long long>(room, 1);
+        int take = static_cast<int>(std::min<long long>(left, here));
+        take = std::min(take, hard_cap);
+        if (left - take > 0 && left - take < min_split_tiles) take = std::min(left, hard_cap);  // no sliver
+        if (take < min_split_tiles && left > take && cta + 1 < grid) {  // sliver at the range end: next CTA
+          ++cta;
+          room = E;
+          continue;
+        }
+        if (take < units[ui].tiles) cutc[ui] = 1;
+        pc_.push_back({ui, t0, take, cta});
+        t0 += take;
+        left -= take;
+        room -= take;
+      }
+    }
+    for (const Piece& x : pc_) loads[x.cta] += x.nt + kItem + (cutc[x.unit] ? kSplit : 0.0);
+    span_c = 0;
+    for (double l : loads) span_c = std::max(span_c, l);
+  }
+
   // Prefer whole units unless cutting buys >3% of the makespan, net of the split
   // combine launch and partial traffic it brings (kCombine, measured).
-  bool use_b = span_b + kCombine < 0.97 * span_a && static_cast<int>(pb.size()) <= max_work;
-  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE"))  // diagnostics: "whole" | "cut"
-    use_b = std::strcmp(f, "cut") == 0 && static_cast<int>(pb.size()) <= max_work;
-  const std::vector<Piece>& P = use_b ? pb : pa;
+  const bool c_better = span_c < span_b;
+  const double span_cut = c_better ? span_c : span_b;
+  bool use_b = span_cut + kCombine < 0.97 * span_a &&
+               static_cast<int>((c_better ? pc_ : pb).size()) <= max_work;
+  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE")) {  // diagnostics: "whole" | "cut" | "flat"
+    use_b = (std::strcmp(f, "cut") == 0 || std::strcmp(f, "flat") == 0);
+    if (use_b) {
+      std::vector<Piece>& want = std::strcmp(f, "flat") == 0 ? pc_ : pb;
+      use_b = static_cast<int>(want.size()) <= max_work;
+    }
+  }
+  const bool use_c = use_b && (std::getenv("OPTIMUS_PLAN_FORCE") ? std::strcmp(std::getenv("OPTIMUS_PLAN_FORCE"), "flat") == 0
+                                                                 : c_better);
+  const std::vector<Piece>& P = use_b ? (use_c ? pc_ : pb) : pa;
   if (static_cast<int>(P.size()) > max_work) return fail("attn_plan: work buffer too small");
   if (std::getenv("OPTIMUS_PLAN_DEBUG"))
-    std::fprintf(stderr, "attn_plan: whole-unit LPT span %.1f (%zu items), cutting LPT %.1f (%zu items) -> %s\n",
-                 span_a, pa.size(), span_b, pb.size(), use_b ? "cut" : "whole");
+    std::fprintf(stderr, "attn_plan: whole-unit LPT span %.1f (%zu items), cutting LPT %.1f (%zu items), "
+                 "flat %.1f (%zu items) -> %s\n", span_a, pa.size(), span_b, pb.size(), span_c, pc_.size(),
+                 use_b ? (use_c ? "flat" : "cut") : "whole");
   // Split groups: the pieces of a unit, in key order, get consecutive partial slots.
   std::vector<int> byu(P.size());
   for (size_t x = 0; x < P.size(); ++x) byu[x] = static_cast<int>(x);
