@@ -263,6 +263,16 @@ int optimus_host_apply(int n, const int32_t* slots, int block, const int32_t* cu
                        int32_t* block_index, int32_t* committed, int32_t* steps_taken,
                        int32_t* cached_prefix, const int32_t* out_len, int32_t* commits_out);
 
+/*
+ * fp16 V-cache range gate.  With an fp16 V cache, K1 (and the fused append) store
+ * each bf16 V value as fp16 with cvt.rn.satfinite: |v| > 65504 is clamped to
+ * +-65504.  Every kernel that clamps sets a device flag; this copies the flags
+ * (out[0]: K1, out[1]: fused append; pinned host memory, stream-ordered: read them
+ * after synchronizing `stream`) and, with reset != 0, clears them.  A set flag means
+ * the model's V range needs a bf16 V cache.
+ */
+int optimus_v_saturated(int32_t* out, int reset, void* stream);
+
 /* Recommended vocab split count for n_rows x vocab on the current device. */
 int optimus_unmask_splits(int n_rows, int vocab);
 

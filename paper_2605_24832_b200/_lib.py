@@ -69,6 +69,7 @@ SIGNATURES = {
         [_vp, _i32, _i32, _i32, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     ),
     "optimus_unmask_splits": (_i32, [_i32, _i32]),
+    "optimus_v_saturated": (_i32, [_vp, _i32, _vp]),
     "optimus_unmask_commit": (
         _i32,
         [_vp, _i32, _i64, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _f32, _i32, _vp, _vp, _vp, _vp, _vp,

@@ -36,6 +36,8 @@ int launch_unmask_finalize(const float*, int, int, int, const int32_t*, int, flo
 int launch_unmask_commit(const void*, int, int64_t, const int32_t*, int, const int32_t*, int, int, float*,
                          const int32_t*, const int32_t*, int32_t*, float, int, uint8_t*, int32_t*, float*,
                          const int32_t*, uint8_t*, int32_t*, int64_t, cudaStream_t);
+int v_saturated_k1(int32_t*, int, cudaStream_t);
+int v_saturated_k2(int32_t*, int, cudaStream_t);
 int launch_lmhead_unmask(const CUtensorMap&, const CUtensorMap&, int, int, int, int, float*, cudaStream_t);
 int launch_merge_splits(const float*, int, int, float*, cudaStream_t);
 
@@ -822,6 +824,15 @@ int optimus_unmask_splits(int n_rows, int vocab) {
   int s = eq < 64 ? 8 : eq < 256 ? 4 : eq < 400 ? 2 : eq < 650 ? 3 : eq < 1250 ? 2 : 1;
   s = std::min(s, std::max(1, vocab / 8192));
   return s;
+}
+
+int optimus_v_saturated(int32_t* out, int reset, void* stream) {
+  if (!out) return fail("v_saturated: null pointer");
+  if (int st = check_device()) return st;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int st = cuda_status(v_saturated_k1(out, reset, s), "v_saturated");
+  if (st) return st;
+  return cuda_status(v_saturated_k2(out + 1, reset, s), "v_saturated");
 }
 
 int optimus_unmask_commit(const void* logits, int logits_dtype, int64_t row_stride, const int32_t* row_src,

@@ -18,6 +18,25 @@
 
 namespace optimus {
 
+// Set when a bf16 V value beyond the fp16 range (|v| > 65504) was clamped on its way
+// into an fp16 V cache (cvt.rn.satfinite); read and cleared by optimus_v_saturated.
+__device__ int g_v_saturated_k1;
+
+// Store 8 bf16 V values (one 16-byte vector) as fp16; flag values fp16 clamps.
+__device__ __forceinline__ uint4 v_to_fp16(uint4 vv) {
+  const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+  uint32_t h[4];
+  bool sat = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+    sat |= fabsf(lo) > 65504.f || fabsf(hi) > 65504.f;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(h[i]) : "f"(hi), "f"(lo));
+  }
+  if (__builtin_expect(sat, 0)) atomicOr(&g_v_saturated_k1, 1);
+  return make_uint4(h[0], h[1], h[2], h[3]);
+}
+
 // One thread per 16-byte vector of a (token, head) row: n_tok*Hkv*head_dim/8
 // independent load/store pairs for K and for V, so the scatter runs at full
 // memory-level parallelism instead of one serial loop per token.
@@ -54,14 +73,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
       ((static_cast<int64_t>(page) * hkv + h) * page_size + off) * vec_per_head + c;
   k_cache[dst] = kv;
   if (v_fp16) {
-    const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
-    uint32_t h[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
-      asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(h[i]) : "f"(hi), "f"(lo));
-    }
-    v_cache[dst] = make_uint4(h[0], h[1], h[2], h[3]);
+    v_cache[dst] = v_to_fp16(vv);
   } else {
     v_cache[dst] = vv;
   }
@@ -146,14 +158,7 @@ __global__ void __launch_bounds__(256) kv_append_slots_kernel(
                        (slot & (page_size - 1))) * vec_per_head + c;
   k_cache[dst] = kv;
   if (v_fp16) {
-    const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
-    uint32_t hh[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float lo = __uint_as_float(w[k] << 16), hi = __uint_as_float(w[k] & 0xFFFF0000u);
-      asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(hh[k]) : "f"(hi), "f"(lo));
-    }
-    v_cache[dst] = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+    v_cache[dst] = v_to_fp16(vv);
   } else {
     v_cache[dst] = vv;
   }
@@ -194,6 +199,17 @@ int launch_slot_map(const int32_t* tok_req, const int32_t* tok_pos, const int32_
   slot_map_kernel<<<(n_tok + 255) / 256, 256, 0, stream>>>(tok_req, tok_pos, prompt_len, block_tables,
                                                            max_pages, n_tok, page_size, out);
   return static_cast<int>(cudaGetLastError());
+}
+
+// Copy the saturation flag into *out (stream-ordered) and optionally clear it.
+int v_saturated_k1(int32_t* out, int reset, cudaStream_t stream) {
+  cudaError_t e = cudaMemcpyFromSymbolAsync(out, g_v_saturated_k1, sizeof(int), 0, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess && reset) {
+    void* a = nullptr;
+    e = cudaGetSymbolAddress(&a, g_v_saturated_k1);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, sizeof(int), stream);
+  }
+  return static_cast<int>(e);
 }
 
 }  // namespace optimus

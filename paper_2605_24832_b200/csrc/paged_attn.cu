@@ -38,6 +38,19 @@
 
 namespace optimus {
 
+// Set when the fused append clamps a bf16 V value beyond the fp16 range (see K1).
+__device__ int g_v_saturated_k2;
+
+int v_saturated_k2(int32_t* out, int reset, cudaStream_t stream) {
+  cudaError_t e = cudaMemcpyFromSymbolAsync(out, g_v_saturated_k2, sizeof(int), 0, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess && reset) {
+    void* a = nullptr;
+    e = cudaGetSymbolAddress(&a, g_v_saturated_k2);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, sizeof(int), stream);
+  }
+  return static_cast<int>(e);
+}
+
 constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
 constexpr int kThreads = 384;  // 12 warps: 8 softmax, 4 control
@@ -633,11 +646,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if (p.v_fp16) {
               const uint32_t w4[4] = {val[k].x, val[k].y, val[k].z, val[k].w};
               uint32_t hv[4];
+              bool sat = false;
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const float lo = __uint_as_float(w4[i] << 16), hi = __uint_as_float(w4[i] & 0xFFFF0000u);
+                sat |= fabsf(lo) > 65504.f || fabsf(hi) > 65504.f;
                 asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(hv[i]) : "f"(hi), "f"(lo));
               }
+              if (__builtin_expect(sat, 0)) atomicOr(&g_v_saturated_k2, 1);
               reinterpret_cast<uint4*>(p.v_cache_w)[dst] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
             } else {
               reinterpret_cast<uint4*>(p.v_cache_w)[dst] = val[k];

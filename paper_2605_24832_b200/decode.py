@@ -62,6 +62,9 @@ class DecodeConfig:
     num_pages: int = 16384
     min_split_tiles: int = 4
     logits_dtype: torch.dtype = torch.bfloat16
+    # V cache dtype: fp16 (default: one fp16 P.V MMA in K2; bf16 V values beyond +-65504
+    # are clamped and flagged, see ops.VRangeGate) or bf16 (exact, two MMAs)
+    v_dtype: torch.dtype = torch.float16
     max_output_tokens: int = 4096   # per-request capacity of the packed native state
     max_chunk: int = 64
 
@@ -102,7 +105,15 @@ class StreamingDecoder:
         self.forward = forward
         self.device = torch.device(device)
         self.cache = cache or PagedKVCache(cfg.num_layers, cfg.num_pages, cfg.num_kv_heads,
-                                           cfg.page_size, cfg.head_dim, device=self.device)
+                                           cfg.page_size, cfg.head_dim, device=self.device, v_dtype=cfg.v_dtype)
+        # fp16 V: every step's D2H point also reads the clamp flags (ops.VRangeGate)
+        self.v_gate = ops.VRangeGate() if self.cache.v.dtype == torch.float16 else None
+        if self.v_gate is not None and torch.cuda.is_available():
+            # the flags are per process: start from a clean state (earlier clamps were
+            # reported, or belong to caches this decoder never reads)
+            self.v_gate.issue()
+            torch.cuda.current_stream().synchronize()
+            self.v_gate.buf.zero_()
         self.pool = PagePool(self.cache.num_pages)
         self.tables = BlockTables(self.pool, cfg.max_batch, cfg.max_pages_per_req, cfg.page_size)
         self.grid = ops.sm_count()
@@ -313,9 +324,16 @@ class StreamingDecoder:
     def fetch_commits(self, dm: DeviceMeta, res: ops.UnmaskResult) -> list:
         """One D2H copy of the commit mask -> per-request commit sets."""
         m = dm.host
+        if self.v_gate is not None:
+            self.v_gate.issue()
         if m.n_rows == 0:
+            torch.cuda.current_stream().synchronize()
+            if self.v_gate is not None:
+                self.v_gate.check()
             return [set() for _ in range(m.n_req)]
         mask = res.commit_mask[: m.n_rows].cpu().numpy().astype(bool)
+        if self.v_gate is not None:
+            self.v_gate.check()
         self.d2h_bytes = m.n_rows
         rows = np.flatnonzero(mask)
         req_of = m.row_req[rows]

@@ -210,6 +210,8 @@ class DeviceLoop:
         for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
             self.H[k].copy_(M[k], non_blocking=True)
         self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
+        if self.dec.v_gate is not None:
+            self.dec.v_gate.issue_raw(stream)  # fp16 V clamp flags, read after the step's sync
 
     def _unmask_synthetic(self, M, stream) -> None:
         cfg, fwd, cr = self.cfg, self.dec.forward, self.caps[1]
@@ -289,6 +291,8 @@ class DeviceLoop:
             self.graph.replay()
         torch.cuda.current_stream().synchronize()
         self.t_device += time.perf_counter() - t0
+        if self.dec.v_gate is not None:
+            self.dec.v_gate.check()
         H = self.H
         n = self.n
         n_tok, n_rows = int(H["counts"][0]), int(H["counts"][1])

@@ -266,9 +266,14 @@ class NativeStepper:
             self.mask_host[:n_rows].copy_(res.commit_mask[:n_rows], non_blocking=True)
             if want_tok:
                 self.tok_host[:n_rows].copy_(res.tokens[:n_rows], non_blocking=True)
+        gate = self.dec.v_gate
+        if gate is not None:
+            gate.issue()
         # always: the next plan() rewrites the pinned arena this step's non-blocking
         # upload reads from, so that upload must have completed (even with no rows)
         torch.cuda.current_stream().synchronize()
+        if gate is not None:
+            gate.check()
         self.d2h_bytes = n_rows * (5 if want_tok else 1)
         if want_tok and n_rows:
             fwd.on_commit(dm, self.mask_host.numpy()[:n_rows].astype(bool), self.tok_host.numpy()[:n_rows])

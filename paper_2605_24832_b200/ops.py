@@ -334,6 +334,29 @@ class UnmaskResult:
     conf: torch.Tensor         # float32 [n_rows]
 
 
+class VRangeGate:
+    """fp16 V-cache range gate (``optimus_v_saturated``).  K1 stores bf16 V rows as
+    fp16 (clamping |v| > 65504) and flags any clamp on the device; ``issue`` queues
+    a copy of the flags into pinned memory (and clears them) on the stream, ``check``
+    (after that stream synchronized) raises ``ConfigError`` if a value was clamped.
+    The device flags are per process (a decoder clears them when it is created)."""
+
+    def __init__(self):
+        self.buf = torch.zeros(2, dtype=torch.int32, pin_memory=torch.cuda.is_available())
+
+    def issue(self, stream=None) -> None:
+        _lib.check(_lib.call("optimus_v_saturated", self.buf.data_ptr(), 1, _stream(stream)), "optimus_v_saturated")
+
+    def issue_raw(self, stream_handle: int) -> None:
+        _lib.check(_lib.call("optimus_v_saturated", self.buf.data_ptr(), 1, stream_handle), "optimus_v_saturated")
+
+    def check(self) -> None:
+        if int(self.buf[0]) or int(self.buf[1]):
+            self.buf.zero_()
+            raise ConfigError("fp16 V cache: V values beyond +-65504 were clamped (cvt.satfinite); this model's "
+                              "V range needs a bf16 V cache (DecodeConfig(v_dtype=torch.bfloat16))")
+
+
 def unmask_splits(n_rows: int, vocab: int) -> int:
     return int(_lib.call("optimus_unmask_splits", n_rows, vocab))
 

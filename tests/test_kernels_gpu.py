@@ -469,3 +469,41 @@ def test_decoder_step_with_no_requests():
                        max_batch=4, max_pages_per_req=16, num_pages=64)
     dec = StreamingDecoder(cfg, SyntheticForward(cfg, 64, 4))
     assert dec.step([], 8) == []
+
+
+def test_fp16_v_cache_range_gate():
+    """K1 stores bf16 V rows into an fp16 V cache with saturation; a value beyond
+    +-65504 sets the device flag that ops.VRangeGate reads (and clears), so a model
+    whose V range needs a bf16 cache fails loudly instead of silently clamping.  A
+    bf16 V cache stores the same rows exactly and never flags."""
+    from paper_2605_24832_b200.errors import ConfigError
+    dev = torch.device("cuda")
+    n, hkv, d, page = 5, 2, 128, 16
+    k = torch.randn((n, hkv, d), device=dev).to(torch.bfloat16)
+    v = torch.randn((n, hkv, d), device=dev).to(torch.bfloat16)
+    tok_req = torch.zeros(n, dtype=torch.int32, device=dev)
+    tok_pos = torch.arange(n, dtype=torch.int32, device=dev)
+    prompt = torch.tensor([3], dtype=torch.int32, device=dev)
+    bt = torch.tensor([[2, 0, 1]], dtype=torch.int32, device=dev)
+    gate = ops.VRangeGate()
+    for big, want in ((False, False), (True, True), (False, False)):
+        vv = v.clone()
+        if big:
+            vv[2, 1, 7] = 1.0e5
+        kc = torch.zeros((3, hkv, page, d), dtype=torch.bfloat16, device=dev)
+        vc = torch.zeros((3, hkv, page, d), dtype=torch.float16, device=dev)
+        ops.kv_append(k, vv, tok_req, tok_pos, prompt, bt, kc, vc)
+        gate.issue()
+        torch.cuda.synchronize()
+        if want:
+            with pytest.raises(ConfigError, match="bf16 V cache"):
+                gate.check()
+            assert float(vc.float().abs().max()) == 65504.0
+        else:
+            gate.check()
+        vb = torch.zeros((3, hkv, page, d), dtype=torch.bfloat16, device=dev)
+        ops.kv_append(k, vv, tok_req, tok_pos, prompt, bt, kc, vb)
+        gate.issue()
+        torch.cuda.synchronize()
+        gate.check()  # bf16 V: exact, never flagged
+        assert float(vb.float().abs().max()) == float(vv.float().abs().max())

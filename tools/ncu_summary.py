@@ -20,25 +20,27 @@ for a in args:
     name, path = a.split("=", 1)
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h, units, v = rows[0], rows[1], rows[2]
-    kern = v[h.index("Kernel Name")]
-    md.append(f"## {name}: {kern[:90]}  ({path.split('/')[-1]}, ncu --set full --clock-control none, one launch)")
-    d = {"kernel": kern}
-    for m in METRICS:
-        if m in h:
-            k = h.index(m)
-            md.append(f"- {m}: {v[k]} {units[k]}")
-            try:
-                d[m] = float(v[k].replace(",", "")) * UNIT.get(units[k], 1)
-            except ValueError:
-                d[m] = v[k]
-    if "dram__bytes_read.sum" in d:
-        d["dram_bytes_per_launch"] = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
-        d["dram_gbs"] = d["dram_bytes_per_launch"] / d["gpu__time_duration.sum"] / 1e9
-        md.append(f"- derived: DRAM traffic {d['dram_bytes_per_launch']/1e6:.1f} MB/launch, "
-                  f"{d['dram_gbs']:.0f} GB/s over the (cold, serialised) launch")
-    js[name] = d
-    md.append("")
+    h, units = rows[0], rows[1]
+    for j, v in enumerate(rows[2:]):  # one row per captured launch
+        kern = v[h.index("Kernel Name")]
+        key = name if len(rows) == 3 else f"{name}[{j}]"
+        md.append(f"## {key}: {kern[:90]}  ({path.split('/')[-1]}, ncu --set full --clock-control none, one launch)")
+        d = {"kernel": kern}
+        for m in METRICS:
+            if m in h:
+                k = h.index(m)
+                md.append(f"- {m}: {v[k]} {units[k]}")
+                try:
+                    d[m] = float(v[k].replace(",", "")) * UNIT.get(units[k], 1)
+                except ValueError:
+                    d[m] = v[k]
+        if "dram__bytes_read.sum" in d:
+            d["dram_bytes_per_launch"] = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+            d["dram_gbs"] = d["dram_bytes_per_launch"] / d["gpu__time_duration.sum"] / 1e9
+            md.append(f"- derived: DRAM traffic {d['dram_bytes_per_launch']/1e6:.1f} MB/launch, "
+                      f"{d['dram_gbs']:.0f} GB/s over the (cold, serialised) launch")
+        js[key] = d
+        md.append("")
 if launches:
     rows = [r for r in csv.reader(open(launches)) if len(r) > 5]
     h = rows[0]
