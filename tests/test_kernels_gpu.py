@@ -145,6 +145,26 @@ def test_paged_attention_shapes(page, d, hq, hkv, v_dtype):
     assert err <= ATTN_RTOL, err
 
 
+@pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("chunk", [8, 16, 24, 32, 48])
+def test_paged_attention_group8_two_query_tiles(chunk, v_dtype):
+    """G = 8 (SDAR-30B heads, 32q/4kv): 16 tokens fill a 128-row query tile, so chunks
+    above 16 give a (request, KV head) two query-tile items over the same pages."""
+    s = _step(70 + chunk, 14, chunk, 32, 64, 32, 4, 128, v_dtype=v_dtype)
+    plan, err, got, ref = _attn_check(s)
+    assert (np.diff(s["meta"].cu_seqlens) > 16).any() == (chunk > 16)
+    assert err <= ATTN_RTOL, err
+
+
+def test_paged_attention_group8_page_cap_and_long_context():
+    """G = 8 with requests longer than one item's page cap (255 pages of 16 keys): their
+    units are cut at the cap (split-KV + combine) beside short two-tile requests."""
+    s = _step(93, 8, 32, 32, 16, 32, 4, 128, prompt_range=(300, 9000), out_range=(40, 120))
+    plan, err, got, ref = _attn_check(s, min_split_tiles=4, grid=148)
+    assert plan.n_groups > 0
+    assert err <= ATTN_RTOL, err
+
+
 def test_paged_attention_long_context_split_kv():
     # LongBench-like prompts: forces split-KV and the combine kernel.
     s = _step(99, 6, 8, 32, 64, 32, 8, 128, prompt_range=(4096, 9000), out_range=(20, 120))
