@@ -769,8 +769,23 @@ def main():
 
     # ---- end to end through the public per-step call (closed loop, live state)
     dec.release_all(reqs)
-    e2e = run_e2e(args, dec, fwd, W.pool, world, dev)
-    dloop = run_device_loop(args, dec, world)
+    # headline e2e: StreamingDecoder.step on its graph-captured device-loop backend
+    # (lookahead) where the forward runs in the loop; the host-planned step beside it
+    loop_ok = world == 1 and args.workload != "tp30b"
+    e2e_host = run_e2e(args, dec, fwd, W.pool, world, dev, backend="host")
+    if loop_ok:
+        pool2 = [workload_requests(args, seed_offset=1),
+                 workload_requests(args, seed_offset=2,
+                                   n=16 if args.workload in ("longbench", "ctx4096") else None)]
+        from paper_2605_24832_b200.errors import ConfigError
+        try:
+            e2e = run_e2e(args, dec, fwd, pool2, world, dev, backend="loop_lookahead")
+        except ConfigError as exc:  # a request beyond the device planners' limits
+            print(f"loop backend unavailable ({exc}); e2e = host step", file=sys.stderr)
+            dec.release_all(pool2[0] + pool2[1])
+            e2e, loop_ok = e2e_host, False
+    else:
+        e2e = e2e_host
     m_host = dm.host
     graph = dm = res = dec = fwd = None
 
@@ -820,7 +835,7 @@ def main():
         **extra,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "e2e_device_loop": dloop,
+        "e2e_host_step": e2e_host if loop_ok else None,
         "gpu_launches": n_launch * args.steps,
         "unmask": "vocab-sharded + all-gather (--sharded-unmask)" if args.sharded_unmask and world > 1
         else "replicated (no collective)",
@@ -902,21 +917,31 @@ def chunk_label(args):
     return f"mixed{list(w['mixed'])}" if w["mixed"] else args.chunk
 
 
-def run_e2e(args, dec, fwd, pool, world, dev):
+def run_e2e(args, dec, fwd, pool, world, dev, backend="host"):
     """Closed loop through StreamingDecoder.step: finished requests are replaced
-    from a pool so the batch stays full; the timed region includes host planning,
-    the H2D of the step metadata, the device step, the D2H of the commits and the
-    host apply."""
+    from a pool so the batch stays full; the timed region includes, every step, the
+    host's part of the call, the H2D of that step's inputs (step metadata for the host
+    backend; admissions and chunk changes for the loop backend), the device step, the
+    D2H of the commits (+ the plan arrays for the loop) and the host apply.
+
+    backend "host": C++ host plan -> one H2D -> L x (K1, K2) -> K3 -> D2H -> host apply.
+    backend "loop_lookahead": the DeviceLoop behind the same call (device plan -> work
+    plan -> L x (K1, K2) -> K3 -> device apply as one CUDA graph; the next iteration is
+    launched before the host apply of this one, so an admission enters one call later)."""
+    import dataclasses
     import torch
     import torch.distributed as dist
     batch = list(pool[0])
     spare = list(pool[1])
     n_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 20)
+    cfg0 = dec.cfg
+    dec.cfg = dataclasses.replace(cfg0, step_backend=backend)
 
     def one():
         nonlocal batch
         summ = dec.step(batch, step_chunks(args, batch))
-        fwd.next_version()
+        if backend == "host":
+            fwd.next_version()
         done = [r for r in batch if r.finished]
         if done:
             batch = [r for r in batch if not r.finished]
@@ -939,67 +964,19 @@ def run_e2e(args, dec, fwd, pool, world, dev):
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     dec.release_all(batch)
+    dec.cfg = cfg0
     if world > 1:
         t = torch.tensor([el], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
+    path = ("StreamingDecoder.step, step_backend='loop_lookahead' (DeviceLoop: one graph per iteration: device "
+            "plan -> work plan -> L x (K1,K2) -> K3 -> device apply; D2H plan + mask; the next iteration runs "
+            "during the host apply)" if backend != "host" else
+            "StreamingDecoder.step, step_backend='host' (C++ host plan -> H2D meta -> L x (K1,K2) -> K3 -> D2H "
+            "-> host apply)")
     return {"value": commits / el, "unit": "tokens/s", "h2d_bytes_per_step": h2d // n_steps,
             "d2h_bytes_per_step": d2h // n_steps, "steps": n_steps, "ms_per_step": el / n_steps * 1e3,
-            "path": "StreamingDecoder.step (plan_batch -> H2D meta -> L x (K1,K2) -> K3 -> D2H -> apply_batch)"}
-
-
-def run_device_loop(args, dec, world):
-    """Fixed batch through DeviceLoop: plan, attention work list, L x
-    (K1, K2, combine), K3 and apply as ONE CUDA graph on device-resident request
-    state; per step the host copies back the plan and commit mask and replays the
-    transitions on its Request objects.  No H2D per step (the state stays resident);
-    D2H = the plan arrays + mask.  Timed on the host clock around whole steps."""
-    import torch
-    from paper_2605_24832_b200.device_loop import DeviceLoop
-    from paper_2605_24832_b200.errors import ConfigError
-    if world != 1 or args.workload == "tp30b":
-        return None
-    long_ctx = args.workload in ("longbench", "ctx4096")
-    # the same batch and spare pool as run_e2e (fresh objects): the two e2e numbers
-    # decode the same requests
-    reqs = workload_requests(args, seed_offset=1)
-    spare = workload_requests(args, seed_offset=2, n=16 if long_ctx else None)
-    try:
-        loop = DeviceLoop(dec, reqs, step_chunks(args, reqs), lookahead=True)
-    except (ConfigError, RuntimeError) as e:
-        dec.release_all(reqs)
-        return {"unavailable": str(e)[:200]}
-    n_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 20)
-    h2d = 0
-
-    def one():
-        nonlocal h2d
-        c = loop.step(summaries=False)
-        for i in sorted(loop.free):  # continuous batching: refill finished positions
-            if not spare:
-                break
-            loop.replace(i, spare.pop())
-            h2d += sum(loop.D[k][0].numel() * loop.D[k].element_size() for k in loop.state_keys) + \
-                loop.Dt.shape[1] * 4
-        return c
-
-    for _ in range(3):
-        one()
-    torch.cuda.synchronize()
-    h2d = 0
-    t0 = time.perf_counter()
-    commits = 0
-    for _ in range(n_steps):
-        commits += one()
-    el = time.perf_counter() - t0
-    loop.drain()
-    d2h = sum(t.numel() * t.element_size() for t in loop.H.values())
-    dec.release_all([r for r in loop.requests if not r.finished])
-    return {"value": commits / el, "unit": "tokens/s", "steps": n_steps, "ms_per_step": el / n_steps * 1e3,
-            "h2d_bytes_per_step": h2d // n_steps, "d2h_bytes_per_step": d2h,
-            "batch": "closed loop: finished positions refilled from a spare pool (DeviceLoop.replace)",
-            "path": "DeviceLoop.step, lookahead (one graph: device plan -> work plan -> L x (K1,K2,combine) -> "
-                    "K3 -> device apply; D2H plan + mask; the next graph runs during the host apply)"}
+            "batch": "closed loop: finished requests replaced from a spare pool", "path": path}
 
 
 if __name__ == "__main__":

@@ -66,6 +66,11 @@ class DecodeConfig:
     # are clamped and flagged, see ops.VRangeGate) or bf16 (exact, two MMAs)
     v_dtype: torch.dtype = torch.float16
     max_output_tokens: int = 4096   # per-request capacity of the packed native state
+    # StreamingDecoder.step backend: "host" (C++ host plan -> H2D -> device step -> D2H ->
+    # host apply), "loop" (the graph-captured DeviceLoop: planning on the device, one graph
+    # per iteration; same results) or "loop_lookahead" (the next iteration is launched
+    # before step() returns: admissions and chunk changes take effect one call later)
+    step_backend: str = "host"
     max_chunk: int = 64
 
     def __post_init__(self):
@@ -76,6 +81,8 @@ class DecodeConfig:
         rule_value(self.window_rule)
         if self.fallback not in ops.FALLBACK_MODES:
             raise ConfigError(f"fallback must be one of {sorted(ops.FALLBACK_MODES)}")
+        if self.step_backend not in ("host", "loop", "loop_lookahead"):
+            raise ConfigError("step_backend must be 'host', 'loop' or 'loop_lookahead'")
 
 
 class Forward:
@@ -128,6 +135,7 @@ class StreamingDecoder:
         self.d2h_bytes = 0
         # multi-GPU: a TensorParallelUnmask merges vocab-shard partials across ranks
         self.unmask_impl = None
+        self._loop = None  # DeviceLoop behind step() when cfg.step_backend != "host"
         self._unmask_counters = None  # K3 arrival counters (unmask_fused), zero between launches
         # native (C++) batched host step over packed request state; the Python path
         # (step_python) stays for foreign callers and as the readable specification
@@ -155,6 +163,9 @@ class StreamingDecoder:
             self.tables.release(request.id)
 
     def release_all(self, requests) -> None:
+        if self._loop is not None:
+            self._loop.drain()
+            self._loop = None
         for r in requests:
             if self.tables.slot(r.id) is not None:
                 self.release(r)
@@ -344,8 +355,10 @@ class StreamingDecoder:
         return out
 
     # ------------------------------------------------------------------ the call
-    def step(self, requests: Sequence, chunk_size: int) -> list:
+    def step(self, requests: Sequence, chunk_size) -> list:
         """One streaming decode iteration for the whole batch (sim.py:269-305)."""
+        if self.cfg.step_backend != "host":
+            return self._loop_step(requests, chunk_size)
         if self.use_native:
             nat = self.native()
             out = nat.step(requests, chunk_size)
@@ -372,6 +385,44 @@ class StreamingDecoder:
             if req.finished:
                 self.release(req)
         return summaries
+
+    def _loop_step(self, requests: Sequence, chunk_size) -> list:
+        """``step`` on the graph-captured DeviceLoop.  The loop keeps one position per
+        request of the first call; later calls may drop FINISHED requests and bring new
+        ones into the freed positions (``DeviceLoop.replace``); the chunk may change
+        every call (elastic, up to ``max_chunk``)."""
+        from .device_loop import DeviceLoop
+
+        reqs = list(requests)
+        look = self.cfg.step_backend == "loop_lookahead"
+        L = self._loop
+        if L is None:
+            self._loop = L = DeviceLoop(self, reqs, chunk_size, lookahead=look,
+                                        max_chunk=max(int(np.max(chunk_size)), 32))
+        else:
+            ids = {r.id for r in reqs}
+            pos = {r.id: i for i, r in enumerate(L.requests) if i not in L.free}
+            if any(rid not in ids for rid in pos):
+                raise ConfigError("step_backend loop: a live request left the batch before finishing "
+                                  "(only finished requests may be dropped)")
+            new = [r for r in reqs if r.id not in pos]
+            free = sorted(L.free)
+            if len(new) > len(free):
+                raise ConfigError(f"step_backend loop: {len(new)} new requests but {len(free)} free positions "
+                                  f"(the loop holds {L.n}; start it with the full batch)")
+            for i, r in zip(free, new):
+                L.replace(i, r)
+        where = {r.id: i for i, r in enumerate(L.requests)}
+        if np.ndim(chunk_size):
+            per = np.full(L.n, int(np.min(chunk_size)), dtype=np.int32)
+            for r, c in zip(reqs, chunk_size):
+                per[where[r.id]] = c
+            chunk = per
+        else:
+            chunk = int(chunk_size)
+        summ = L.step(chunk=chunk)
+        self.h2d_bytes, self.d2h_bytes = L.h2d_bytes, L.d2h_bytes
+        return [summ[where[r.id]] for r in reqs]
 
     def step_python(self, requests: Sequence, chunk_size: int) -> list:
         """The same iteration with the host half in Python (plan_batch / apply_batch)."""

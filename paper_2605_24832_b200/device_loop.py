@@ -134,22 +134,34 @@ class DeviceLoop:
         self.res = ops.UnmaskResult(z(cr, torch.uint8), z(cr), z(cr, torch.float32))
         self.out = torch.empty((ct, cfg.num_q_heads, cfg.head_dim), dtype=torch.bfloat16, device=dev)
         # pinned host mirrors of what the host replay needs
-        self.H = {k: torch.zeros(M[k].numel(), dtype=torch.int32, pin_memory=True)
-                  for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos")}
-        self.H["mask"] = torch.zeros(max(cr, 1), dtype=torch.uint8, pin_memory=True)
-        self.graph = None
+        # with lookahead two graphs alternate, each reading back into its own buffers, so
+        # the next iteration is launched before this one's results are read
+        def host_mirror():
+            H = {k: torch.zeros(M[k].numel(), dtype=torch.int32, pin_memory=True)
+                 for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos")}
+            H["mask"] = torch.zeros(max(cr, 1), dtype=torch.uint8, pin_memory=True)
+            H["vsat"] = torch.zeros(2, dtype=torch.int32, pin_memory=True)  # fp16 V clamp flags
+            return H
+        self.Hs = [host_mirror() for _ in range(2 if lookahead else 1)]
+        self.H = self.Hs[0]
+        self.graphs = []
+        self._events = [torch.cuda.Event() for _ in self.Hs]
+        self._cur = 0
         self.t_device = 0.0  # host seconds spent in replay + sync (diagnostics)
         self.free = set()  # loop indices whose request finished and was released
         self.lookahead = bool(lookahead)
         self._inflight = False  # a lookahead iteration was launched and not yet consumed
         self._stale = set()  # positions refilled while an iteration was in flight
         self._last = (np.zeros(n + 1, np.int32), np.zeros(1, np.int32), np.zeros(1, np.uint8))
+        self._h2d = 0
+        self.h2d_bytes = self.d2h_bytes = 0
         if self.model:
             fwd.loop_setup(self)
 
     # ------------------------------------------------------------------ device
-    def _enqueue(self, stream) -> None:
+    def _enqueue(self, stream, H=None) -> None:
         cfg, D, M, n = self.cfg, self.D, self.M, self.n
+        H = self.H if H is None else H
         ct, cr, cw = self.caps
         p = lambda t: t.data_ptr()
         L = _lib
@@ -208,10 +220,10 @@ class DeviceLoop:
             p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["counts"][3:]),
             stream), "device_apply")  # apply's status = the plan's counts[3]: a rejected plan skips apply
         for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
-            self.H[k].copy_(M[k], non_blocking=True)
-        self.H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
-        if self.dec.v_gate is not None:
-            self.dec.v_gate.issue_raw(stream)  # fp16 V clamp flags, read after the step's sync
+            H[k].copy_(M[k], non_blocking=True)
+        H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
+        if self.dec.v_gate is not None:  # fp16 V clamp flags, read after the iteration completed
+            _lib.check(L.call("optimus_v_saturated", H["vsat"].data_ptr(), 1, stream), "optimus_v_saturated")
 
     def _unmask_synthetic(self, M, stream) -> None:
         cfg, fwd, cr = self.cfg, self.dec.forward, self.caps[1]
@@ -244,9 +256,12 @@ class DeviceLoop:
         with torch.cuda.stream(s):
             self._enqueue(s.cuda_stream)  # warm (lazy kernel attributes)
             s.synchronize()
-            self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph, stream=s):
-                self._enqueue(s.cuda_stream)
+            self.graphs = []
+            for H in self.Hs:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self._enqueue(s.cuda_stream, H)
+                self.graphs.append(g)
         torch.cuda.synchronize()
         for k, v in saved.items():
             self.D[k].copy_(v)
@@ -267,6 +282,7 @@ class DeviceLoop:
             self._chunks_ev.synchronize()  # the previous staging copy has read the pinned buffer
         self._chunks_pin.numpy()[:] = c
         self.chunks_d.copy_(self._chunks_pin, non_blocking=True)
+        self._h2d += c.nbytes
         self._chunks_ev = torch.cuda.Event()
         self._chunks_ev.record()
         self.chunk_h = c
@@ -282,18 +298,40 @@ class DeviceLoop:
         overlaps the GPU; a request admitted by ``replace`` — and a chunk given here —
         then takes effect one iteration later (the in-flight iteration was planned
         with the previous state)."""
-        if self.graph is None:
+        if not self.graphs:
             self.capture()
         if chunk is not None:
             self.set_chunk(chunk)
+        # per-step copies: what this step's host calls staged (admissions, chunks) and the
+        # plan arrays + commit mask every replay reads back
+        self.h2d_bytes, self._h2d = self._h2d, 0
+        self.d2h_bytes = sum(v.numel() * v.element_size() for v in self.H.values())
         t0 = time.perf_counter()
-        if not self._inflight:
-            self.graph.replay()
-        torch.cuda.current_stream().synchronize()
+        if not self.lookahead:
+            self.graphs[0].replay()
+            torch.cuda.current_stream().synchronize()
+            H = self.Hs[0]
+        else:
+            if not self._inflight:  # first call: this iteration was not launched yet
+                self.graphs[self._cur].replay()
+                self._events[self._cur].record()
+            # the next iteration goes in before this one is waited for: the GPU never idles
+            # on the host (its plan reads the state this one leaves; its read-back buffers
+            # are the other graph's)
+            nxt = len(self.graphs) - 1 - self._cur
+            self.graphs[nxt].replay()
+            self._events[nxt].record()
+            self._events[self._cur].synchronize()
+            H = self.Hs[self._cur]
+            self._cur = nxt
+            self._inflight = True
         self.t_device += time.perf_counter() - t0
         if self.dec.v_gate is not None:
-            self.dec.v_gate.check()
-        H = self.H
+            vs = H["vsat"]
+            if int(vs[0]) or int(vs[1]):
+                vs.zero_()
+                raise ConfigError("fp16 V cache: V values beyond +-65504 were clamped (cvt.satfinite); this "
+                                  "model's V range needs a bf16 V cache (DecodeConfig(v_dtype=torch.bfloat16))")
         n = self.n
         n_tok, n_rows = int(H["counts"][0]), int(H["counts"][1])
         if int(H["counts"][3]) != 0:
@@ -307,9 +345,6 @@ class DeviceLoop:
         row_pos = H["row_pos"].numpy()[: max(n_rows, 1)].copy()
         mask = H["mask"].numpy()[: max(n_rows, 1)].copy()
         stale, self._stale = sorted(self._stale), set()
-        self._inflight = self.lookahead
-        if self.lookahead:
-            self.graph.replay()  # the next iteration runs while the host applies this one
         # positions refilled after this iteration was launched: it planned nothing for
         # them (their previous request had finished); drop them from the host replay
         for i in stale:
@@ -361,6 +396,7 @@ class DeviceLoop:
         if self._inflight:
             torch.cuda.current_stream().synchronize()
             self._inflight = False
+            self._cur = 0
 
     def replace(self, i: int, request) -> None:
         """Continuous batching: admit `request` into loop position i, whose request
@@ -380,7 +416,9 @@ class DeviceLoop:
         for k in self.state_keys:
             src = torch.from_numpy(np.ascontiguousarray(getattr(bs, k)[s : s + 1])).pin_memory()
             self.D[k][s : s + 1].copy_(src, non_blocking=True)
+            self._h2d += src.numel() * src.element_size()
         self.Dt[s].copy_(torch.from_numpy(self.dec.tables.table[s].copy()).pin_memory(), non_blocking=True)
+        self._h2d += self.Dt[s].numel() * 4
         self.requests[i] = request
         self.free.discard(i)
         if self._inflight:

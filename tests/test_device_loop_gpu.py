@@ -300,3 +300,71 @@ def test_device_loop_rejects_what_the_device_planners_cannot_run():
     big = Request(id=999, arrival_time=0.0, prompt_tokens=10, output_tokens=5000)
     with pytest.raises(ConfigError):
         DeviceLoop(dec, reqs[:3] + [big], 8)
+
+
+@pytest.mark.parametrize("backend", ["loop", "loop_lookahead"])
+def test_streaming_decoder_step_on_the_device_loop(backend):
+    """StreamingDecoder.step with DecodeConfig.step_backend = "loop" runs the
+    graph-captured DeviceLoop behind the same per-step call: a closed loop that drops
+    finished requests and brings new ones into the batch gives exactly the host
+    step's commits and states (new requests take the freed positions' batch slots, so
+    the host run admits them into the same slots).  With "loop_lookahead" the next
+    iteration is already in flight when step() returns, so an admission takes effect
+    one call later: the host run admits with that lag."""
+    import dataclasses
+    batch, chunk = 10, 16
+    reqs_h, dec_h = _setup(12, batch, chunk)
+    reqs_d, dec_d = _setup(12, batch, chunk)
+    dec_d.cfg = dataclasses.replace(dec_d.cfg, step_backend=backend)
+    look = backend == "loop_lookahead"
+
+    def spares():
+        class A:
+            pass
+        a = A()
+        a.workload, a.chunk, a.page, a.batch, a.seed, a.steps = "sharegpt", chunk, 64, 6, 12, 1
+        return [r for r in bench.workload_requests(a, seed_offset=9)
+                if r.prompt_tokens + r.output_tokens <= dec_h.cfg.max_pages_per_req * 64]
+
+    spare_h, spare_d = spares(), spares()
+    live_h, live_d = list(reqs_h), list(reqs_d)
+    sd = dec_d.step(live_d, chunk)  # builds the loop: its positions take the batch slots
+    L = dec_d._loop
+    for i, r in enumerate(reqs_h):
+        dec_h.native()._slot(r, int(L.slots_h[i]))
+    sh = dec_h.step(live_h, chunk)
+    lagged, steps, admitted = [], 0, 0
+    while True:
+        by_id = {r.id: s for r, s in zip(live_h, sh)}
+        for r, s in zip(live_d, sd):
+            if r.id in by_id:
+                assert set(s.commits) == set(by_id[r.id].commits), (steps, r.id)
+                assert s.computed == by_id[r.id].computed, (steps, r.id)
+            else:
+                assert s.computed == 0 and not s.commits, (steps, r.id)
+        for a in live_h:
+            b = next(x for x in live_d if x.id == a.id)
+            assert np.array_equal(a.states, b.states), (steps, a.id)
+        live_h = [r for r in live_h if not r.finished]
+        done_d = [r for r in live_d if r.finished]
+        live_d = [r for r in live_d if not r.finished]
+        for nh in lagged:
+            live_h.append(nh)
+        lagged = []
+        for r in done_d:  # every finished request is replaced by the next spare
+            if not spare_d:
+                break
+            nh, nd = spare_h.pop(0), spare_d.pop(0)
+            slot = int(L.slots_h[[x.id for x in L.requests].index(r.id)])
+            live_d.append(nd)
+            dec_h.native()._slot(nh, slot)
+            (lagged if look else live_h).append(nh)
+            admitted += 1
+        if not live_d and not live_h and not lagged:
+            break
+        sd = dec_d.step(live_d, chunk)
+        sh = dec_h.step(live_h, chunk) if live_h else []
+        steps += 1
+        assert steps < 5000
+    dec_d.release_all([])
+    assert admitted >= 3
