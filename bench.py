@@ -348,6 +348,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    weak = args.gpus > 1 and args.workload != "tp30b"
+    if weak:  # the B200 arm's global batch (weak scaling); bounded number of whole steps
+        args.batch *= args.gpus
+        args.steps = max(1, min(args.steps, 3))
+        args.warmup = min(args.warmup, 1)
     args.oproj_hidden = workload_spec(args.workload).get("oproj_hidden")
     cfg, reqs, plans, m = reference_batch(args)
     step = CpuStep(args, reqs, plans, m, cfg)
@@ -369,7 +374,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "decoded_tokens_per_s", "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak" if weak else "strong",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
         "config": config_block(args, cfg, m, commits, vis_keys, args.gpus),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": step.workers, "kind": "port",
@@ -611,9 +616,10 @@ def configs_block(args, W0, dev):
 def per_rank_projection(args, dev, t1_lines):
     """SURVEY §8e projection from one GPU: rank 0's KV-head shard of the step for
     tp = 2/4/8 (Hq/tp query heads, Hkv/tp KV heads and their pages; the unmask
-    replicated over the full vocabulary), run alone.  Per-GPU efficiency
-    T1 / (N * T_rank) for attention only (L x (K1 + K2)) and for the whole step
-    (attention + unmask).  A projection, not a measured multi-GPU curve."""
+    replicated over the full vocabulary), run alone.  Strong scaling (the batch of 64
+    split over the ranks): per-GPU efficiency T1 / (N * T_rank) for attention only
+    (L x (K1 + K2)) and for the whole step.  Weak scaling (what ``--gpus N`` runs: a
+    batch of 64 N): T1 / T_rank.  A projection, not a measured multi-GPU curve."""
     res = {}
     for wl, t1 in t1_lines.items():
         a = argparse.Namespace(**{**vars(args), "workload": wl, "batch": 64, "chunk": 32})
@@ -627,7 +633,21 @@ def per_rank_projection(args, dev, t1_lines):
                          "rank_k2_us": ln["k2_us"], "rank_k2_frac": ln["k2_frac"], "rank_k3_us": ln["k3_us"],
                          "eff_attention": t1["attention_ms"] / (tp * ln["attention_ms"]),
                          "eff_step": t1["ms_per_step"] / (tp * ln["ms_per_step"])})
-        res[wl] = {"t1_ms_per_step": t1["ms_per_step"], "t1_attention_ms": t1["attention_ms"], "ranks": rows}
+        # weak scaling (what bench.py --gpus N runs): the batch grows with N, rank 0
+        # streams the same (request, head) pairs as one GPU; the replicated unmask covers
+        # every request's window rows
+        weak = []
+        for tp in (2, 4, 8):
+            aw = argparse.Namespace(**{**vars(a), "batch": 64 * tp})
+            W = build_decoder(aw, dev, world=tp, rank=0, e2e_pools=False)
+            ln = step_line(aw, W, dev, steps=10, label=f"{workload_name(a)} rank 0 of tp{tp}, batch {64 * tp}")
+            W = None
+            free()
+            weak.append({"tp": tp, "global_batch": 64 * tp, "rank_ms_per_step": ln["ms_per_step"],
+                         "rank_k2_us": ln["k2_us"], "rank_k3_us": ln["k3_us"],
+                         "eff_step": t1["ms_per_step"] / ln["ms_per_step"]})
+        res[wl] = {"t1_ms_per_step": t1["ms_per_step"], "t1_attention_ms": t1["attention_ms"], "ranks": rows,
+                   "weak": weak}
     return res
 
 
@@ -741,6 +761,12 @@ def main():
 
     from paper_2605_24832_b200.engine import plan_batch
 
+    # N > 1: the KV heads shard over the ranks and the batch grows with them (weak
+    # scaling: every rank streams the pages of batch x Hkv / N (request, head) pairs, the
+    # same as one GPU at the base batch); tp30b is the fixed TP decode step (strong)
+    weak = world > 1 and args.workload != "tp30b"
+    if weak:
+        args.batch *= world
     W = build_decoder(args, dev, world, rank, sharded_unmask=args.sharded_unmask)
     cfg, fwd, dec, reqs = W.cfg, W.fwd, W.dec, W.reqs
     plans = plan_batch(reqs, step_chunks(args, reqs), cfg.block_size, cfg.window_rule)
@@ -817,7 +843,7 @@ def main():
     line = {
         "metric": "decoded_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": config_block(args, cfg, m_host, commits_per_step, vis_keys, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "kernel": "paged_attn_kernel (K2)",
