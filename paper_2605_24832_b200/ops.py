@@ -347,9 +347,6 @@ class VRangeGate:
     def issue(self, stream=None) -> None:
         _lib.check(_lib.call("optimus_v_saturated", self.buf.data_ptr(), 1, _stream(stream)), "optimus_v_saturated")
 
-    def issue_raw(self, stream_handle: int) -> None:
-        _lib.check(_lib.call("optimus_v_saturated", self.buf.data_ptr(), 1, stream_handle), "optimus_v_saturated")
-
     def check(self) -> None:
         if int(self.buf[0]) or int(self.buf[1]):
             self.buf.zero_()
