@@ -368,3 +368,40 @@ def test_streaming_decoder_step_on_the_device_loop(backend):
         assert steps < 5000
     dec_d.release_all([])
     assert admitted >= 3
+
+
+def test_streaming_decoder_loop_backend_mixed_chunks():
+    """The loop backend takes the per-request chunk list of the mixed-chunk workload
+    (BASELINE configs[3]) through the same StreamingDecoder.step call: each request's
+    chunk lands at its loop position; same decode as the host backend."""
+    import dataclasses
+    batch = 12
+    rng = np.random.default_rng(21)
+    reqs_h, dec_h = _setup(21, batch, 32)
+    reqs_d, dec_d = _setup(21, batch, 32)
+    dec_d.cfg = dataclasses.replace(dec_d.cfg, step_backend="loop")
+    chunk_of = {r.id: int(c) for r, c in zip(reqs_h, rng.choice([8, 16, 24, 32], batch))}
+    # both paths decode in reverse order, so list order != loop position order
+    live_d = list(reversed(reqs_d))
+    sd = dec_d.step(live_d, [chunk_of[r.id] for r in live_d])
+    L = dec_d._loop
+    for r in reqs_h:
+        dec_h.native()._slot(r, int(L.slots_h[[x.id for x in L.requests].index(r.id)]))
+    live_h = list(reversed(reqs_h))
+    sh = dec_h.step(live_h, [chunk_of[r.id] for r in live_h])
+    steps = 0
+    while True:
+        assert [set(s.commits) for s in sd] == [set(s.commits) for s in sh], steps
+        assert [s.computed for s in sd] == [s.computed for s in sh], steps
+        for a, b in zip(live_h, live_d):
+            assert a.id == b.id and np.array_equal(a.states, b.states), (steps, a.id)
+        live_h = [r for r in live_h if not r.finished]
+        live_d = [r for r in live_d if not r.finished]
+        if not live_d:
+            break
+        sd = dec_d.step(live_d, [chunk_of[r.id] for r in live_d])
+        sh = dec_h.step(live_h, [chunk_of[r.id] for r in live_h])
+        steps += 1
+        assert steps < 5000
+    assert not live_h
+    dec_d.release_all([])
