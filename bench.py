@@ -797,7 +797,9 @@ def main():
     dec.release_all(reqs)
     # headline e2e: StreamingDecoder.step on its graph-captured device-loop backend
     # (lookahead) where the forward runs in the loop; the host-planned step beside it
-    loop_ok = world == 1 and args.workload != "tp30b"
+    # (every rank runs its own loop: with the replicated unmask the ranks commit alike
+    # and need no exchange; the vocab-sharded unmask needs its all-gather: host backend)
+    loop_ok = args.workload != "tp30b" and not args.sharded_unmask
     e2e_host = run_e2e(args, dec, fwd, W.pool, world, dev, backend="host")
     if loop_ok:
         pool2 = [workload_requests(args, seed_offset=1),
