@@ -54,6 +54,9 @@ int v_saturated_k2(int32_t* out, int reset, cudaStream_t stream) {
 constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
 constexpr int kThreads = 384;  // 12 warps: 8 softmax, 4 control
+// registers per thread after the setmaxnreg split: 128 x 56 + 256 x 224 = 384 x 168
+constexpr int kCtrlRegs = 56;
+constexpr int kMathRegs = 224;
 constexpr int kSBuf = 3;       // S/P buffers in TMEM, rotating over the CTA's tile stream
 constexpr int kInfo = 4;       // staged work-item records: the metadata warp runs 3 items ahead
 constexpr int kEpiRing = 8;    // per-item epilogue records (outlive the staged record)
@@ -215,263 +218,271 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int w_begin = p.cta_off[blockIdx.x];
   const int w_end = p.cta_off[blockIdx.x + 1];
 
+  // Register split (setmaxnreg, per warpgroup): the control warpgroup (warps 8-11: TMA
+  // producers, MMA issuer, metadata) runs in kCtrlRegs registers and hands the rest to
+  // the two softmax warpgroups.  Each side's code is reachable only after its own
+  // setmaxnreg, so the allocator budgets the two sides separately.
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kCtrlRegs));
   if (warp == 8 || warp == 10) {
-    // ------------------------------------------------------------ TMA producers
-    // Warp 8 loads Q and the K ring, warp 10 the V ring.  The whole warp runs the
-    // loop (operands warp-uniform, in uniform registers); one elected lane issues.
-    const bool is_k = warp == 8;
-    const int NST = is_k ? KST : VST;
-    const uint32_t q_tx = KB * 64 * p.group * p.tok_per_tile * 2;
-    const uint32_t chunk_tx = p.box_rows * 128 * KB;  // one tensor, one box-row group
-    const int chunks_per_tile = kTileN / p.box_rows;
-    const int shift = p.page_shift;
-    const int pmask = p.page_size - 1;
-    const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
-    uint8_t* ring = is_k ? sK : sV;
-    uint64_t* full = is_k ? k_full : v_full;
-    uint64_t* empty = is_k ? k_empty : v_empty;
-    // K/V pages are read once per step: stream them through L2 with evict_first so
-    // the step metadata and Q stay resident
-    const uint64_t pol_stream = l2_policy_evict_first();
-    int tile_ctr = 0;
-    int unit = 0;
-    bool need_append = p.k_new != nullptr;  // output-region tiles wait for the fused append
-    if (need_append) {
-      // the append's loads go first; (diagnostics, dbg 64: no load before it landed)
-      mbar_wait((p.dbg & 64) ? append_done : append_issued, 0);
-      if (p.dbg & 64) need_append = false;
-    }
-    for (int w = w_begin; w < w_end; ++w, ++unit) {
-      const int ib = unit % kInfo;
-      mbar_wait(&info_full[ib], (unit / kInfo) & 1);
-      // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
-      // everything above overlapped their tail under PDL; the loads may not.
-      if (unit == 0) grid_dep_wait();
-      const UnitInfo& u = info[ib];
-      const int head = __shfl_sync(0xFFFFFFFFu, u.head, 0);
-      const int key_begin = __shfl_sync(0xFFFFFFFFu, u.key_begin, 0);
-      const int key_end = __shfl_sync(0xFFFFFFFFu, u.key_end, 0);
-      const int pg0 = key_begin >> shift;
-      // first key this step appends in this item's range: tiles below it never wait
-      // for the fused append (new rows are the recomputed kv positions + the window)
-      int first_new = 0x7FFFFFFF;
+      // ------------------------------------------------------------ TMA producers
+      // Warp 8 loads Q and the K ring, warp 10 the V ring.  The whole warp runs the
+      // loop (operands warp-uniform, in uniform registers); one elected lane issues.
+      const bool is_k = warp == 8;
+      const int NST = is_k ? KST : VST;
+      const uint32_t q_tx = KB * 64 * p.group * p.tok_per_tile * 2;
+      const uint32_t chunk_tx = p.box_rows * 128 * KB;  // one tensor, one box-row group
+      const int chunks_per_tile = kTileN / p.box_rows;
+      const int shift = p.page_shift;
+      const int pmask = p.page_size - 1;
+      const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+      uint8_t* ring = is_k ? sK : sV;
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      // K/V pages are read once per step: stream them through L2 with evict_first so
+      // the step metadata and Q stay resident
+      const uint64_t pol_stream = l2_policy_evict_first();
+      int tile_ctr = 0;
+      int unit = 0;
+      bool need_append = p.k_new != nullptr;  // output-region tiles wait for the fused append
       if (need_append) {
-        const int n_tok_u = __shfl_sync(0xFFFFFFFFu, u.n_tok, 0);
-        for (int i = lane; i < n_tok_u; i += 32) first_new = min(first_new, u.qpos[i]);
+        // the append's loads go first; (diagnostics, dbg 64: no load before it landed)
+        mbar_wait((p.dbg & 64) ? append_done : append_issued, 0);
+        if (p.dbg & 64) need_append = false;
+      }
+      for (int w = w_begin; w < w_end; ++w, ++unit) {
+        const int ib = unit % kInfo;
+        mbar_wait(&info_full[ib], (unit / kInfo) & 1);
+        // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
+        // everything above overlapped their tail under PDL; the loads may not.
+        if (unit == 0) grid_dep_wait();
+        const UnitInfo& u = info[ib];
+        const int head = __shfl_sync(0xFFFFFFFFu, u.head, 0);
+        const int key_begin = __shfl_sync(0xFFFFFFFFu, u.key_begin, 0);
+        const int key_end = __shfl_sync(0xFFFFFFFFu, u.key_end, 0);
+        const int pg0 = key_begin >> shift;
+        // first key this step appends in this item's range: tiles below it never wait
+        // for the fused append (new rows are the recomputed kv positions + the window)
+        int first_new = 0x7FFFFFFF;
+        if (need_append) {
+          const int n_tok_u = __shfl_sync(0xFFFFFFFFu, u.n_tok, 0);
+          for (int i = lane; i < n_tok_u; i += 32) first_new = min(first_new, u.qpos[i]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) first_new = min(first_new, __shfl_xor_sync(0xFFFFFFFFu, first_new, o));
-        first_new += __shfl_sync(0xFFFFFFFFu, u.prompt, 0);
-      }
-      if (is_k) {
-        const int tok_begin = __shfl_sync(0xFFFFFFFFu, u.tok_begin, 0);
-        mbar_wait(q_empty, (unit & 1) ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(q_full, q_tx);
-          for (int kb = 0; kb < KB; ++kb)
-            tma_load_4d(sQ + kb * (kBlockM * 128), &tm_q, q_full, kb * 64, 0, head, tok_begin);
+          for (int o = 16; o > 0; o >>= 1) first_new = min(first_new, __shfl_xor_sync(0xFFFFFFFFu, first_new, o));
+          first_new += __shfl_sync(0xFFFFFFFFu, u.prompt, 0);
         }
-        __syncwarp();
-      }
-      for (int kt = key_begin; kt < key_end; kt += kTileN, ++tile_ctr) {
-        const int st = tile_ctr % NST;
-        int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
-        if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
-        if (is_k && lane == 0) trace(p, 0, tile_ctr);
-        if (need_append && kt + kTileN > first_new) {
-          // this tile holds rows appended in this step: wait for the append once
-          mbar_wait(append_done, 0);
-          need_append = false;
-        }
-        mbar_wait(&empty[st], ((tile_ctr / NST) & 1) ^ 1);
-        if (lane == 0) trace(p, is_k ? 4 : 10, tile_ctr);
-        uint8_t* dst = ring + st * L::KT_BYTES;
-        const int pg_lane = lane < n_chunks ? u.pages[((kt + lane * p.box_rows) >> shift) - pg0] : 0;
-        if (elect_one()) mbar_arrive_expect_tx(&full[st], n_chunks * chunk_tx);
-        for (int c = 0; c < n_chunks; ++c) {
-          const int s0 = kt + c * p.box_rows;
-          const int page = __shfl_sync(0xFFFFFFFFu, pg_lane, c);
+        if (is_k) {
+          const int tok_begin = __shfl_sync(0xFFFFFFFFu, u.tok_begin, 0);
+          mbar_wait(q_empty, (unit & 1) ^ 1);
           if (elect_one()) {
-            for (int kb = 0; kb < KB; ++kb) {
-              if (p.dbg & 32)
-                tma_load_4d(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st], kb * 64,
-                            s0 & pmask, head, page);
-              else
-                tma_load_4d_hint(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st],
-                                 kb * 64, s0 & pmask, head, page, pol_stream);
+            mbar_arrive_expect_tx(q_full, q_tx);
+            for (int kb = 0; kb < KB; ++kb)
+              tma_load_4d(sQ + kb * (kBlockM * 128), &tm_q, q_full, kb * 64, 0, head, tok_begin);
+          }
+          __syncwarp();
+        }
+        for (int kt = key_begin; kt < key_end; kt += kTileN, ++tile_ctr) {
+          const int st = tile_ctr % NST;
+          int n_chunks = (min(kTileN, key_end - kt) + p.box_rows - 1) / p.box_rows;
+          if (n_chunks > chunks_per_tile) n_chunks = chunks_per_tile;
+          if (is_k && lane == 0) trace(p, 0, tile_ctr);
+          if (need_append && kt + kTileN > first_new) {
+            // this tile holds rows appended in this step: wait for the append once
+            mbar_wait(append_done, 0);
+            need_append = false;
+          }
+          mbar_wait(&empty[st], ((tile_ctr / NST) & 1) ^ 1);
+          if (lane == 0) trace(p, is_k ? 4 : 10, tile_ctr);
+          uint8_t* dst = ring + st * L::KT_BYTES;
+          const int pg_lane = lane < n_chunks ? u.pages[((kt + lane * p.box_rows) >> shift) - pg0] : 0;
+          if (elect_one()) mbar_arrive_expect_tx(&full[st], n_chunks * chunk_tx);
+          for (int c = 0; c < n_chunks; ++c) {
+            const int s0 = kt + c * p.box_rows;
+            const int page = __shfl_sync(0xFFFFFFFFu, pg_lane, c);
+            if (elect_one()) {
+              for (int kb = 0; kb < KB; ++kb) {
+                if (p.dbg & 32)
+                  tma_load_4d(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st], kb * 64,
+                              s0 & pmask, head, page);
+                else
+                  tma_load_4d_hint(dst + kb * (kTileN * 128) + c * p.box_rows * 128, tm, &full[st],
+                                   kb * 64, s0 & pmask, head, page, pol_stream);
+              }
             }
           }
+          __syncwarp();
+          if (lane == 0) trace(p, is_k ? 5 : 11, tile_ctr);
         }
-        __syncwarp();
-        if (lane == 0) trace(p, is_k ? 5 : 11, tile_ctr);
-      }
-      if (elect_one()) mbar_arrive(&info_empty[ib]);
-      __syncwarp();
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    // One stream of tiles over the CTA's work items.  S(t) = Q K^T goes to S/P buffer
-    // t % 3 with A = the item's Q tile in TMEM (copied from smem by tcgen05.cp when
-    // the S stream enters the item) and B = the K tile; PV(t) accumulates
-    // P(t) (TMEM, TS-MMA) x V into O_{j&1} of its item.  S runs three tiles ahead
-    // of PV, across item boundaries: the in-order tensor pipe retires PV(t) before
-    // S(t+3) overwrites the buffer holding P(t), and the last S of an item before the
-    // next item's Q copy overwrites the Q columns.  The whole warp runs the loop
-    // (warp-uniform operands in uniform registers); one elected lane issues.
-    constexpr uint32_t idesc_s = umma_idesc_bf16(kBlockM, kTileN, false, false);
-    // PV: A = P from TMEM, B = V (MN-major).  fp16 V cache: one fp16 P plane;
-    // bf16 V cache: P = hi + lo bf16 planes, two MMAs per k-step.
-    constexpr uint32_t idesc_o = VF16 ? umma_idesc_f16(kBlockM, HD, false, true, 0u, 0u)
-                                      : umma_idesc_bf16(kBlockM, HD, false, true);
-    const uint32_t sQ_a = smem_u32(sQ), sK_a = smem_u32(sK), sV_a = smem_u32(sV);
-    const int n_units = w_end - w_begin;
-    int s_unit = -1, s_j = 0, s_n = 0, s_cnt = 0;  // S stream cursor
-    auto s_more = [&]() { return s_j < s_n || s_unit + 1 < n_units; };
-    auto issue_s = [&]() {
-      if (s_j == s_n) {
-        // enter the next item: its record gives the tile count, its Q tile goes to TMEM
-        ++s_unit;
-        s_j = 0;
-        mbar_wait(&info_full[s_unit % kInfo], (s_unit / kInfo) & 1);
-        s_n = __shfl_sync(0xFFFFFFFFu, epi[(s_unit % kEpiRing) * kEpiInts + 4], 0);
-        mbar_wait(q_full, s_unit & 1);
-        tc_fence_after();
-        const uint64_t q0 = umma_sdesc_sw128(sQ_a, 16, 1024);
-        if (elect_one()) {
-#pragma unroll
-          for (int ks = 0; ks < HD / 16; ++ks)
-            tmem_cp_128x256b(tm_qt + ks * 8, q0 + (((ks >> 2) * (kBlockM * 128) + (ks & 3) * 32) >> 4));
-          umma_commit(q_empty);  // the smem tile is free once the copies land
-        }
+        if (elect_one()) mbar_arrive(&info_empty[ib]);
         __syncwarp();
       }
-      const int t = s_cnt;
-      const int b = t % kSBuf;
-      const int st = t % KST;
-      if (lane == 0) trace(p, 12, t);
-      mbar_wait(&k_full[st], (t / KST) & 1);
-      tc_fence_after();
-      if (lane == 0) trace(p, 1, t);
-      const uint32_t d = tm_s0 + b * kTileN;
-      const uint64_t b0 = umma_sdesc_sw128(sK_a + st * L::KT_BYTES, 16, 1024);
-      if (elect_one()) {
+    } else if (warp == 9) {
+      // ------------------------------------------------------------ MMA issuer
+      // One stream of tiles over the CTA's work items.  S(t) = Q K^T goes to S/P buffer
+      // t % 3 with A = the item's Q tile in TMEM (copied from smem by tcgen05.cp when
+      // the S stream enters the item) and B = the K tile; PV(t) accumulates
+      // P(t) (TMEM, TS-MMA) x V into O_{j&1} of its item.  S runs three tiles ahead
+      // of PV, across item boundaries: the in-order tensor pipe retires PV(t) before
+      // S(t+3) overwrites the buffer holding P(t), and the last S of an item before the
+      // next item's Q copy overwrites the Q columns.  The whole warp runs the loop
+      // (warp-uniform operands in uniform registers); one elected lane issues.
+      constexpr uint32_t idesc_s = umma_idesc_bf16(kBlockM, kTileN, false, false);
+      // PV: A = P from TMEM, B = V (MN-major).  fp16 V cache: one fp16 P plane;
+      // bf16 V cache: P = hi + lo bf16 planes, two MMAs per k-step.
+      constexpr uint32_t idesc_o = VF16 ? umma_idesc_f16(kBlockM, HD, false, true, 0u, 0u)
+                                        : umma_idesc_bf16(kBlockM, HD, false, true);
+      const uint32_t sQ_a = smem_u32(sQ), sK_a = smem_u32(sK), sV_a = smem_u32(sV);
+      const int n_units = w_end - w_begin;
+      int s_unit = -1, s_j = 0, s_n = 0, s_cnt = 0;  // S stream cursor
+      auto s_more = [&]() { return s_j < s_n || s_unit + 1 < n_units; };
+      auto issue_s = [&]() {
+        if (s_j == s_n) {
+          // enter the next item: its record gives the tile count, its Q tile goes to TMEM
+          ++s_unit;
+          s_j = 0;
+          mbar_wait(&info_full[s_unit % kInfo], (s_unit / kInfo) & 1);
+          s_n = __shfl_sync(0xFFFFFFFFu, epi[(s_unit % kEpiRing) * kEpiInts + 4], 0);
+          mbar_wait(q_full, s_unit & 1);
+          tc_fence_after();
+          const uint64_t q0 = umma_sdesc_sw128(sQ_a, 16, 1024);
+          if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks) {
-          if (p.dbg & 2) break;
-          // +32 B per k-step inside a 128 B swizzle row, +one 64-column box per 4
-          const uint64_t db = ((ks >> 2) * (kTileN * 128) + (ks & 3) * 32) >> 4;
-          umma_bf16_ts(d, tm_qt + ks * 8, b0 + db, idesc_s, ks > 0 ? 1u : 0u);
-        }
-        umma_commit(&s_full[b]);
-        umma_commit(&k_empty[st]);
-      }
-      __syncwarp();
-      ++s_cnt;
-      ++s_j;
-    };
-    for (int i = 0; i < kSBuf && s_more(); ++i) issue_s();
-    int t = 0;  // PV stream position
-    for (int u = 0; u < n_units; ++u) {
-      const int n_tiles = __shfl_sync(0xFFFFFFFFu, epi[(u % kEpiRing) * kEpiInts + 4], 0);
-      mbar_wait(o_empty, (u & 1) ^ 1);  // the previous item's epilogue has read O_0/O_1
-      tc_fence_after();
-      for (int j = 0; j < n_tiles; ++j, ++t) {
-        const int h = j & 1;
-        const int b = t % kSBuf;
-        const int st = t % VST;
-        if (lane == 0) trace(p, 8, t);
-        mbar_wait(&v_full[st], (t / VST) & 1);
-        if (lane == 0) trace(p, 9, t);
-        mbar_wait(&p_full[b], (t / kSBuf) & 1);
-        tc_fence_after();
-        if (lane == 0) trace(p, 7, t);
-        const uint32_t d = tm_o0 + h * HD;
-        const uint32_t pa = tm_s0 + b * kTileN;  // P (hi) at +0..31, bf16 lo plane at +32..63
-        const uint64_t b0 = umma_sdesc_sw128(sV_a + st * L::KT_BYTES, kTileN * 128, 1024);
-        if (elect_one()) {
-#pragma unroll
-          for (int ks = 0; ks < kTileN / 16; ++ks) {
-            if (p.dbg & 8) break;
-            const uint64_t bd = b0 + ((ks * 16 * 128) >> 4);  // 16 keys = 16 rows of 128 B
-            umma_bf16_ts(d, pa + ks * 8, bd, idesc_o, (j > 1 || ks > 0) ? 1u : 0u);
-            if (!VF16 && !(p.dbg & 1)) umma_bf16_ts(d, pa + 32 + ks * 8, bd, idesc_o, 1u);
+            for (int ks = 0; ks < HD / 16; ++ks)
+              tmem_cp_128x256b(tm_qt + ks * 8, q0 + (((ks >> 2) * (kBlockM * 128) + (ks & 3) * 32) >> 4));
+            umma_commit(q_empty);  // the smem tile is free once the copies land
           }
-          umma_commit(&pv_done[b]);
-          umma_commit(&v_empty[st]);
-          // the item's accumulator is complete after its last PV
-          if (j == n_tiles - 1) umma_commit(o_full);
+          __syncwarp();
         }
-        __syncwarp();
-        if (s_more()) issue_s();
-      }
-    }
-  } else if (warp == 11) {
-    // ------------------------------------------------------------ metadata warp
-    // Stages work items into the kInfo-deep record ring.  The work records and the
-    // per-request scalars of up to 32 items are fetched once per batch (lane k holds
-    // item k); per item the warp then only issues asynchronous 4-byte copies of the
-    // page ids, query positions and visibility words, so several items' copies are
-    // in flight at once and the ring fills at the memory system's throughput, not
-    // one dependent round trip chain per item.
-    for (int base = w_begin; base < w_end; base += 32) {
-      const int nb = min(32, w_end - base);
-      int f[8];
-      if (lane < nb) {
-        const int4* wp = reinterpret_cast<const int4*>(p.work + 8 * (base + lane));
-        const int4 a = __ldg(wp), b = __ldg(wp + 1);
-        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-      } else {
+        const int t = s_cnt;
+        const int b = t % kSBuf;
+        const int st = t % KST;
+        if (lane == 0) trace(p, 12, t);
+        mbar_wait(&k_full[st], (t / KST) & 1);
+        tc_fence_after();
+        if (lane == 0) trace(p, 1, t);
+        const uint32_t d = tm_s0 + b * kTileN;
+        const uint64_t b0 = umma_sdesc_sw128(sK_a + st * L::KT_BYTES, 16, 1024);
+        if (elect_one()) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = 0;
-      }
-      int prompt_l = 0, vb_l = 0, voff_l = 0;
-      if (lane < nb) {
-        prompt_l = __ldg(p.prompt_len + f[0]);
-        vb_l = __ldg(p.vis_base + f[0]);
-        voff_l = __ldg(p.vis_off + f[0]);
-      }
-      for (int k = 0; k < nb; ++k) {
-        const int unit = base - w_begin + k;
-        const int ib = unit % kInfo;
-        const int req = __shfl_sync(0xFFFFFFFFu, f[0], k);
-        const int head = __shfl_sync(0xFFFFFFFFu, f[1], k);
-        const int tok_begin = __shfl_sync(0xFFFFFFFFu, f[2], k);
-        const int n_tok = __shfl_sync(0xFFFFFFFFu, f[3], k);
-        const int key_begin = __shfl_sync(0xFFFFFFFFu, f[4], k);
-        const int key_end = __shfl_sync(0xFFFFFFFFu, f[5], k);
-        const int slot = __shfl_sync(0xFFFFFFFFu, f[6], k);
-        const int prompt = __shfl_sync(0xFFFFFFFFu, prompt_l, k);
-        const int vb = __shfl_sync(0xFFFFFFFFu, vb_l, k);
-        const int voff = __shfl_sync(0xFFFFFFFFu, voff_l, k);
-        mbar_wait(&info_empty[ib], ((unit / kInfo) & 1) ^ 1);
-        UnitInfo& u = info[ib];
-        const int pg0 = key_begin >> p.page_shift;
-        const int npg = min(((key_end - 1) >> p.page_shift) - pg0 + 1, kMaxUnitPages);
-        const int32_t* bt = p.block_tables + static_cast<int64_t>(req) * p.max_pages + pg0;
-        for (int i = lane; i < npg; i += 32) cp_async_4(&u.pages[i], bt + i);
-        for (int i = lane; i < n_tok; i += 32) cp_async_4(&u.qpos[i], p.q_pos + tok_begin + i);
-        const int nw = key_end > vb ? (key_end - vb + 31) / 32 : 0;
-        if (nw <= kMaxUnitWords && lane < nw) cp_async_4(&u.words[lane], p.vis_words + voff + lane);
-        cp_async_arrive_noinc(&info_full[ib]);
-        if (lane < kEpiInts) {
-          const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
-          const int v = lane == 0 ? head : lane == 1 ? tok_begin : lane == 2 ? n_tok
-                      : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
-          epi[(unit % kEpiRing) * kEpiInts + lane] = v;
-        }
-        if (lane < 11) {
-          const int v = lane == 0 ? req : lane == 1 ? head : lane == 2 ? tok_begin : lane == 3 ? n_tok
-                      : lane == 4 ? key_begin : lane == 5 ? key_end : lane == 6 ? slot : lane == 7 ? vb
-                      : lane == 8 ? nw : lane == 9 ? voff : prompt;
-          (&u.req)[lane] = v;
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            if (p.dbg & 2) break;
+            // +32 B per k-step inside a 128 B swizzle row, +one 64-column box per 4
+            const uint64_t db = ((ks >> 2) * (kTileN * 128) + (ks & 3) * 32) >> 4;
+            umma_bf16_ts(d, tm_qt + ks * 8, b0 + db, idesc_s, ks > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[b]);
+          umma_commit(&k_empty[st]);
         }
         __syncwarp();
-        if (lane == 0) {
-          trace(p, 6, 5 + unit);
-          mbar_arrive(&info_full[ib]);
+        ++s_cnt;
+        ++s_j;
+      };
+      for (int i = 0; i < kSBuf && s_more(); ++i) issue_s();
+      int t = 0;  // PV stream position
+      for (int u = 0; u < n_units; ++u) {
+        const int n_tiles = __shfl_sync(0xFFFFFFFFu, epi[(u % kEpiRing) * kEpiInts + 4], 0);
+        mbar_wait(o_empty, (u & 1) ^ 1);  // the previous item's epilogue has read O_0/O_1
+        tc_fence_after();
+        for (int j = 0; j < n_tiles; ++j, ++t) {
+          const int h = j & 1;
+          const int b = t % kSBuf;
+          const int st = t % VST;
+          if (lane == 0) trace(p, 8, t);
+          mbar_wait(&v_full[st], (t / VST) & 1);
+          if (lane == 0) trace(p, 9, t);
+          mbar_wait(&p_full[b], (t / kSBuf) & 1);
+          tc_fence_after();
+          if (lane == 0) trace(p, 7, t);
+          const uint32_t d = tm_o0 + h * HD;
+          const uint32_t pa = tm_s0 + b * kTileN;  // P (hi) at +0..31, bf16 lo plane at +32..63
+          const uint64_t b0 = umma_sdesc_sw128(sV_a + st * L::KT_BYTES, kTileN * 128, 1024);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < kTileN / 16; ++ks) {
+              if (p.dbg & 8) break;
+              const uint64_t bd = b0 + ((ks * 16 * 128) >> 4);  // 16 keys = 16 rows of 128 B
+              umma_bf16_ts(d, pa + ks * 8, bd, idesc_o, (j > 1 || ks > 0) ? 1u : 0u);
+              if (!VF16 && !(p.dbg & 1)) umma_bf16_ts(d, pa + 32 + ks * 8, bd, idesc_o, 1u);
+            }
+            umma_commit(&pv_done[b]);
+            umma_commit(&v_empty[st]);
+            // the item's accumulator is complete after its last PV
+            if (j == n_tiles - 1) umma_commit(o_full);
+          }
+          __syncwarp();
+          if (s_more()) issue_s();
+        }
+      }
+    } else if (warp == 11) {
+      // ------------------------------------------------------------ metadata warp
+      // Stages work items into the kInfo-deep record ring.  The work records and the
+      // per-request scalars of up to 32 items are fetched once per batch (lane k holds
+      // item k); per item the warp then only issues asynchronous 4-byte copies of the
+      // page ids, query positions and visibility words, so several items' copies are
+      // in flight at once and the ring fills at the memory system's throughput, not
+      // one dependent round trip chain per item.
+      for (int base = w_begin; base < w_end; base += 32) {
+        const int nb = min(32, w_end - base);
+        int f[8];
+        if (lane < nb) {
+          const int4* wp = reinterpret_cast<const int4*>(p.work + 8 * (base + lane));
+          const int4 a = __ldg(wp), b = __ldg(wp + 1);
+          f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = 0;
+        }
+        int prompt_l = 0, vb_l = 0, voff_l = 0;
+        if (lane < nb) {
+          prompt_l = __ldg(p.prompt_len + f[0]);
+          vb_l = __ldg(p.vis_base + f[0]);
+          voff_l = __ldg(p.vis_off + f[0]);
+        }
+        for (int k = 0; k < nb; ++k) {
+          const int unit = base - w_begin + k;
+          const int ib = unit % kInfo;
+          const int req = __shfl_sync(0xFFFFFFFFu, f[0], k);
+          const int head = __shfl_sync(0xFFFFFFFFu, f[1], k);
+          const int tok_begin = __shfl_sync(0xFFFFFFFFu, f[2], k);
+          const int n_tok = __shfl_sync(0xFFFFFFFFu, f[3], k);
+          const int key_begin = __shfl_sync(0xFFFFFFFFu, f[4], k);
+          const int key_end = __shfl_sync(0xFFFFFFFFu, f[5], k);
+          const int slot = __shfl_sync(0xFFFFFFFFu, f[6], k);
+          const int prompt = __shfl_sync(0xFFFFFFFFu, prompt_l, k);
+          const int vb = __shfl_sync(0xFFFFFFFFu, vb_l, k);
+          const int voff = __shfl_sync(0xFFFFFFFFu, voff_l, k);
+          mbar_wait(&info_empty[ib], ((unit / kInfo) & 1) ^ 1);
+          UnitInfo& u = info[ib];
+          const int pg0 = key_begin >> p.page_shift;
+          const int npg = min(((key_end - 1) >> p.page_shift) - pg0 + 1, kMaxUnitPages);
+          const int32_t* bt = p.block_tables + static_cast<int64_t>(req) * p.max_pages + pg0;
+          for (int i = lane; i < npg; i += 32) cp_async_4(&u.pages[i], bt + i);
+          for (int i = lane; i < n_tok; i += 32) cp_async_4(&u.qpos[i], p.q_pos + tok_begin + i);
+          const int nw = key_end > vb ? (key_end - vb + 31) / 32 : 0;
+          if (nw <= kMaxUnitWords && lane < nw) cp_async_4(&u.words[lane], p.vis_words + voff + lane);
+          cp_async_arrive_noinc(&info_full[ib]);
+          if (lane < kEpiInts) {
+            const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
+            const int v = lane == 0 ? head : lane == 1 ? tok_begin : lane == 2 ? n_tok
+                        : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
+            epi[(unit % kEpiRing) * kEpiInts + lane] = v;
+          }
+          if (lane < 11) {
+            const int v = lane == 0 ? req : lane == 1 ? head : lane == 2 ? tok_begin : lane == 3 ? n_tok
+                        : lane == 4 ? key_begin : lane == 5 ? key_end : lane == 6 ? slot : lane == 7 ? vb
+                        : lane == 8 ? nw : lane == 9 ? voff : prompt;
+            (&u.req)[lane] = v;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            trace(p, 6, 5 + unit);
+            mbar_arrive(&info_full[ib]);
+          }
         }
       }
     }
-  } else if (warp < 8) {
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kMathRegs));
     // ------------------------------------------------------------ softmax + epilogue
     // Two warpgroups ping-pong over the tiles of a work item (h = tile & 1), each
     // with its own running max m_h, sum l_h and TMEM accumulator O_h; the epilogue
