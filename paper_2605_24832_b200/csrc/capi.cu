@@ -521,27 +521,70 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     for (double l : loads) span_c = std::max(span_c, l);
   }
 
-  // Prefer whole units unless cutting buys >3% of the makespan, net of the split
-  // combine launch and partial traffic it brings (kCombine, measured).
-  const bool c_better = span_c < span_b;
-  const double span_cut = c_better ? span_c : span_b;
-  bool use_b = span_cut + kCombine < 0.97 * span_a &&
-               static_cast<int>((c_better ? pc_ : pb).size()) <= max_work;
-  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE")) {  // diagnostics: "whole" | "cut" | "flat"
-    use_b = (std::strcmp(f, "cut") == 0 || std::strcmp(f, "flat") == 0);
-    if (use_b) {
-      std::vector<Piece>& want = std::strcmp(f, "flat") == 0 ? pc_ : pb;
-      use_b = static_cast<int>(want.size()) <= max_work;
+  // ---- candidate D: halve the giants.  Only the units costlier than the mean CTA load
+  // are cut, into the fewest equal pieces that fit it; then LPT over pieces and whole
+  // units alike.  (B cuts whatever overflows as it places, which scatters small pieces
+  // over many CTAs; D leaves every other unit whole.)
+  std::vector<Piece> pd;
+  double span_d = 1e300;
+  if (!a_good) {
+    struct Job {
+      double cost;
+      int unit, t0, nt;
+      bool cut;
+    };
+    std::vector<Job> jobs;
+    jobs.reserve(nu + 2 * grid);
+    for (int ui : order) {
+      const int tiles = units[ui].tiles;
+      int k = std::max(1, (tiles + hard_cap - 1) / hard_cap);
+      if (tiles + kItem > lb && tiles >= 2 * min_split_tiles)
+        k = std::max(k, std::min(tiles / min_split_tiles, static_cast<int>(std::ceil((tiles + kItem) / lb))));
+      const int base = tiles / k, rem = tiles % k;
+      int t0 = 0;
+      for (int q = 0; q < k; ++q) {
+        const int nt = base + (q < rem ? 1 : 0);
+        jobs.push_back({nt + kItem + (k > 1 ? kSplit : 0.0), ui, t0, nt, k > 1});
+        t0 += nt;
+      }
+    }
+    std::stable_sort(jobs.begin(), jobs.end(), [](const Job& a, const Job& b) { return a.cost > b.cost; });
+    typedef std::pair<double, int> LoadCta;
+    std::vector<LoadCta> heap;
+    heap.reserve(grid);
+    for (int c = 0; c < grid; ++c) heap.push_back(LoadCta(0.0, c));
+    auto cmp = [](const LoadCta& a, const LoadCta& b) { return a > b; };
+    pd.reserve(jobs.size());
+    span_d = 0;
+    for (const Job& j : jobs) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      LoadCta& lc = heap.back();
+      pd.push_back({j.unit, j.t0, j.nt, lc.second});
+      lc.first += j.cost;
+      span_d = std::max(span_d, lc.first);
+      std::push_heap(heap.begin(), heap.end(), cmp);
     }
   }
-  const bool use_c = use_b && (std::getenv("OPTIMUS_PLAN_FORCE") ? std::strcmp(std::getenv("OPTIMUS_PLAN_FORCE"), "flat") == 0
-                                                                 : c_better);
-  const std::vector<Piece>& P = use_b ? (use_c ? pc_ : pb) : pa;
+
+  // Prefer whole units unless cutting buys >3% of the makespan, net of the split
+  // combine launch and partial traffic it brings (kCombine, measured).
+  int which = 0;  // 0 whole, 1 LPT-cut, 2 flat, 3 giants halved
+  double span_cut = span_b;
+  which = 1;
+  if (span_c < span_cut) span_cut = span_c, which = 2;
+  if (span_d < span_cut) span_cut = span_d, which = 3;
+  const std::vector<Piece>* cand[4] = {&pa, &pb, &pc_, &pd};
+  if (!(span_cut + kCombine < 0.97 * span_a) || static_cast<int>(cand[which]->size()) > max_work) which = 0;
+  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE")) {  // diagnostics: whole | cut | flat | giants
+    which = std::strcmp(f, "cut") == 0 ? 1 : std::strcmp(f, "flat") == 0 ? 2 : std::strcmp(f, "giants") == 0 ? 3 : 0;
+    if (cand[which]->empty() || static_cast<int>(cand[which]->size()) > max_work) which = 0;
+  }
+  const std::vector<Piece>& P = *cand[which];
   if (static_cast<int>(P.size()) > max_work) return fail("attn_plan: work buffer too small");
   if (std::getenv("OPTIMUS_PLAN_DEBUG"))
     std::fprintf(stderr, "attn_plan: whole-unit LPT span %.1f (%zu items), cutting LPT %.1f (%zu items), "
-                 "flat %.1f (%zu items) -> %s\n", span_a, pa.size(), span_b, pb.size(), span_c, pc_.size(),
-                 use_b ? (use_c ? "flat" : "cut") : "whole");
+                 "flat %.1f (%zu items), giants %.1f (%zu items) -> %d\n", span_a, pa.size(), span_b, pb.size(),
+                 span_c, pc_.size(), span_d, pd.size(), which);
   // Split groups: the pieces of a unit, in key order, get consecutive partial slots.
   std::vector<int> byu(P.size());
   for (size_t x = 0; x < P.size(); ++x) byu[x] = static_cast<int>(x);
