@@ -589,8 +589,12 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
   if (warp == 0) {
     // 3a. pieces per unit: the page cap, and with allow_cut a balanced cut of every
     // unit costlier than the per-CTA budget (mean load + one item) when the longest
-    // unit exceeds the budget by more than the combine launch (the host planner's
-    // candidate-B rule, capacity permitting).
+    // unit exceeds the budget plus the combine (12 tiles) by more than 12%: the host
+    // planner's candidate-B rule with the margin measured for the loop graph, where a
+    // cut layer also pays the combine's pass over the partials behind K2 (ShareGPT
+    // closed-loop batches, tools/loop_parts.py --ab-cut: longest / (budget + combine)
+    // = 1.07 cut 3.2 and 1.4 us per layer slower than whole; 1.17 / 1.21 / 1.37 cut 3.8 /
+    // 5.9 / 7.5 us faster; profiles/r2az_device_cut_rule.md), capacity permitting.
     long long total = 0;
     for (int u = lane; u < nu; u += 32) total += 2LL * u_tiles[u] + 5;
 #pragma unroll
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     const long long budget = (total + grid - 1) / grid + 5;
     const long long longest = nu > 0 ? 2LL * u_tiles[static_cast<int>(keys[0] & 0xFFFFFFFFu)] + 5 : 0;
     const int nt_max = static_cast<int>(max(4LL, (budget - 8) / 2));
-    bool cut = allow_cut && 100 * (budget + 24) < 97 * longest;  // + the combine (12 tiles)
+    bool cut = allow_cut && 100 * (budget + 24) < 89 * longest;  // + the combine (12 tiles)
     for (int pass = 0; pass < 2; ++pass) {
       int pieces = 0, cut_units = 0;
       for (int u = lane; u < nu; u += 32) {

@@ -24,6 +24,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="sharegpt")
 ap.add_argument("--chunk", type=int, default=32)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--between", default="k1", choices=["k1", "combine0", "combine0+k1"],
+                help="what runs between K2(0) and K2(1): K1(1), a split-KV combine with a device "
+                     "group count of 0 (the DeviceLoop's per-layer launch), or both")
 a = ap.parse_args()
 a.page, a.seed, a.steps, a.batch = 64, 0, 1, 64
 dev = torch.device("cuda")
@@ -49,6 +52,18 @@ def k2(l):
     kc, vc = dec.cache.layer(l)
     ops.paged_attention(q, kc, vc, dm.tok_pos, dm.prompt_len, dm.vis_base, dm.vis_off, dm.vis_words,
                         dm.block_tables, plan, cfg.block_size, out=out[: m.n_tok], ws_o=dec._ws_o, ws_ml=dec._ws_ml)
+
+
+zero = torch.zeros(4, dtype=torch.int32, device=dev)
+gdummy = torch.zeros((1, 8), dtype=torch.int32, device=dev)
+ws_dummy = torch.zeros(64 * 128 * 128, dtype=torch.float32, device=dev)  # never read: 0 groups
+
+
+def combine0():
+    _lib.check(_lib.call(
+        "optimus_paged_attn_combine_dev", gdummy.data_ptr(), zero.data_ptr(), 64, ws_dummy.data_ptr(),
+        ws_dummy.data_ptr(), cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, out.data_ptr(), out.stride(0),
+        torch.cuda.current_stream().cuda_stream), "combine_dev")
 
 
 tra = torch.zeros((plan.grid, 4096), dtype=torch.int64, device=dev)
@@ -77,7 +92,10 @@ with torch.cuda.stream(s_):
         k2(0)
         _lib.call("optimus_set_attn_trace", None)
         set_k1_trace(trk.data_ptr())
-        k1(1)
+        if a.between.startswith("combine0"):
+            combine0()
+        if a.between.endswith("k1"):
+            k1(1)
         set_k1_trace(None)
         _lib.call("optimus_set_attn_trace", trb.data_ptr())
         k2(1)
@@ -110,6 +128,7 @@ for rep in range(a.reps + 1):
         k1_end_max=(K[:, 4] - t0).max(), k1_blocks=len(K), k1_sms=len(set(K[:, 0].astype(int))),
         b_entry_min=b_entry.min(), b_entry_med=np.median(b_entry), b_entry_max=b_entry.max(),
         b_first_min=b_first.min(), b_first_med=np.median(b_first), b_done_last=b_done.max()))
+print(f"between: {a.between}")
 print(f"workload {a.workload}: K2 grid {plan.grid}, n_tok {m.n_tok}; times in us from K2(l)'s first CTA entry")
 for k in rows[0]:
     v = np.array([r[k] for r in rows])

@@ -25,13 +25,15 @@ ap.add_argument("--tps", default="1,2,4,8")
 ap.add_argument("--plans", default="auto,whole,cut,flat")
 ap.add_argument("--layers", type=int, default=36)
 ap.add_argument("--rounds", type=int, default=10)
+ap.add_argument("--seed-offset", type=int, default=0, help="another batch of the workload (bench: 0)")
 a = ap.parse_args()
 a.page, a.seed, a.steps, a.chunk = 64, 0, 1, 32
 a.batch = 128 if a.workload == "llada" else 64
 dev = torch.device("cuda")
 hbm, _ = bench.peaks()
 for tp in [int(t) for t in a.tps.split(",")]:
-    W = bench.build_decoder(a, dev, world=tp, rank=0, layers=a.layers, e2e_pools=False)
+    W = bench.build_decoder(a, dev, world=tp, rank=0, layers=a.layers, e2e_pools=False,
+                            reqs=bench.workload_requests(a, seed_offset=a.seed_offset) if a.seed_offset else None)
     dec, fwd, cfg = W.dec, W.fwd, W.cfg
     plans = plan_batch(W.reqs, bench.step_chunks(a, W.reqs), cfg.block_size, cfg.window_rule)
     dm = dec.prepare(W.reqs, plans)
