@@ -336,6 +336,20 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
                          int32_t* commits_out, int32_t* status, void* stream);
 
 /*
+ * Continuous batching on the device state (DeviceLoop.replace): copy n_adm admitted
+ * requests' packed rows into their batch slots with ONE launch.  `records` (device)
+ * holds n_adm records of optimus_admit_record_ints(state_stride, qcap, max_pages) int32:
+ * {slot, q_head, q_len, block_index, committed, steps_taken, cached_prefix, prompt,
+ * out_len, states row (state_stride bytes; state_stride % 4 == 0), queue row (qcap),
+ * block-table row (max_pages)}.
+ */
+int optimus_admit_record_ints(int64_t state_stride, int qcap, int max_pages);
+int optimus_device_admit(int n_adm, const int32_t* records, int8_t* states, int64_t state_stride, int32_t* queue,
+                         int qcap, int32_t* q_head, int32_t* q_len, int32_t* block_index, int32_t* committed,
+                         int32_t* steps_taken, int32_t* cached_prefix, int32_t* prompt, int32_t* out_len,
+                         int32_t* block_tables, int max_pages, void* stream);
+
+/*
  * Device twin of optimus_attn_plan (capi.cu) from device-resident cu_seqlens /
  * key_end (n_req <= 256, <= 4096 units and pieces, grid <= 1024).  allow_cut = 0:
  * its whole-unit placement (candidate A), output identical to the host planner under

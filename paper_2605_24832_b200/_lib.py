@@ -87,6 +87,9 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "optimus_device_apply": (_i32, [_i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _vp,
                                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "optimus_admit_record_ints": (_i32, [_i64, _i32, _i32]),
+    "optimus_device_admit": (_i32, [_i32, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _i32, _vp]),
     "optimus_device_attn_plan": (_i32, [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
                                         _vp, _vp]),
     "optimus_lmhead_splits": (_i32, [_i32]),

@@ -138,7 +138,8 @@ class BatchState:
         self.max_slots = max_slots
         self.max_out = max_out
         self.qcap = qcap
-        self.states = np.zeros((max_slots, max_out), dtype=np.int8)
+        # rows padded to 16 bytes: the device planner stages a row with 16-byte loads
+        self.states = np.zeros((max_slots, (max_out + 15) // 16 * 16), dtype=np.int8)
         self.queue = np.zeros((max_slots, qcap), dtype=np.int32)
         for f in self.FIELDS:
             setattr(self, f, np.zeros(max_slots, dtype=np.int32))

@@ -100,7 +100,23 @@ struct PlanArgs {
 
 __device__ __forceinline__ bool planned_bit(const uint32_t* bm, int p) { return (bm[p >> 5] >> (p & 31)) & 1u; }
 
+// Copy a request's state row (out positions, int8) into the warp's shared-memory slot:
+// one round trip of independent 16-byte loads (rows padded to 16 bytes, BatchState)
+// instead of a dependent global load per 32 positions in every scan below.
+__device__ __forceinline__ const int8_t* stage_row(int8_t* dst, const int8_t* src, int64_t stride, int out,
+                                                   int lane) {
+  if ((stride & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int nv = (out + 15) >> 4;  // <= stride / 16: the tail bytes are the row's padding
+    for (int i = lane; i < nv; i += 32) reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+  } else {
+    for (int i = lane; i < out; i += 32) dst[i] = src[i];
+  }
+  __syncwarp();
+  return dst;
+}
+
 __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) {
+  extern __shared__ __align__(16) int8_t stage_sm[];  // [kWarps][kMaxOut]: the warp's staged state row
   __shared__ uint32_t bitmap[kWarps][kMaxOut / 32];
   __shared__ int ntok_s[kMaxReq], nrow_s[kMaxReq], nword_s[kMaxReq], nkv_s[kMaxReq];
   __shared__ int ke_s[kMaxReq], vb_s[kMaxReq];
@@ -114,12 +130,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
   for (int r = warp; r < a.n; r += kWarps) {
     const int s = a.slots[r];
     const int out = a.out_len[s];
-    const int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
     const int chunk_r = a.chunk_per_req ? a.chunk_per_req[r] : a.chunk;
     if (chunk_r < 2 || chunk_r > kMaxChunk || out > kMaxOut) {
       if (lane == 0) bad = 1;
       continue;
     }
+    const int8_t* st = stage_row(stage_sm + warp * kMaxOut, a.states + static_cast<int64_t>(s) * a.stride, a.stride,
+                                 out, lane);
     // finished (no MASKED left in the current block, advance_blocks' invariant): nothing
     bool done;
     {
@@ -259,7 +276,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
   for (int r = warp; r < a.n; r += kWarps) {
     const int s = a.slots[r];
     const int out = a.out_len[s];
-    const int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
+    const int8_t* st = stage_row(stage_sm + warp * kMaxOut, a.states + static_cast<int64_t>(s) * a.stride, a.stride,
+                                 out, lane);
     const int t0 = a.cu_seqlens[r], r0 = a.cu_rows[r];
     const int nkv = nkv_s[r], nwin = nrow_s[r];
     // rebuild the planned bitmap and window of this request (pass 1's were per warp
@@ -347,28 +365,36 @@ struct ApplyArgs {
 // before it mutates, engine.py:83).  *status is sticky: the caller zeroes it (the
 // device loop shares it with the plan's counts[3], so a rejected plan skips apply).
 __global__ void __launch_bounds__(128) apply_validate_kernel(const ApplyArgs a) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per request: the lanes check the FIFO front and the committed rows in
+  // parallel (no dependent load chain per entry)
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (r >= a.n) return;
   const int s = a.slots[r];
   const int out = a.out_len[s];
   if (a.committed[s] >= out) return;
   const int8_t* st = a.states + static_cast<int64_t>(s) * a.stride;
   const int32_t* q = a.queue + static_cast<int64_t>(s) * a.qcap;
-  const int nkv = (a.cu_seqlens[r + 1] - a.cu_seqlens[r]) - (a.cu_rows[r + 1] - a.cu_rows[r]);
+  const int t0 = a.cu_seqlens[r], r0 = a.cu_rows[r], r1 = a.cu_rows[r + 1];
+  const int nkv = (a.cu_seqlens[r + 1] - t0) - (r1 - r0);
   const int head = a.q_head[s], len = a.q_len[s];
   bool ok = nkv >= 0 && nkv <= len;
-  for (int i = 0; i < nkv && ok; ++i) ok = q[(head + i) % a.qcap] == a.tok_pos[a.cu_seqlens[r] + i];
+  if (ok)
+    for (int i = lane; i < nkv; i += 32) ok = ok && q[(head + i) % a.qcap] == a.tok_pos[t0 + i];
   int k = 0;
-  for (int i = a.cu_rows[r]; i < a.cu_rows[r + 1] && ok; ++i) {
+  for (int i = r0 + lane; i < r1; i += 32) {
     if (!a.commit_mask[i]) continue;
     const int p = a.row_pos[i];
-    ok = p >= 0 && p < out && st[p] == MASKED;
+    ok = ok && p >= 0 && p < out && st[p] == MASKED;
     ++k;
   }
-  if (!ok || len - nkv + k > a.qcap) *a.status = OPTIMUS_EINVAL;
+  ok = __all_sync(0xFFFFFFFFu, ok);
+  k = __reduce_add_sync(0xFFFFFFFFu, k);
+  if (lane == 0 && (!ok || len - nkv + k > a.qcap)) *a.status = OPTIMUS_EINVAL;
 }
 
-// One warp per request (lane 0 walks the FIFO; the rest scan in parallel).
+// One warp per request: the KV plan's positions become CACHED and the commits (in
+// row order) are pushed onto the FIFO by all lanes at once; lane 0 updates the scalars.
 __global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -381,28 +407,31 @@ __global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
     if (lane == 0) a.commits_out[r] = 0;
     return;
   }
-  if (lane == 0) {  // validated: pop the KV plan, push the commits
-    const int nkv = (a.cu_seqlens[r + 1] - a.cu_seqlens[r]) - (a.cu_rows[r + 1] - a.cu_rows[r]);
-    int head = a.q_head[s], len = a.q_len[s];
-    for (int i = 0; i < nkv; ++i) {
-      st[a.tok_pos[a.cu_seqlens[r] + i]] = CACHED;
-      head = (head + 1) % a.qcap;
-      --len;
-    }
+  {  // validated: pop the KV plan, push the commits
+    const int t0 = a.cu_seqlens[r], r0 = a.cu_rows[r], r1 = a.cu_rows[r + 1];
+    const int nkv = (a.cu_seqlens[r + 1] - t0) - (r1 - r0);
+    for (int i = lane; i < nkv; i += 32) st[a.tok_pos[t0 + i]] = CACHED;
+    const int head = (a.q_head[s] + nkv) % a.qcap;
+    const int len = a.q_len[s] - nkv;
     int k = 0;
-    for (int i = a.cu_rows[r]; i < a.cu_rows[r + 1]; ++i) {
-      if (!a.commit_mask[i]) continue;
-      const int p = a.row_pos[i];
-      st[p] = UNCACHED;
-      q[(head + len) % a.qcap] = p;
-      ++len;
-      ++k;
+    for (int base = r0; base < r1; base += 32) {
+      const int i = base + lane;
+      const bool m = i < r1 && a.commit_mask[i];
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+      if (m) {
+        const int p = a.row_pos[i];
+        st[p] = UNCACHED;
+        q[(head + len + k + __popc(bal & ((1u << lane) - 1u))) % a.qcap] = p;
+      }
+      k += __popc(bal);
     }
-    a.q_head[s] = head;
-    a.q_len[s] = len;
-    a.commits_out[r] = k;
-    a.committed[s] += k;
-    a.steps[s] += 1;
+    if (lane == 0) {
+      a.q_head[s] = head;
+      a.q_len[s] = len + k;
+      a.commits_out[r] = k;
+      a.committed[s] += k;
+      a.steps[s] += 1;
+    }
   }
   __syncwarp();
   // advance_blocks: skip blocks without MASKED positions
@@ -439,10 +468,62 @@ __global__ void __launch_bounds__(128) apply_kernel(const ApplyArgs a) {
   }
 }
 
+// Admissions: one block per admitted request copies its record into the slot's rows.
+__global__ void __launch_bounds__(256) admit_kernel(int n_adm, const int32_t* __restrict__ rec, int rec_ints,
+                                                    int8_t* states, int64_t stride, int32_t* queue, int qcap,
+                                                    int32_t* q_head, int32_t* q_len, int32_t* block_index,
+                                                    int32_t* committed, int32_t* steps, int32_t* cached_prefix,
+                                                    int32_t* prompt, int32_t* out_len, int32_t* tables,
+                                                    int max_pages) {
+  if (blockIdx.x >= n_adm) return;
+  const int32_t* r = rec + static_cast<int64_t>(blockIdx.x) * rec_ints;
+  const int s = r[0];
+  if (threadIdx.x == 0) {
+    q_head[s] = r[1];
+    q_len[s] = r[2];
+    block_index[s] = r[3];
+    committed[s] = r[4];
+    steps[s] = r[5];
+    cached_prefix[s] = r[6];
+    prompt[s] = r[7];
+    out_len[s] = r[8];
+  }
+  const int sw = static_cast<int>(stride / 4);
+  const int32_t* src = r + 9;
+  int32_t* st = reinterpret_cast<int32_t*>(states + static_cast<int64_t>(s) * stride);
+  for (int i = threadIdx.x; i < sw; i += blockDim.x) st[i] = src[i];
+  src += sw;
+  for (int i = threadIdx.x; i < qcap; i += blockDim.x) queue[static_cast<int64_t>(s) * qcap + i] = src[i];
+  src += qcap;
+  for (int i = threadIdx.x; i < max_pages; i += blockDim.x) tables[static_cast<int64_t>(s) * max_pages + i] = src[i];
+}
+
 }  // namespace dstep
 }  // namespace optimus
 
 extern "C" {
+
+int optimus_admit_record_ints(int64_t state_stride, int qcap, int max_pages) {
+  if (state_stride < 0 || state_stride % 4 || qcap < 0 || max_pages < 0) return OPTIMUS_EINVAL;
+  return static_cast<int>(9 + state_stride / 4 + qcap + max_pages);
+}
+
+int optimus_device_admit(int n_adm, const int32_t* records, int8_t* states, int64_t state_stride, int32_t* queue,
+                         int qcap, int32_t* q_head, int32_t* q_len, int32_t* block_index, int32_t* committed,
+                         int32_t* steps_taken, int32_t* cached_prefix, int32_t* prompt, int32_t* out_len,
+                         int32_t* block_tables, int max_pages, void* stream) {
+  using namespace optimus::dstep;
+  const int rec_ints = optimus_admit_record_ints(state_stride, qcap, max_pages);
+  if (n_adm < 0 || rec_ints < 0) return OPTIMUS_EINVAL;
+  if (n_adm == 0) return 0;
+  if (!records || !states || !queue || !q_head || !q_len || !block_index || !committed || !steps_taken ||
+      !cached_prefix || !prompt || !out_len || !block_tables)
+    return OPTIMUS_EINVAL;
+  admit_kernel<<<n_adm, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n_adm, records, rec_ints, states, state_stride, queue, qcap, q_head, q_len, block_index, committed,
+      steps_taken, cached_prefix, prompt, out_len, block_tables, max_pages);
+  return static_cast<int>(cudaGetLastError());
+}
 
 int optimus_device_plan(int n, const int32_t* slots, int chunk, const int32_t* chunk_per_req, int block,
                         int window_rule, const int8_t* states, int64_t state_stride, const int32_t* queue,
@@ -460,7 +541,14 @@ int optimus_device_plan(int n, const int32_t* slots, int chunk, const int32_t* c
              q_head, q_len, block_index, cached_prefix, prompt, out_len, block_tables, max_pages,
              cu_seqlens, tok_req, tok_pos, cap_tok, prompt_len, key_end, vis_base, vis_off, vis_words,
              cap_words, cu_rows, row_tok, row_pos, row_req, cap_rows, block_tables_out, counts};
-  plan_kernel<<<1, kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  constexpr int kStageSmem = kWarps * kMaxOut;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    configured = true;
+  }
+  plan_kernel<<<1, kWarps * 32, kStageSmem, static_cast<cudaStream_t>(stream)>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -476,7 +564,7 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
   ApplyArgs a{n, slots, block, cu_seqlens, tok_pos, cu_rows, row_pos, commit_mask, states, state_stride, queue,
               qcap, q_head, q_len, block_index, committed, steps_taken, cached_prefix, out_len, commits_out,
               status};
-  apply_validate_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  apply_validate_kernel<<<(n * 32 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   apply_kernel<<<(n * 32 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
@@ -841,11 +929,13 @@ extern "C" int optimus_device_attn_plan(int n_req, const int32_t* cu_seqlens, co
   const size_t smem = kMaxUnits * (8 + 12 * 4);
   static bool configured = false;
   if (!configured) {
+    cudaFuncSetAttribute(work_plan_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(work_plan_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(work_plan_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
-  auto kern = grid <= 256 ? work_plan_kernel<8> : work_plan_kernel<32>;
+  // CTA loads per lane: 5 covers one B200 (148 SMs); fewer registers to reduce per placed piece
+  auto kern = grid <= 160 ? work_plan_kernel<5> : grid <= 256 ? work_plan_kernel<8> : work_plan_kernel<32>;
   kern<<<1, kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       n_req, cu_seqlens, key_end, hkv, 128 / G, grid, hard_cap, allow_cut, work, max_work, cta_off, groups, max_groups,
       counts);

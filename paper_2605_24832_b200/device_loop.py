@@ -155,6 +155,14 @@ class DeviceLoop:
         self._last = (np.zeros(n + 1, np.int32), np.zeros(1, np.int32), np.zeros(1, np.uint8))
         self._h2d = 0
         self.h2d_bytes = self.d2h_bytes = 0
+        # admissions (replace) are packed into one record per request and copied into the
+        # device state by ONE H2D + ONE optimus_device_admit launch before the next replay
+        self._rec_ints = _lib.call("optimus_admit_record_ints", bs.states.shape[1], bs.qcap, self.Dt.shape[1])
+        _lib.check(min(self._rec_ints, 0), "optimus_admit_record_ints")
+        self._pending = []
+        self._adm_pin = torch.zeros((n, self._rec_ints), dtype=torch.int32, pin_memory=True)
+        self._adm_dev = torch.zeros((n, self._rec_ints), dtype=torch.int32, device=dev)
+        self._adm_ev = None  # the last staging copy (the pinned buffer is reused)
         if self.model:
             fwd.loop_setup(self)
 
@@ -302,6 +310,7 @@ class DeviceLoop:
             self.capture()
         if chunk is not None:
             self.set_chunk(chunk)
+        self.flush_admissions()
         # per-step copies: what this step's host calls staged (admissions, chunks) and the
         # plan arrays + commit mask every replay reads back
         self.h2d_bytes, self._h2d = self._h2d, 0
@@ -393,6 +402,7 @@ class DeviceLoop:
     def drain(self) -> None:
         """Wait for an in-flight lookahead iteration and discard it (its effects on
         the device state are kept: call only when every request has finished)."""
+        self.flush_admissions()
         if self._inflight:
             torch.cuda.current_stream().synchronize()
             self._inflight = False
@@ -411,18 +421,44 @@ class DeviceLoop:
         s = self.nat._slot(request, int(self.slots_h[i]))
         self.dec.tables.ensure(s, request.prompt_tokens + request.output_tokens)
         bs = self.bs
-        # pinned staging + async copies, stream-ordered after any in-flight iteration
-        # (the host caching allocator keeps each staging buffer until its copy ran)
-        for k in self.state_keys:
-            src = torch.from_numpy(np.ascontiguousarray(getattr(bs, k)[s : s + 1])).pin_memory()
-            self.D[k][s : s + 1].copy_(src, non_blocking=True)
-            self._h2d += src.numel() * src.element_size()
-        self.Dt[s].copy_(torch.from_numpy(self.dec.tables.table[s].copy()).pin_memory(), non_blocking=True)
-        self._h2d += self.Dt[s].numel() * 4
+        # the slot's packed rows as one record (flush_admissions copies them in)
+        rec = np.empty(self._rec_ints, dtype=np.int32)
+        rec[0] = s
+        for j, k in enumerate(("q_head", "q_len", "block_index", "committed", "steps_taken", "cached_prefix",
+                               "prompt", "out_len")):
+            rec[1 + j] = getattr(bs, k)[s]
+        sw = bs.states.shape[1] // 4
+        rec[9: 9 + sw] = np.ascontiguousarray(bs.states[s]).view(np.int32)
+        rec[9 + sw: 9 + sw + bs.qcap] = bs.queue[s]
+        rec[9 + sw + bs.qcap:] = self.dec.tables.table[s]
+        self._pending = [r for r in self._pending if r[0] != s] + [rec]
         self.requests[i] = request
         self.free.discard(i)
         if self._inflight:
             self._stale.add(i)
+
+    def flush_admissions(self) -> None:
+        """Copy the pending admissions into the device state: one H2D of the packed
+        records + one optimus_device_admit launch, stream-ordered after any in-flight
+        iteration (step() calls it before each replay)."""
+        if not self._pending:
+            return
+        recs = np.stack(self._pending)
+        m = len(recs)
+        if self._adm_ev is not None:
+            self._adm_ev.synchronize()  # the previous flush's copy has read the pinned buffer
+        self._adm_pin.numpy()[:m] = recs
+        self._adm_dev[:m].copy_(self._adm_pin[:m], non_blocking=True)
+        D, p = self.D, lambda t: t.data_ptr()
+        _lib.check(_lib.call(
+            "optimus_device_admit", m, p(self._adm_dev), p(D["states"]), D["states"].shape[1], p(D["queue"]),
+            self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
+            p(D["steps_taken"]), p(D["cached_prefix"]), p(D["prompt"]), p(D["out_len"]), p(self.Dt),
+            self.Dt.shape[1], torch.cuda.current_stream().cuda_stream), "optimus_device_admit")
+        self._adm_ev = torch.cuda.Event()
+        self._adm_ev.record()
+        self._h2d += recs.nbytes
+        self._pending = []
 
     def finished(self) -> bool:
         return all(r.finished for r in self.requests)

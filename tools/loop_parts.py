@@ -82,8 +82,7 @@ for label, skip in (("graph", ()), ("graph without combine launches", ("optimus_
     res[label] = graph_us(L.graphs[0])
     print(f"{label:34s} {res[label]:8.1f} us  (split groups {groups})")
 
-# the planners alone, eager back to back on the last loop's state (pure functions)
-s = torch.cuda.current_stream().cuda_stream
+# the planners alone, back to back on the last loop's state (pure functions)
 cfg, D, M, n = L.cfg, L.D, L.M, L.n
 ct, cr, cw = L.caps
 p = lambda t: t.data_ptr()
@@ -91,6 +90,7 @@ rule = 0
 
 
 def plan():
+    s = torch.cuda.current_stream().cuda_stream
     _lib.check(_lib.call(
         "optimus_device_plan", n, p(L.slots), L.chunk, p(L.chunks_d), cfg.block_size, rule, p(D["states"]),
         D["states"].shape[1], p(D["queue"]), L.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]),
@@ -101,6 +101,7 @@ def plan():
 
 
 def wplan():
+    s = torch.cuda.current_stream().cuda_stream
     _lib.check(_lib.call(
         "optimus_device_attn_plan", n, p(M["cu_seqlens"]), p(M["key_end"]), cfg.num_q_heads, cfg.num_kv_heads,
         L.grid, cfg.page_size, 1, p(M["work"]), L.max_work, p(M["cta_off"]), p(M["groups"]),
@@ -110,8 +111,40 @@ def wplan():
 for label, fn in (("optimus_device_plan", plan), ("optimus_device_attn_plan", wplan)):
     g = torch.cuda.CUDAGraph()
     fn(); torch.cuda.synchronize()
-    with torch.cuda.graph(g):
+    with torch.cuda.graph(g):  # (captures on its own stream: current_stream() inside)
         for _ in range(10):
             fn()
     print(f"{label:34s} {graph_us(g) / 10:8.1f} us per launch (10 in one graph)")
+# apply mutates the state: time (restore + apply) minus (restore) graphs
+snap = {k: v.clone() for k, v in D.items()}
+
+
+def restore():
+    for k, v in snap.items():
+        D[k].copy_(v)
+
+
+def apply():
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.call(
+        "optimus_device_apply", n, p(L.slots), cfg.block_size, p(M["cu_seqlens"]), p(M["tok_pos"]),
+        p(M["cu_rows"]), p(M["row_pos"]), p(L.res.commit_mask), p(D["states"]), D["states"].shape[1],
+        p(D["queue"]), L.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
+        p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["counts"][3:]),
+        s), "device_apply")
+
+
+gs = {}
+for label, fns in (("restore", (restore,)), ("restore+apply", (restore, apply))):
+    g = torch.cuda.CUDAGraph()
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        for _ in range(10):
+            for f in fns:
+                f()
+    gs[label] = graph_us(g) / 10
+restore()
+print(f"{'optimus_device_apply':34s} {gs['restore+apply'] - gs['restore']:8.1f} us per launch pair (validate + apply)")
 print(f"n_tok {int(M['counts'][0])} rows {int(M['counts'][1])} work {int(M['wcounts'][0])}")
