@@ -123,7 +123,21 @@ class DeviceLoop:
         # split-KV partials (m, l, O) of the cut pieces: at most one per work item
         self.ws_o = torch.empty(self.max_work * 128 * cfg.head_dim, dtype=torch.float32, device=dev)
         self.ws_ml = torch.empty(self.max_work * 128 * 2, dtype=torch.float32, device=dev)
-        M["wcounts"] = z(4)
+        # what the host replay reads back every iteration lives in ONE device buffer
+        # (16-byte aligned views), so each iteration ends with one D2H copy, not seven
+        rb = [("counts", 4), ("wcounts", 4), ("cu_seqlens", n + 1), ("tok_pos", max(ct, 1)),
+              ("cu_rows", n + 1), ("row_pos", max(cr, 1)), ("mask", (max(cr, 1) + 3) // 4)]
+        offs, o = {}, 0
+        for k, m in rb:
+            offs[k] = (o, m)
+            o += -(-m // 4) * 4
+        self._rb = torch.zeros(o, dtype=torch.int32, device=dev)
+        for k, (o0, m) in offs.items():
+            if k != "mask":
+                M[k] = self._rb[o0: o0 + m]
+        o0, m = offs["mask"]
+        mask_d = self._rb[o0: o0 + m].view(torch.uint8)[: max(cr, 1)]
+        self._rb_offs = offs
         self.M = M
         vocab = cfg.vocab if self.model else fwd.logit_table.shape[-1]
         self.logits = None if self.model else fwd.logit_table
@@ -131,15 +145,16 @@ class DeviceLoop:
         self.n_vsplit = ops.unmask_splits(max(cr // 2, 1), vocab)
         self.part = torch.empty((cr, self.n_vsplit, 3), dtype=torch.float32, device=dev)
         self.k3_counters = torch.zeros(n, dtype=torch.int32, device=dev)  # unmask_fused arrivals (zero between steps)
-        self.res = ops.UnmaskResult(z(cr, torch.uint8), z(cr), z(cr, torch.float32))
+        self.res = ops.UnmaskResult(mask_d, z(cr), z(cr, torch.float32))
         self.out = torch.empty((ct, cfg.num_q_heads, cfg.head_dim), dtype=torch.bfloat16, device=dev)
         # pinned host mirrors of what the host replay needs
         # with lookahead two graphs alternate, each reading back into its own buffers, so
         # the next iteration is launched before this one's results are read
         def host_mirror():
-            H = {k: torch.zeros(M[k].numel(), dtype=torch.int32, pin_memory=True)
-                 for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos")}
-            H["mask"] = torch.zeros(max(cr, 1), dtype=torch.uint8, pin_memory=True)
+            buf = torch.zeros(self._rb.numel(), dtype=torch.int32, pin_memory=True)
+            H = {"_all": buf}
+            for k, (o0, m) in offs.items():
+                H[k] = buf[o0: o0 + m] if k != "mask" else buf[o0: o0 + m].view(torch.uint8)[: max(cr, 1)]
             H["vsat"] = torch.zeros(2, dtype=torch.int32, pin_memory=True)  # fp16 V clamp flags
             return H
         self.Hs = [host_mirror() for _ in range(2 if lookahead else 1)]
@@ -227,9 +242,7 @@ class DeviceLoop:
             p(D["queue"]), self.bs.qcap, p(D["q_head"]), p(D["q_len"]), p(D["block_index"]), p(D["committed"]),
             p(D["steps_taken"]), p(D["cached_prefix"]), p(D["out_len"]), p(M["commits"]), p(M["counts"][3:]),
             stream), "device_apply")  # apply's status = the plan's counts[3]: a rejected plan skips apply
-        for k in ("counts", "wcounts", "cu_seqlens", "tok_pos", "cu_rows", "row_pos"):
-            H[k].copy_(M[k], non_blocking=True)
-        H["mask"][: self.res.commit_mask.numel()].copy_(self.res.commit_mask, non_blocking=True)
+        H["_all"].copy_(self._rb, non_blocking=True)  # counts, plan arrays and commit mask at once
         if self.dec.v_gate is not None:  # fp16 V clamp flags, read after the iteration completed
             _lib.check(L.call("optimus_v_saturated", H["vsat"].data_ptr(), 1, stream), "optimus_v_saturated")
 
@@ -314,7 +327,7 @@ class DeviceLoop:
         # per-step copies: what this step's host calls staged (admissions, chunks) and the
         # plan arrays + commit mask every replay reads back
         self.h2d_bytes, self._h2d = self._h2d, 0
-        self.d2h_bytes = sum(v.numel() * v.element_size() for v in self.H.values())
+        self.d2h_bytes = (self.H["_all"].numel() + self.H["vsat"].numel()) * 4
         t0 = time.perf_counter()
         if not self.lookahead:
             self.graphs[0].replay()
