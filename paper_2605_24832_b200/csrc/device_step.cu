@@ -122,15 +122,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
   __shared__ int ke_s[kMaxReq], vb_s[kMaxReq];
   __shared__ int bad;
   __shared__ unsigned scan_ws[32];
+  // per-request scalars, loaded once for the whole batch (two parallel round trips)
+  // instead of a dependent chain of global loads inside each warp's request loop
+  __shared__ int sl_s[kMaxReq], out_s[kMaxReq], ch_s[kMaxReq], bi_s[kMaxReq], qh_s[kMaxReq], ql_s[kMaxReq];
+  __shared__ int cp_s[kMaxReq], pr_s[kMaxReq], t0_s[kMaxReq], r0_s[kMaxReq], vo_s[kMaxReq];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) bad = 0;
+  if (threadIdx.x < a.n) {
+    const int r = threadIdx.x;
+    const int s = a.slots[r];
+    sl_s[r] = s;
+    ch_s[r] = a.chunk_per_req ? a.chunk_per_req[r] : a.chunk;
+    out_s[r] = a.out_len[s];
+    bi_s[r] = a.block_index[s];
+    qh_s[r] = a.q_head[s];
+    ql_s[r] = a.q_len[s];
+    cp_s[r] = a.cached_prefix[s];
+    pr_s[r] = a.prompt[s];
+  }
   __syncthreads();
   uint32_t* bm = bitmap[warp];
   // ---- pass 1: counts, key_end, vis_base
   for (int r = warp; r < a.n; r += kWarps) {
-    const int s = a.slots[r];
-    const int out = a.out_len[s];
-    const int chunk_r = a.chunk_per_req ? a.chunk_per_req[r] : a.chunk;
+    const int s = sl_s[r];
+    const int out = out_s[r];
+    const int chunk_r = ch_s[r];
     if (chunk_r < 2 || chunk_r > kMaxChunk || out > kMaxOut) {
       if (lane == 0) bad = 1;
       continue;
@@ -140,15 +156,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
     // finished (no MASKED left in the current block, advance_blocks' invariant): nothing
     bool done;
     {
-      const int b0 = a.block_index[s] * a.block, b1 = min(b0 + a.block, out);
+      const int b0 = bi_s[r] * a.block, b1 = min(b0 + a.block, out);
       bool any = false;
       for (int base = b0; base < b1; base += 32)
         any = any || __any_sync(0xFFFFFFFFu, base + lane < b1 && st[base + lane] == MASKED);
       done = !any;
     }
-    const int nkv = done ? 0 : min(a.q_len[s], chunk_r);
+    const int nkv = done ? 0 : min(ql_s[r], chunk_r);
     int room = done ? 0 : chunk_r - nkv;
-    int lo = a.block_index[s] * a.block;
+    int lo = bi_s[r] * a.block;
     int hi = min(lo + a.block, out);
     if (a.window_rule == 1) {
       hi = out;
@@ -159,7 +175,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
     // kv positions: the FIFO front of the uncached ring
     int maxq = -1;
     for (int i = lane; i < nkv; i += 32) {
-      const int p = a.queue[static_cast<int64_t>(s) * a.qcap + (a.q_head[s] + i) % a.qcap];
+      const int p = a.queue[static_cast<int64_t>(s) * a.qcap + (qh_s[r] + i) % a.qcap];
       atomicOr(&bm[p >> 5], 1u << (p & 31));
       maxq = max(maxq, p);
     }
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
     }
     // rule V: visible = CACHED before the step, or planned now
     // cp: first position from cached_prefix on that is not visible
-    int cp = min(a.cached_prefix[s], out);
+    int cp = min(cp_s[r], out);
     while (true) {
       const int p = cp + lane;
       const bool v = p < out && (st[p] == CACHED || planned_bit(bm, p));
@@ -208,15 +224,37 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
     }
     cp = min(cp, out);
     const int cap_end = (maxq / a.block + 1) * a.block;
-    // last: the largest visible position
-    int last = -1;
-    for (int base = ((out - 1) / 32) * 32; base >= 0 && last < 0; base -= 32) {
-      const int p = base + lane;
-      const bool v = p < out && (st[p] == CACHED || planned_bit(bm, p));
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
-      if (bal) last = base + 31 - __clz(bal);
+    // last: the largest visible position = max(largest planned (maxq), largest CACHED);
+    // the CACHED one by a backward scan of the staged row, 16 positions per lane
+    int last = maxq;
+    {
+      const uint4* st4 = reinterpret_cast<const uint4*>(st);
+      const int nvec = (out + 15) >> 4;
+      for (int top = nvec - 1; top >= 0; top -= 32) {
+        const int j = top - lane;
+        int c = -1;
+        if (j >= 0) {
+          const uint4 v = st4[j];
+          uint32_t m[4] = {__vcmpeq4(v.x, 0x02020202u), __vcmpeq4(v.y, 0x02020202u), __vcmpeq4(v.z, 0x02020202u),
+                           __vcmpeq4(v.w, 0x02020202u)};  // CACHED == 2
+          const int lim = out - 16 * j;  // positions of this vector inside the row
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int nb = lim - 4 * q;
+            m[q] &= nb >= 4 ? 0xFFFFFFFFu : nb <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - nb)));
+          }
+#pragma unroll
+          for (int q = 3; q >= 0; --q)
+            if (c < 0 && m[q]) c = 16 * j + 4 * q + (31 - __clz(m[q])) / 8;
+        }
+        const int best = __reduce_max_sync(0xFFFFFFFFu, c);
+        if (best >= 0) {
+          last = max(last, best);
+          break;
+        }
+      }
     }
-    const int pr = a.prompt[s];
+    const int pr = pr_s[r];
     const int ke = pr + min(last + 1, cap_end);
     int vb = ((pr + cp) / 32) * 32;
     if (vb > ke) vb = (ke / 32) * 32;
@@ -239,7 +277,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
       a.vis_off[r] = static_cast<int>(w_pre);
       a.cu_seqlens[r + 1] = static_cast<int>(t_pre) + ntok_s[r];
       a.cu_rows[r + 1] = static_cast<int>(r_pre) + nrow_s[r];
-      a.prompt_len[r] = a.prompt[a.slots[r]];
+      a.prompt_len[r] = pr_s[r];
+      t0_s[r] = static_cast<int>(t_pre);
+      r0_s[r] = static_cast<int>(r_pre);
+      vo_s[r] = static_cast<int>(w_pre);
       a.key_end[r] = ke_s[r];
       a.vis_base[r] = vb_s[r];
     }
@@ -274,25 +315,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
   }
   // ---- pass 2: layouts, visibility words, block tables
   for (int r = warp; r < a.n; r += kWarps) {
-    const int s = a.slots[r];
-    const int out = a.out_len[s];
+    const int s = sl_s[r];
+    const int out = out_s[r];
     const int8_t* st = stage_row(stage_sm + warp * kMaxOut, a.states + static_cast<int64_t>(s) * a.stride, a.stride,
                                  out, lane);
-    const int t0 = a.cu_seqlens[r], r0 = a.cu_rows[r];
+    const int t0 = t0_s[r], r0 = r0_s[r];
     const int nkv = nkv_s[r], nwin = nrow_s[r];
     // rebuild the planned bitmap and window of this request (pass 1's were per warp
     // and reused by later requests of the same warp)
     for (int w = lane; w < (out + 31) / 32; w += 32) bm[w] = 0;
     __syncwarp();
     for (int i = lane; i < nkv; i += 32) {
-      const int p = a.queue[static_cast<int64_t>(s) * a.qcap + (a.q_head[s] + i) % a.qcap];
+      const int p = a.queue[static_cast<int64_t>(s) * a.qcap + (qh_s[r] + i) % a.qcap];
       a.tok_req[t0 + i] = r;
       a.tok_pos[t0 + i] = p;
       atomicOr(&bm[p >> 5], 1u << (p & 31));
     }
     {
       int room = nwin;  // pass 1's window size (0 for a finished request)
-      int lo = a.block_index[s] * a.block;
+      int lo = bi_s[r] * a.block;
       int hi = min(lo + a.block, out);
       if (a.window_rule == 1) {
         hi = out;
@@ -317,10 +358,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) plan_kernel(const PlanArgs a) 
       }
     }
     __syncwarp();
-    const int pr = a.prompt[s];
+    const int pr = pr_s[r];
     const int ke = ke_s[r], vb = vb_s[r];
     const int words = nword_s[r];
-    uint32_t* vw = a.vis_words + a.vis_off[r];
+    uint32_t* vw = a.vis_words + vo_s[r];
     for (int w = 0; w < words; ++w) {
       const int abs = vb + w * 32 + lane;
       const int p = abs - pr;
@@ -651,28 +692,47 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     }
   }
   __syncthreads();
-  // 2. stable sort by tiles, descending: ascending keys (~tiles, index), bitonic
-  int np2 = 1;
-  while (np2 < nu) np2 <<= 1;
-  for (int i = tid; i < np2; i += kPlanThreads)
-    keys[i] = i < nu ? (static_cast<unsigned long long>(0x7FFFFFFF - u_tiles[i]) << 32) | static_cast<unsigned>(i)
-                     : ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= np2; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < np2; i += kPlanThreads) {
-        const int ix = i ^ j;
-        if (ix > i) {
-          const bool up = (i & k) == 0;
-          const unsigned long long a = keys[i], b = keys[ix];
-          if ((a > b) == up) {
-            keys[i] = b;
-            keys[ix] = a;
-          }
+  // 2. stable sort of the units by tiles, descending.  A request's units are
+  // contiguous and share its tile count, so sorting the requests (stable, by rank
+  // counting: tpr threads per request each compare a stripe of the others) and laying
+  // each request's units out in index order gives the stable unit order.
+  {
+    int* rank_cnt = p_slot;  // [257] units of the request of each rank, then their offsets
+    int* rank_of = p_t0;     // [256] (both arrays are written only from step 3 on)
+    // threads per request: a power of two <= 32 (a request's threads share a warp)
+    const int tpr = 1 << (31 - __clz(min(32, max(1, kPlanThreads / max(n_req, 1)))));
+    const int r = tid / tpr, sub = tid - r * tpr;
+    int tiles_r = 0, cnt_r = 0, rank = 0;
+    if (r < n_req) {
+      cnt_r = req_off[r + 1] - req_off[r];
+      tiles_r = (key_end[r] + 63) / 64;
+      if (cnt_r > 0)
+        for (int q = sub; q < n_req; q += tpr) {
+          if (req_off[q + 1] == req_off[q]) continue;
+          const int tq = (key_end[q] + 63) / 64;
+          rank += (tq > tiles_r || (tq == tiles_r && q < r)) ? 1 : 0;
         }
-      }
-      __syncthreads();
     }
+    for (int o = 1; o < tpr; o <<= 1) rank += __shfl_xor_sync(0xFFFFFFFFu, rank, o);
+    if (tid < 257) rank_cnt[tid] = 0;
+    __syncthreads();
+    if (r < n_req && sub == 0 && cnt_r > 0) {
+      rank_cnt[rank] = cnt_r;
+      rank_of[r] = rank;
+    }
+    __syncthreads();
+    unsigned total;
+    const unsigned pre = block_exclusive_scan(tid < n_req ? static_cast<unsigned>(rank_cnt[tid]) : 0u, scan_ws, &total);
+    __syncthreads();
+    if (tid < n_req) rank_cnt[tid] = static_cast<int>(pre);
+    __syncthreads();
+    if (r < n_req && cnt_r > 0) {
+      const int base = rank_cnt[rank_of[r]];
+      const unsigned long long hi = static_cast<unsigned long long>(0x7FFFFFFF - tiles_r) << 32;
+      for (int j = sub; j < cnt_r; j += tpr) keys[base + j] = hi | static_cast<unsigned>(req_off[r] + j);
+    }
+    __syncthreads();
+  }
   // 3. placement (loads in half-tiles)
   if (warp == 0) {
     // 3a. pieces per unit: the page cap, and with allow_cut a balanced cut of every
