@@ -23,7 +23,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--workload", default="sharegpt")
 a = ap.parse_args()
-a.page, a.seed, a.chunk, a.batch = 64, 0, 32, 64
+a.page, a.seed, a.chunk = 64, 0, 32
+a.batch = 128 if a.workload == "llada" else 64
 a.e2e_steps = a.steps
 dev = torch.device("cuda")
 W = bench.build_decoder(a, dev, world=1, rank=0)
