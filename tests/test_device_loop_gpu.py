@@ -405,3 +405,46 @@ def test_streaming_decoder_loop_backend_mixed_chunks():
         assert steps < 5000
     assert not live_h
     dec_d.release_all([])
+
+
+@pytest.mark.gpu
+def test_device_admit_writes_the_slot_rows():
+    """optimus_device_admit (DeviceLoop.replace + flush_admissions): after admitting
+    requests into finished positions, every field of their batch slots in the device
+    state (scalars, state row, FIFO ring, block-table row) equals the host's packed rows,
+    and the other slots are untouched."""
+    batch, chunk = 6, 16
+    reqs, dec = _setup(11, batch, chunk)
+    loop = DeviceLoop(dec, reqs, chunk)
+    while not any(r.finished for r in loop.requests):
+        loop.step()
+    free = sorted(loop.free)
+    assert free
+
+    class A:
+        pass
+    a = A()
+    a.workload, a.chunk, a.page, a.batch, a.seed, a.steps = "sharegpt", chunk, 64, 8, 7, 1
+    cand = [r for r in bench.workload_requests(a, seed_offset=9)
+            if r.prompt_tokens + r.output_tokens <= dec.cfg.max_pages_per_req * 64]
+    before = {k: v.clone() for k, v in loop.D.items()}
+    tbl_before = loop.Dt.clone()
+    admitted = []
+    for i, r in zip(free, cand):
+        loop.replace(i, r)
+        admitted.append(int(loop.slots_h[i]))
+    loop.flush_admissions()
+    torch.cuda.synchronize()
+    bs = loop.bs
+    for k in loop.state_keys:
+        dev = loop.D[k].cpu().numpy()
+        host = getattr(bs, k)
+        for s in admitted:
+            assert np.array_equal(dev[s], host[s]), (k, s)
+        others = [s for s in range(dev.shape[0]) if s not in admitted]
+        assert np.array_equal(dev[others], before[k].cpu().numpy()[others]), k
+    tbl = loop.Dt.cpu().numpy()
+    for s in admitted:
+        assert np.array_equal(tbl[s], dec.tables.table[s])
+    others = [s for s in range(tbl.shape[0]) if s not in admitted]
+    assert np.array_equal(tbl[others], tbl_before.cpu().numpy()[others])
