@@ -53,13 +53,16 @@ int v_saturated_k2(int32_t* out, int reset, cudaStream_t stream) {
 
 constexpr int kTileN = 64;     // keys per pipeline stage
 constexpr int kBlockM = 128;   // MMA rows (query token x head-in-group)
-constexpr int kThreads = 384;  // 12 warps: 8 softmax, 4 control
-// registers per thread after the setmaxnreg split: 128 x 56 + 256 x 224 = 384 x 168
+constexpr int kThreads = 512;  // 16 warps: 8 softmax, 4 control, 4 epilogue
+// registers per thread after the setmaxnreg split (launch: 512 x 128):
+// 128 x 56 (control) + 128 x 80 (epilogue) + 256 x 184 (softmax) = 64,512 <= 65,536
 constexpr int kCtrlRegs = 56;
-constexpr int kMathRegs = 224;
+constexpr int kEpiRegs = 80;
+constexpr int kMathRegs = 184;
+static_assert(128 * kCtrlRegs + 128 * kEpiRegs + 256 * kMathRegs <= 65536, "setmaxnreg split exceeds the SM");
 constexpr int kSBuf = 3;       // S/P buffers in TMEM, rotating over the CTA's tile stream
 constexpr int kInfo = 4;       // staged work-item records: the metadata warp runs 3 items ahead
-constexpr int kEpiRing = 8;    // per-item epilogue records (outlive the staged record)
+constexpr int kEpiRing = 16;   // per-item epilogue records (outlive the staged record)
 static_assert(kEpiRing > kInfo + 1, "epilogue records must outlive the staging ring");
 constexpr int kTraceSlots = 4096;
 constexpr int kAppItems = 64;  // work records per fused-append batch  // per CTA: [role*256 + i], 16 roles
@@ -107,11 +110,11 @@ struct AttnSmem {
   static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
   static constexpr uint32_t OFF_V = OFF_K + KST * KT_BYTES;
   static constexpr uint32_t OFF_INFO = OFF_V + VST * KT_BYTES;
-  static constexpr uint32_t OFF_RED = OFF_INFO + kInfo * sizeof(UnitInfo);  // float[{m,l}][wg][128]
-  static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * kBlockM * 4;
+  static constexpr uint32_t OFF_RED = OFF_INFO + kInfo * sizeof(UnitInfo);  // float[item&1][{m,l}][wg][128]
+  static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * 2 * kBlockM * 4;
   static constexpr uint32_t OFF_APP = OFF_EPI + kEpiRing * kEpiInts * 4;  // fused-append scratch
   static constexpr uint32_t OFF_BAR = (OFF_APP + (kAppItems * 9 + 1) * 4 + 15) / 16 * 16;
-  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 2 + 2 * kInfo + 2;
+  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 6 + 2 * kInfo + 2;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
@@ -148,7 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* pv_done = p_full + kSBuf;  // [buffer]
   uint64_t* o_full = pv_done + kSBuf;
   uint64_t* o_empty = o_full + 1;
-  uint64_t* info_full = o_empty + 1;
+  uint64_t* red_full = o_empty + 1;   // [item & 1]: both softmax warpgroups' (m, l) are in `red`
+  uint64_t* red_empty = red_full + 2; // [item & 1]: the epilogue warpgroup has read them
+  uint64_t* info_full = red_empty + 2;
   uint64_t* info_empty = info_full + kInfo;
   uint64_t* append_done = info_empty + kInfo;  // fused KV append of this CTA's items landed
   uint64_t* append_issued = append_done + 1;   // ... and its first loads are in flight
@@ -187,7 +192,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(o_full, 1);
-    mbar_init(o_empty, 256);
+    mbar_init(o_empty, 128);  // the epilogue warpgroup
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&red_full[i], 256);
+      mbar_init(&red_empty[i], 128);
+    }
     mbar_init(append_done, 256);
     mbar_init(append_issued, 256);
     mbar_fence_init();
@@ -219,10 +228,88 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int w_end = p.cta_off[blockIdx.x + 1];
 
   // Register split (setmaxnreg, per warpgroup): the control warpgroup (warps 8-11: TMA
-  // producers, MMA issuer, metadata) runs in kCtrlRegs registers and hands the rest to
-  // the two softmax warpgroups.  Each side's code is reachable only after its own
-  // setmaxnreg, so the allocator budgets the two sides separately.
-  if (warp >= 8) {
+  // producers, MMA issuer, metadata) runs in kCtrlRegs registers and the epilogue
+  // warpgroup (12-15) in kEpiRegs, handing the rest to the two softmax warpgroups.
+  // Each side's code is reachable only after its own setmaxnreg, so the allocator
+  // budgets the sides separately.
+  if (warp >= 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kEpiRegs));
+    // ------------------------------------------------------------ epilogue warpgroup
+    // Per item, in order: merge the two softmax warpgroups' (m_0, l_0, O_0) and
+    // (m_1, l_1, O_1) like two key splits, hand O back to the MMA warp as soon as it is
+    // read, and write the output rows (bf16, or fp32 split-KV partials).  Warp w reads
+    // TMEM lanes 32 (w % 4) .. +31, so the four warps cover the tile's 128 rows.  The
+    // softmax warpgroups never stop for an epilogue: the next item's tiles flow while
+    // this warpgroup drains the last one.
+    const int ew = warp & 3;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const int G = p.group;
+    const int t_in = row / G;
+    const int g_in = row - t_in * G;
+    const bool row_exists = t_in < p.tok_per_tile;
+    const int n_units = w_end - w_begin;
+    for (int e = 0; e < n_units; ++e) {
+      mbar_wait(&red_full[e & 1], (e >> 1) & 1);
+      // (the item's epilogue record was published before its staged record, which the
+      // softmax warpgroups acquired before arriving on red_full)
+      const int* er = epi + (e % kEpiRing) * kEpiInts;
+      const int head = er[0], tok_begin = er[1], n_tok = er[2], slot = er[3];
+      const bool valid = row_exists && t_in < n_tok;
+      const bool warp_valid = (ew * 32) / G < n_tok;
+      if (threadIdx.x == 384) trace(p, 13, e);
+      const float* rd = red + (e & 1) * 4 * kBlockM;
+      const float m0 = rd[0 * kBlockM + row], m1 = rd[1 * kBlockM + row];
+      const float l0 = rd[2 * kBlockM + row], l1 = rd[3 * kBlockM + row];
+      mbar_arrive(&red_empty[e & 1]);
+      const float mx = fmaxf(m0, m1);
+      const float w0 = l0 > 0.f ? fast_exp2(m0 - mx) : 0.f;
+      const float w1 = l1 > 0.f ? fast_exp2(m1 - mx) : 0.f;
+      const float l_tot = w0 * l0 + w1 * l1;
+      const float inv_l = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
+      const float f0 = w0 * (slot < 0 ? inv_l : 1.f), f1 = w1 * (slot < 0 ? inv_l : 1.f);
+      mbar_wait(o_full, e & 1);
+      tc_fence_after();
+      if (threadIdx.x == 384) trace(p, 14, e);
+      const int tok = tok_begin + t_in;
+      const int qh = head * G + g_in;
+#pragma unroll
+      for (int c0 = 0; c0 < HD; c0 += 16) {
+        uint32_t o0[16], o1[16];
+        if (warp_valid) {
+          tmem_ld16(tm_o0 + lane_off + c0, o0);
+          tmem_ld16(tm_o0 + lane_off + HD + c0, o1);
+          tmem_wait_ld();
+        }
+        if (c0 + 16 >= HD) {  // all of O_0 / O_1 read: back to the MMA warp
+          tc_fence_before();
+          mbar_arrive(o_empty);
+          if (threadIdx.x == 384) trace(p, 15, e);
+        }
+        if (valid) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            o0[c] = __float_as_uint((w0 > 0.f ? __uint_as_float(o0[c]) * f0 : 0.f) +
+                                    (w1 > 0.f ? __uint_as_float(o1[c]) * f1 : 0.f));
+          const float* o = reinterpret_cast<const float*>(o0);
+          if (slot < 0) {
+            uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(tok) * p.out_stride_tok +
+                                                  static_cast<int64_t>(qh) * HD + c0);
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              dst[v] = make_uint4(pack_bf16x2(o[8 * v], o[8 * v + 1]), pack_bf16x2(o[8 * v + 2], o[8 * v + 3]),
+                                  pack_bf16x2(o[8 * v + 4], o[8 * v + 5]), pack_bf16x2(o[8 * v + 6], o[8 * v + 7]));
+          } else {
+            float4* dst = reinterpret_cast<float4*>(p.ws_o + (static_cast<int64_t>(slot) * kBlockM + row) * HD + c0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+          }
+        }
+      }
+      if (valid && slot >= 0)
+        reinterpret_cast<float2*>(p.ws_ml)[static_cast<int64_t>(slot) * kBlockM + row] = make_float2(mx, l_tot);
+    }
+  } else if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kCtrlRegs));
   if (warp == 8 || warp == 10) {
       // ------------------------------------------------------------ TMA producers
@@ -496,77 +583,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int g_in = row - t_in * G;
     const bool row_exists = t_in < p.tok_per_tile;
     const float sc = p.scale_log2;
-    // Epilogue of item `e`: exchange (m, l) between the warpgroups through `red`;
-    // warpgroup h then writes output columns [h*HD/2, (h+1)*HD/2) merged from O_0
-    // and O_1 and releases the accumulators to the MMA warp.  It runs after this
-    // warpgroup's first tile of item e+1, so the next item's softmax overlaps the
-    // last PV and this drain instead of waiting behind them.
-    auto epilogue = [&](int e) {
-      const int* er = epi + (e % kEpiRing) * kEpiInts;
-      const int head = er[0], tok_begin = er[1], n_tok = er[2], slot = er[3];
-      const bool valid = row_exists && t_in < n_tok;
-      const bool warp_valid = (wq * 32) / G < n_tok;
-      if (threadIdx.x == 0) trace(p, 13, e);
-      named_bar_sync(1, 256);
-      const float m0 = red[0 * kBlockM + row], m1 = red[1 * kBlockM + row];
-      const float l0 = red[2 * kBlockM + row], l1 = red[3 * kBlockM + row];
-      named_bar_sync(1, 256);  // both read before the slots are reused
-      const float mx = fmaxf(m0, m1);
-      const float w0 = l0 > 0.f ? fast_exp2(m0 - mx) : 0.f;
-      const float w1 = l1 > 0.f ? fast_exp2(m1 - mx) : 0.f;
-      const float l_tot = w0 * l0 + w1 * l1;
-      const float inv_l = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
-      const float f0 = w0 * (slot < 0 ? inv_l : 1.f), f1 = w1 * (slot < 0 ? inv_l : 1.f);
-      mbar_wait(o_full, e & 1);
-      tc_fence_after();
-      if (threadIdx.x == 0) trace(p, 14, e);
-      // Drain this warpgroup's half of the merged O (packed to bf16 in registers, or
-      // stored as fp32 split-KV partials), then hand the accumulators back to the MMA
-      // warp before the bf16 output stores.
-      const int tok = tok_begin + t_in;
-      const int qh = head * G + g_in;
-      uint32_t pk[HD / 4] = {};
-      if (warp_valid) {
-#pragma unroll
-        for (int c0 = 0; c0 < HD / 2; c0 += 16) {
-          const int col = wg * (HD / 2) + c0;
-          uint32_t o0[16], o1[16];
-          tmem_ld16(tm_o0 + lane_off + col, o0);
-          tmem_ld16(tm_o0 + lane_off + HD + col, o1);
-          tmem_wait_ld();
-          float o[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            o[c] = (w0 > 0.f ? __uint_as_float(o0[c]) * f0 : 0.f) +
-                   (w1 > 0.f ? __uint_as_float(o1[c]) * f1 : 0.f);
-          if (slot < 0) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) pk[c0 / 2 + c] = pack_bf16x2(o[2 * c], o[2 * c + 1]);
-          } else if (valid) {
-            float4* dst = reinterpret_cast<float4*>(
-                p.ws_o + (static_cast<int64_t>(slot) * kBlockM + row) * HD + col);
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(o_empty);
-      if (threadIdx.x == 0) trace(p, 15, e);
-      if (valid) {
-        if (slot < 0) {
-          uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(tok) * p.out_stride_tok +
-                                                static_cast<int64_t>(qh) * HD + wg * (HD / 2));
-#pragma unroll
-          for (int v = 0; v < HD / 16; ++v)
-            dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
-        } else if (wg == 0) {
-          reinterpret_cast<float2*>(p.ws_ml)[static_cast<int64_t>(slot) * kBlockM + row] =
-              make_float2(mx, l_tot);
-        }
-      }
-    };
     if (p.k_new != nullptr) {
       // Fused KV append (K1): while the first tiles are in flight, the softmax
       // threads scatter the new K/V rows of this CTA's items into the pages.  Item i
@@ -802,17 +818,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&p_full[b]);
         if (threadIdx.x == 0) trace(p, 3, cw);
-        if (j == wg && unit > 0 && !(p.dbg & 16)) epilogue(unit - 1);  // previous item, overlapped
       }
       mbar_arrive(&info_empty[ib]);
-      // no tile of this item for this warpgroup: drain the previous item now
-      if (n_tiles <= wg && unit > 0 && !(p.dbg & 16)) epilogue(unit - 1);
-      red[(0 * 2 + wg) * kBlockM + row] = m;  // read by this item's epilogue
-      red[(1 * 2 + wg) * kBlockM + row] = l;
-      if (p.dbg & 16) epilogue(unit);  // diagnostics: drain in place (no overlap)
+      {  // this warpgroup's (m, l) of the item, for the epilogue warpgroup (two slots by
+         // item parity; slot reuse waits until the item two back was read)
+        if (unit >= 2) mbar_wait(&red_empty[unit & 1], ((unit >> 1) - 1) & 1);
+        float* rw = red + (unit & 1) * 4 * kBlockM;
+        rw[(0 * 2 + wg) * kBlockM + row] = m;
+        rw[(1 * 2 + wg) * kBlockM + row] = l;
+        mbar_arrive(&red_full[unit & 1]);
+      }
       tbase += n_tiles;
     }
-    if (unit > 0 && !(p.dbg & 16)) epilogue(unit - 1);
   }
   grid_dep_launch();
   if (threadIdx.x == 256) trace(p, 6, 2);
