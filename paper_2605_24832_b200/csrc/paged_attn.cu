@@ -249,6 +249,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int g_in = row - t_in * G;
     const bool row_exists = t_in < p.tok_per_tile;
     const int n_units = w_end - w_begin;
+    {
+      // zero O_0 / O_1 once: an accumulator a warpgroup does not touch in an item (no
+      // tile of its parity) then holds finite values, and the merge below can weight it
+      // by 0 with one FMA instead of a select (first phase of o_empty: the MMA's first
+      // PV waits for it)
+      uint32_t z[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) z[c] = 0u;
+#pragma unroll
+      for (int c0 = 0; c0 < 2 * HD; c0 += 16) tmem_st16(tm_o0 + lane_off + c0, z);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(o_empty);
+    }
     for (int e = 0; e < n_units; ++e) {
       mbar_wait(&red_full[e & 1], (e >> 1) & 1);
       // (the item's epilogue record was published before its staged record, which the
@@ -287,10 +301,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (threadIdx.x == 384) trace(p, 15, e);
         }
         if (valid) {
+          // f0 / f1 are 0 for a warpgroup without keys (w = 0), whose O is finite
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
-            o0[c] = __float_as_uint((w0 > 0.f ? __uint_as_float(o0[c]) * f0 : 0.f) +
-                                    (w1 > 0.f ? __uint_as_float(o1[c]) * f1 : 0.f));
+          for (int c = 0; c < 16; c += 2) {
+            float a0, a1, b0, b1;
+            ffma2(a0, a1, __uint_as_float(o0[c]), __uint_as_float(o0[c + 1]), f0, f0, 0.f, 0.f);
+            ffma2(b0, b1, __uint_as_float(o1[c]), __uint_as_float(o1[c + 1]), f1, f1, a0, a1);
+            o0[c] = __float_as_uint(b0);
+            o0[c + 1] = __float_as_uint(b1);
+          }
           const float* o = reinterpret_cast<const float*>(o0);
           if (slot < 0) {
             uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<int64_t>(tok) * p.out_stride_tok +
@@ -468,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int t = 0;  // PV stream position
       for (int u = 0; u < n_units; ++u) {
         const int n_tiles = __shfl_sync(0xFFFFFFFFu, epi[(u % kEpiRing) * kEpiInts + 4], 0);
-        mbar_wait(o_empty, (u & 1) ^ 1);  // the previous item's epilogue has read O_0/O_1
+        mbar_wait(o_empty, u & 1);  // O zeroed (u = 0) / the previous item's epilogue has read O_0/O_1
         tc_fence_after();
         for (int j = 0; j < n_tiles; ++j, ++t) {
           const int h = j & 1;
