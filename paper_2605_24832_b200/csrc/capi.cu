@@ -367,9 +367,11 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
   }
   // Cost model (in 64-key tile units; a tile is ~1100 SM cycles in the steady
   // state): every item pays a fixed prologue/epilogue (Q load, O drain, pipeline
-  // refill, measured ~2.5 tiles) and a cut item also pays its partial write and
-  // the combine read.
-  double kItem = 2.5;
+  // refill: ~1.9 tiles in a per-CTA fit since the epilogue warpgroup drains O beside
+  // the softmax, 0.57 us/tile + 1.08 us/item; 1.5 picks the faster plans across the
+  // bench workloads, profiles/r2ce_kitem.md) and a cut item also pays its partial write
+  // and the combine read.
+  double kItem = 1.5;
   const double kSplit = 1.5;
   if (const char* e = std::getenv("OPTIMUS_PLAN_KITEM")) kItem = std::atof(e);  // diagnostics
   const int hard_cap = item_tile_cap(page_size);

@@ -617,7 +617,7 @@ int optimus_device_apply(int n, const int32_t* slots, int block, const int32_t* 
 // (optimus_attn_plan, capi.cu, candidate A): units (request, KV head, query tile)
 // sorted longest first (stable), each cut only at the per-item page cap, placed
 // piece by piece on the least-loaded CTA (ties: lowest CTA), costs in half-tiles
-// (2 * tiles + 5 per item, + 3 for a cut piece: the host's 2.5 / 1.5 exactly);
+// (2 * tiles + 3 per item, + 3 for a cut piece: the host's 1.5 / 1.5 exactly);
 // work list in CTA order, split groups / partial slots in unit order.  Same output
 // as the host planner whenever it keeps whole units (OPTIMUS_PLAN_FORCE=whole);
 // one CTA, ~10 us for 512 units.
@@ -744,19 +744,19 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
     // = 1.07 cut 3.2 and 1.4 us per layer slower than whole; 1.17 / 1.21 / 1.37 cut 3.8 /
     // 5.9 / 7.5 us faster; profiles/r2az_device_cut_rule.md), capacity permitting.
     long long total = 0;
-    for (int u = lane; u < nu; u += 32) total += 2LL * u_tiles[u] + 5;
+    for (int u = lane; u < nu; u += 32) total += 2LL * u_tiles[u] + 3;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xFFFFFFFFu, total, off);
-    const long long budget = (total + grid - 1) / grid + 5;
-    const long long longest = nu > 0 ? 2LL * u_tiles[static_cast<int>(keys[0] & 0xFFFFFFFFu)] + 5 : 0;
-    const int nt_max = static_cast<int>(max(4LL, (budget - 8) / 2));
+    const long long budget = (total + grid - 1) / grid + 3;
+    const long long longest = nu > 0 ? 2LL * u_tiles[static_cast<int>(keys[0] & 0xFFFFFFFFu)] + 3 : 0;
+    const int nt_max = static_cast<int>(max(4LL, (budget - 6) / 2));
     bool cut = allow_cut && 100 * (budget + 24) < 89 * longest;  // + the combine (12 tiles)
     for (int pass = 0; pass < 2; ++pass) {
       int pieces = 0, cut_units = 0;
       for (int u = lane; u < nu; u += 32) {
         const int tiles = u_tiles[u];
         int sc = (tiles + hard_cap - 1) / hard_cap;
-        if (cut && 2LL * tiles + 5 > budget) sc = max(sc, (tiles + nt_max - 1) / nt_max);
+        if (cut && 2LL * tiles + 3 > budget) sc = max(sc, (tiles + nt_max - 1) / nt_max);
         u_sc[u] = sc;
         pieces += sc;
         cut_units += sc > 1;
@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) work_plan_kernel(
           p_unit[x] = u;
           p_t0[x] = t0;
           p_nt[x] = nt;
-          p_cta[x] = 2 * nt + 5 + (sc > 1 ? 3 : 0);  // cost in half-tiles, replaced by the placement
+          p_cta[x] = 2 * nt + 3 + (sc > 1 ? 3 : 0);  // cost in half-tiles, replaced by the placement
           t0 += nt;
         }
         pre += static_cast<unsigned>(sc);

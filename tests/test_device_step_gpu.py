@@ -262,14 +262,14 @@ def test_device_work_planner_cut_mode_invariants(hq, hkv, page, maxq, ke_hi):
             else:
                 assert pcs[0][2] == -1
             for a, b, _, cta in pcs:
-                loads[cta] += 2 * ((b - a + 63) // 64) + 5 + (3 if len(pcs) > 1 else 0)
+                loads[cta] += 2 * ((b - a + 63) // 64) + 3 + (3 if len(pcs) > 1 else 0)
         assert cut_units == c[1] and sum(int(x[5]) for x in g) == c[2]
         # makespan vs the whole-unit plan
         c0, w0, o0, _ = res[0]
         loads0 = np.zeros(grid)
         for x, r in enumerate(w0):
             cta = int(np.searchsorted(o0, x, side="right") - 1)
-            loads0[cta] += 2 * ((r[5] - r[4] + 63) // 64) + 5 + (3 if r[6] >= 0 else 0)
+            loads0[cta] += 2 * ((r[5] - r[4] + 63) // 64) + 3 + (3 if r[6] >= 0 else 0)
         assert loads.max() <= loads0.max() + 8
         hard_cap = 255 * page // 64  # tiles per item (the page cap cuts longer units in both modes)
         if it == 0 and (ke[0] + 63) // 64 <= hard_cap and 2 * (ke[0] + 63) // 64 > 1.2 * loads0.mean() + 40:
