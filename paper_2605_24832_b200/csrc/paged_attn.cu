@@ -1006,11 +1006,13 @@ int launch_paged_attn(int head_dim, bool v_fp16, const CUtensorMap& tq, const CU
   // held until its PV retires, a K slot only until its S does).
   if (head_dim == 128) {
     // Shallow rings measured fastest (3/3 vs 5/6: -10% on the ShareGPT batch, -4% at
-    // 4K): every CTA keeps ~96 KB in flight, enough to cover the unloaded HBM latency
-    // at its bandwidth share, while deeper rings only lengthen the DRAM queues that
-    // every dependent step (item start, first tile, tail) waits behind.
+    // 4K): every CTA keeps ~96-128 KB in flight, enough to cover the unloaded HBM
+    // latency at its bandwidth share, while deeper rings only lengthen the DRAM queues
+    // that every dependent step (item start, first tile, tail) waits behind.  With the
+    // epilogue warpgroup 4/4 edges out 3/3 (ShareGPT K2 29.7 -> 29.3 us, 4K and
+    // LongBench -1%, LLaDA +1%: profiles/r2ck_rings.md).
     const char* e = getenv("OPTIMUS_K2_RINGS");  // diagnostics: ring-depth variants
-    const int rings = e ? atoi(e) : 33;
+    const int rings = e ? atoi(e) : 44;
     if (rings == 44)
       return v_fp16 ? launch_attn_t<128, 4, 4, true>(tq, tk, tv, prm, grid, groups, n_groups, stream)
                     : launch_attn_t<128, 4, 4, false>(tq, tk, tv, prm, grid, groups, n_groups, stream);
