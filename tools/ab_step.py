@@ -35,8 +35,15 @@ for l in range(cfg.num_layers):
     dec.cache.k[l].normal_(); dec.cache.v[l].normal_()
 dm = dec.prepare(reqs, plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule))
 graphs = {}
+import os
 for mode in a.modes.split(","):
-    dec.append_mode = mode
+    # "k1@43": append mode k1 with OPTIMUS_K2_RINGS=43 (K2 variant chosen at capture)
+    am, _, rings = mode.partition("@")
+    if rings:
+        os.environ["OPTIMUS_K2_RINGS"] = rings
+    else:
+        os.environ.pop("OPTIMUS_K2_RINGS", None)
+    dec.append_mode = am
     s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
