@@ -779,7 +779,7 @@ def main():
     # ---- the device step as one CUDA graph (NCCL collectives captured with it)
     graph = capture_step(dec, dm, eager=world > 1 and backend != "nccl")
     # L x (K1, K2 [+ split-KV combine]) + K3 (one launch: partials and finalize fused)
-    n_launch = 2 * cfg.num_layers + (cfg.num_layers if dec.last_plan.n_groups else 0) + \
+    n_launch = 2 * cfg.num_layers + (cfg.num_layers if dec.last_plan.n_groups and not dec.last_plan.tail_merge else 0) + \
         (2 if dec.unmask_impl is not None else 1)
 
     sampler = ClockSampler(local)

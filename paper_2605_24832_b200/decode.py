@@ -296,7 +296,7 @@ class StreamingDecoder:
             dm.vis_base.data_ptr(), dm.vis_off.data_ptr(), dm.vis_words.data_ptr(),
             dm.block_tables.data_ptr(), dm.block_tables.shape[1], plan.work.data_ptr(),
             plan.cta_off.data_ptr(), plan.grid if plan.n_work else 0, plan.groups.data_ptr(),
-            plan.n_groups, cfg.block_size, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+            plan.n_groups_arg, cfg.block_size, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
             cfg.page_size, 1.0 / float(cfg.head_dim) ** 0.5, out_a, out.stride(0),
             self._ws_o.data_ptr() if plan.n_partials else None,
             self._ws_ml.data_ptr() if plan.n_partials else None,

@@ -21,6 +21,7 @@ ap.add_argument("--dump", default="")
 ap.add_argument("--ab", action="store_true")
 ap.add_argument("--dbgs", default="0,16")  # OPTIMUS_DBG[:OPTIMUS_K2_RINGS] per variant
 ap.add_argument("--plans", default="both")
+ap.add_argument("--forces", default="whole,cut", help="OPTIMUS_PLAN_FORCE values to A/B (whole, cut, flat, giants, tail)")
 ap.add_argument("--trace-fused", action="store_true")
 a = ap.parse_args()
 a.steps = 1
@@ -81,7 +82,7 @@ if a.ab:
     import os
     from paper_2605_24832_b200 import _lib
     variants = []
-    for force in ("whole", "cut"):
+    for force in a.forces.split(","):
         os.environ["OPTIMUS_PLAN_FORCE"] = force
         pl = ops.plan_attention(m.cu_seqlens, m.key_end, cfg.num_q_heads, cfg.num_kv_heads, grid=dec.grid,
                                 min_split_tiles=cfg.min_split_tiles, device=dev, page_size=cfg.page_size)
