@@ -669,12 +669,10 @@ def parity_check(W, dm, res, layer=0, n_sample=12, full_k3=True):
     reqs, plans = dm.__dict__["requests"], dm.__dict__["plans"]
     q, k, v = fwd.qkv(layer, dm)
     kc, vc = dec.cache.layer(layer)
-    # K1 (idempotent: the same rows are written again)
-    slots = torch.empty(m.n_tok, dtype=torch.int64, device=dec.device)
-    ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc, slot_mapping_out=slots)
-    torch.cuda.synchronize()
+    # K1: the rows the timed step's own K1 (append mode dec.append_mode) left in the pages,
+    # at the oracle's slots; then the slot mapping of the k1 form (idempotent: the same
+    # rows are written again)
     ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.block_tables, P)
-    out["k1_slots_exact"] = bool(np.array_equal(slots.cpu().numpy(), ref_slots))
     sl = torch.as_tensor(ref_slots, device=dec.device)
     pg, off = sl // P, sl % P
     k_rows = kc[pg, :, off, :]
@@ -682,6 +680,11 @@ def parity_check(W, dm, res, layer=0, n_sample=12, full_k3=True):
     v_want = on.v_storage(v[: m.n_tok].float().cpu().numpy(), "fp16" if vc.dtype == torch.float16 else "bf16")
     out["k1_rows_bit_exact"] = bool(torch.equal(k_rows, k[: m.n_tok]) and
                                     np.array_equal(v_rows.cpu().view(torch.int16).numpy(), v_want))
+    out["k1_append_mode"] = dec.append_mode
+    slots = torch.empty(m.n_tok, dtype=torch.int64, device=dec.device)
+    ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc, slot_mapping_out=slots)
+    torch.cuda.synchronize()
+    out["k1_slots_exact"] = bool(np.array_equal(slots.cpu().numpy(), ref_slots))
     # K2 on the same layer, sampled requests
     plan = dm.__dict__["attn_plan"]
     o = dec._workspaces(plan, m.n_tok)
@@ -778,9 +781,9 @@ def main():
 
     # ---- the device step as one CUDA graph (NCCL collectives captured with it)
     graph = capture_step(dec, dm, eager=world > 1 and backend != "nccl")
-    # L x (K1, K2 [+ split-KV combine]) + K3 (one launch: partials and finalize fused)
-    n_launch = 2 * cfg.num_layers + (cfg.num_layers if dec.last_plan.n_groups and not dec.last_plan.tail_merge else 0) + \
-        (2 if dec.unmask_impl is not None else 1)
+    # [slot map +] L x (K1, K2 [+ split-KV combine]) + K3 (one launch: partials and finalize fused)
+    n_launch = 2 * cfg.num_layers + (cfg.num_layers if dec.last_plan.n_groups else 0) + \
+        (2 if dec.unmask_impl is not None else 1) + (1 if dec.append_mode == "slots" else 0)
 
     sampler = ClockSampler(local)
     sampler.start()

@@ -382,6 +382,20 @@ int optimus_kv_append_dev(const void* k_new, const void* v_new, int64_t new_stri
                           const int32_t* tok_pos, const int32_t* prompt_len, const int32_t* block_tables,
                           int max_pages, int n_tok_cap, const int32_t* n_tok_dev, int num_kv_heads, int head_dim,
                           int page_size, void* k_cache, void* v_cache, int v_dtype, void* stream);
+/*
+ * Device-count twins of optimus_slot_mapping / optimus_kv_append_slots (the loop's
+ * "slots" K1: the step's slot map once, then one round trip per row in every layer).
+ * optimus_slot_mapping_dev is a plain launch; optimus_kv_append_slots_dev launches with
+ * programmatic stream serialization and reads n_tok_dev / slot_abs before its PDL wait,
+ * so the slot map must come from an earlier, non-PDL launch of the same step.
+ */
+int optimus_slot_mapping_dev(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                             const int32_t* block_tables, int max_pages, int n_tok_cap, const int32_t* n_tok_dev,
+                             int page_size, int32_t* slot_abs_out, void* stream);
+int optimus_kv_append_slots_dev(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                                const int32_t* slot_abs, int n_tok_cap, const int32_t* n_tok_dev, int num_kv_heads,
+                                int head_dim, int page_size, void* k_cache, void* v_cache, int v_dtype,
+                                void* stream);
 int optimus_unmask_partials_dev(const void* logits, int logits_dtype, int64_t row_stride, const int32_t* row_src,
                                 int n_rows_cap, const int32_t* n_rows_dev, int vocab, int vocab_offset,
                                 int n_vsplit, float* part, void* stream);

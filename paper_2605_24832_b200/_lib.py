@@ -101,6 +101,8 @@ SIGNATURES = {
     "optimus_unmask_partials_dev": (_i32, [_vp, _i32, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp]),
     "optimus_device_row_src": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "optimus_slot_mapping": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "optimus_slot_mapping_dev": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "optimus_kv_append_slots_dev": (_i32, [_vp, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
     "optimus_host_plan": (_i32, [_i32, _vp, _i32, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),

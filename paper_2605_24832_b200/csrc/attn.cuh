@@ -18,11 +18,6 @@ struct AttnParams {
   int64_t out_stride_tok;
   float* ws_o;
   float* ws_ml;
-  // tail-merged split-KV (n_tail > 0): group records [n_tail][8] with [6] = the CTAs (+ 1,
-  // 8 bits each) merging the output's 32-row slabs s = 0..3, and [7] = group index + 1 (its arrival counter, kept in the library's device array);
-  // a piece's work record carries the same value in [7]
-  const int32_t* groups;
-  int n_tail;
   int max_pages;
   int block_size;
   int num_q_heads;
@@ -47,10 +42,6 @@ struct AttnParams {
   unsigned long long* trace;
   int dbg;  // diagnostics: bit0 skip lo-plane PV, bit1 skip S MMA, bit2 skip softmax math, bit3 skip PV  // optional per-CTA timeline (diagnostics), nullptr in production
 };
-
-// Tail-merged plans: at most this many groups per launch (one device counter each);
-// tail-merged launches on one device must be stream-ordered (they share the counters).
-constexpr int kMaxTailGroups = 4096;
 
 int launch_attn_combine_dev(int head_dim, const AttnParams& prm, const int32_t* groups, int max_groups,
                             const int32_t* n_groups_dev, cudaStream_t stream);

@@ -25,6 +25,10 @@ int launch_unmask_partials_dev(const void*, int, int64_t, const int32_t*, int, c
                                float*, cudaStream_t);
 int launch_slot_map(const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int,
                     int32_t*, cudaStream_t);
+int launch_slot_map_dev(const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, const int32_t*,
+                        int, int32_t*, cudaStream_t);
+int launch_kv_append_slots_dev(const void*, const void*, int64_t, const int32_t*, int, const int32_t*, int, int,
+                               int, void*, void*, int, cudaStream_t);
 int launch_kv_append(const void*, const void*, int64_t, const int32_t*, const int32_t*,
                      const int32_t*, const int32_t*, int, int, int, int, int, void*, void*,
                      int64_t*, int, cudaStream_t);
@@ -285,6 +289,41 @@ int optimus_lmhead_unmask_partials(const void* hidden, int64_t hidden_stride, in
   return cuda_status(launch_lmhead_unmask(th, tw, n_rows, vocab, k_dim, vocab_offset, part,
                                           static_cast<cudaStream_t>(stream)),
                      "lmhead_unmask");
+}
+
+int optimus_slot_mapping_dev(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                             const int32_t* block_tables, int max_pages, int n_tok_cap, const int32_t* n_tok_dev,
+                             int page_size, int32_t* slot_abs_out, void* stream) {
+  if (n_tok_cap < 0 || max_pages < 1 || page_size < 1) return fail("slot_mapping_dev: bad sizes");
+  if (n_tok_cap == 0) return 0;
+  if (!n_tok_dev || !tok_req || !tok_pos || !prompt_len || !block_tables || !slot_abs_out)
+    return fail("slot_mapping_dev: null pointer");
+  if (reinterpret_cast<uintptr_t>(slot_abs_out) % 8) return fail("slot_mapping_dev: slot_abs must be 8-byte aligned");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_slot_map_dev(tok_req, tok_pos, prompt_len, block_tables, max_pages, n_tok_cap,
+                                         n_tok_dev, page_size, slot_abs_out, static_cast<cudaStream_t>(stream)),
+                     "slot_mapping_dev");
+}
+
+int optimus_kv_append_slots_dev(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                                const int32_t* slot_abs, int n_tok_cap, const int32_t* n_tok_dev, int num_kv_heads,
+                                int head_dim, int page_size, void* k_cache, void* v_cache, int v_dtype,
+                                void* stream) {
+  if (v_dtype != 0 && v_dtype != 1) return fail("kv_append_slots_dev: v_dtype must be 0 or 1");
+  if (n_tok_cap < 0 || num_kv_heads < 1 || head_dim % 8 || head_dim < 8)
+    return fail("kv_append_slots_dev: bad sizes");
+  if (new_stride_tok < static_cast<int64_t>(num_kv_heads) * head_dim || new_stride_tok % 8)
+    return fail("kv_append_slots_dev: bad new_stride_tok");
+  if (!page_ok(page_size)) return fail("kv_append_slots_dev: page_size must be a power of two in [8, 1024]");
+  if (n_tok_cap == 0) return 0;
+  if (!n_tok_dev || !k_new || !v_new || !slot_abs || !k_cache || !v_cache)
+    return fail("kv_append_slots_dev: null pointer");
+  if (reinterpret_cast<uintptr_t>(slot_abs) % 8) return fail("kv_append_slots_dev: slot_abs must be 8-byte aligned");
+  if (int st = check_device()) return st;
+  return cuda_status(launch_kv_append_slots_dev(k_new, v_new, new_stride_tok, slot_abs, n_tok_cap, n_tok_dev,
+                                                num_kv_heads, head_dim, page_size, k_cache, v_cache, v_dtype,
+                                                static_cast<cudaStream_t>(stream)),
+                     "kv_append_slots_dev");
 }
 
 int optimus_unmask_merge_splits(const float* part, int n_rows, int n_split, float* out, void* stream) {
@@ -568,102 +607,25 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     }
   }
 
-  // ---- candidate E: giants halved and merged in the tail.  The units costlier than the
-  // mean CTA load are cut into exactly two pieces; after LPT over pieces and whole units,
-  // each cut unit's merge goes to the least-loaded CTA, which runs it after its own items
-  // (the pieces, placed first, are long done by then).  No combine launch follows K2, so
-  // the cut costs kMerge tiles on a CTA with slack instead of kCombine on the critical
-  // path.
-  std::vector<Piece> pe;
-  std::vector<unsigned> merge_cta(nu, 0u);  // per cut unit: CTA + 1 merging each 32-row slab, 8 bits each
-  double span_e = 1e300;
-  const double kTail = 1.0, kMerge = 0.75;  // per 32-row slab
-  const bool a_good_tail = lb + kTail >= 0.97 * span_a && std::getenv("OPTIMUS_PLAN_FORCE") == nullptr;
-  if (!a_good_tail && grid <= 255 && std::getenv("OPTIMUS_PLAN_NOTAIL") == nullptr) {
-    struct Job {
-      double cost;
-      int unit, t0, nt;
-    };
-    std::vector<Job> jobs;
-    jobs.reserve(nu + 2 * grid);
-    bool ok = true;
-    for (int ui : order) {
-      const int tiles = units[ui].tiles;
-      const bool halve = tiles + kItem > lb && tiles >= 2 * min_split_tiles;
-      if (!halve && tiles > hard_cap) ok = false;
-      if (halve && (tiles + 1) / 2 > hard_cap) ok = false;
-      if (halve) {
-        const int a0 = (tiles + 1) / 2;
-        jobs.push_back({a0 + kItem + kSplit, ui, 0, a0});
-        jobs.push_back({tiles - a0 + kItem + kSplit, ui, a0, tiles - a0});
-      } else {
-        jobs.push_back({tiles + kItem, ui, 0, tiles});
-      }
-    }
-    if (ok) {
-      std::stable_sort(jobs.begin(), jobs.end(), [](const Job& a, const Job& b) { return a.cost > b.cost; });
-      std::vector<double> loads(grid, 0.0);
-      typedef std::pair<double, int> LoadCta;
-      std::vector<LoadCta> heap;
-      heap.reserve(grid);
-      for (int c = 0; c < grid; ++c) heap.push_back(LoadCta(0.0, c));
-      auto cmp = [](const LoadCta& a, const LoadCta& b) { return a > b; };
-      pe.reserve(jobs.size());
-      for (const Job& j : jobs) {
-        std::pop_heap(heap.begin(), heap.end(), cmp);
-        LoadCta& lc = heap.back();
-        pe.push_back({j.unit, j.t0, j.nt, lc.second});
-        lc.first += j.cost;
-        std::push_heap(heap.begin(), heap.end(), cmp);
-      }
-      // merges: each 32-row slab of a cut unit's output on the least-loaded CTA at that
-      // point (a slab is a bulk copy of its rows of both partials and a few us of math)
-      std::vector<char> seen(nu, 0);
-      for (const Piece& x : pe)
-        if (x.t0 > 0 && !seen[x.unit]) {
-          seen[x.unit] = 1;
-          const int slabs = (units[x.unit].n_tok * G + 31) / 32;
-          for (int sl = 0; sl < slabs; ++sl) {
-            std::pop_heap(heap.begin(), heap.end(), cmp);
-            LoadCta& lc = heap.back();
-            merge_cta[x.unit] |= static_cast<unsigned>(lc.second + 1) << (8 * sl);
-            lc.first += kMerge;
-            std::push_heap(heap.begin(), heap.end(), cmp);
-          }
-        }
-      span_e = 0;
-      for (const LoadCta& lc : heap) span_e = std::max(span_e, lc.first);
-      if (std::find(seen.begin(), seen.end(), 1) == seen.end()) span_e = 1e300;
-    }
-  }
-
   // Prefer whole units unless cutting buys >3% of the makespan, net of the split
   // combine launch and partial traffic it brings (kCombine, measured).
-  int which = 0;  // 0 whole, 1 LPT-cut, 2 flat, 3 giants halved, 4 giants halved + tail merge
+  int which = 0;  // 0 whole, 1 LPT-cut, 2 flat, 3 giants halved
   double span_cut = span_b;
   which = 1;
   if (span_c < span_cut) span_cut = span_c, which = 2;
   if (span_d < span_cut) span_cut = span_d, which = 3;
-  const std::vector<Piece>* cand[5] = {&pa, &pb, &pc_, &pd, &pe};
+  const std::vector<Piece>* cand[4] = {&pa, &pb, &pc_, &pd};
   if (!(span_cut + kCombine < 0.97 * span_a) || static_cast<int>(cand[which]->size()) > max_work) which = 0;
-  {
-    const double best = which == 0 ? span_a : span_cut + kCombine;
-    if (span_e + kTail < 0.97 * best && span_e + kTail < 0.97 * span_a &&
-        static_cast<int>(pe.size()) <= max_work && static_cast<int>(pe.size()) - nu <= kMaxTailGroups)
-      which = 4;
-  }
-  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE")) {  // diagnostics: whole | cut | flat | giants | tail
-    which = std::strcmp(f, "cut") == 0 ? 1 : std::strcmp(f, "flat") == 0 ? 2 : std::strcmp(f, "giants") == 0 ? 3
-          : std::strcmp(f, "tail") == 0 ? 4 : 0;
+  if (const char* f = std::getenv("OPTIMUS_PLAN_FORCE")) {  // diagnostics: whole | cut | flat | giants
+    which = std::strcmp(f, "cut") == 0 ? 1 : std::strcmp(f, "flat") == 0 ? 2 : std::strcmp(f, "giants") == 0 ? 3 : 0;
     if (cand[which]->empty() || static_cast<int>(cand[which]->size()) > max_work) which = 0;
-    if (which == 4 && static_cast<int>(pe.size()) - nu > kMaxTailGroups) which = 0;
   }
   const std::vector<Piece>& P = *cand[which];
   if (static_cast<int>(P.size()) > max_work) return fail("attn_plan: work buffer too small");
   if (std::getenv("OPTIMUS_PLAN_DEBUG"))
     std::fprintf(stderr, "attn_plan: whole-unit LPT span %.1f (%zu items), cutting LPT %.1f (%zu items), "
-                 "flat %.1f (%zu items), giants %.1f (%zu items), tail-merged %.1f (%zu items) -> %d\n", span_a,
-                 pa.size(), span_b, pb.size(), span_c, pc_.size(), span_d, pd.size(), span_e, pe.size(), which);
+                 "flat %.1f (%zu items), giants %.1f (%zu items) -> %d\n", span_a, pa.size(), span_b, pb.size(),
+                 span_c, pc_.size(), span_d, pd.size(), which);
   // Split groups: the pieces of a unit, in key order, get consecutive partial slots.
   std::vector<int> byu(P.size());
   for (size_t x = 0; x < P.size(); ++x) byu[x] = static_cast<int>(x);
@@ -671,7 +633,6 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     return P[a].unit != P[b].unit ? P[a].unit < P[b].unit : P[a].t0 < P[b].t0;
   });
   std::vector<int> slot(P.size(), -1);
-  std::vector<int> group_unit;
   int n_groups = 0, n_partials = 0;
   for (size_t i = 0; i < byu.size();) {
     size_t k = i + 1;
@@ -680,36 +641,17 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
       if (n_groups >= max_groups) return fail("attn_plan: groups buffer too small");
       const Unit& u = units[P[byu[i]].unit];
       int32_t* g = groups + 8 * n_groups++;
-      group_unit.push_back(P[byu[i]].unit);
       g[0] = u.req;
       g[1] = u.head;
       g[2] = u.tok_begin;
       g[3] = u.n_tok;
       g[4] = n_partials;
       g[5] = static_cast<int>(k - i);
-      g[6] = 0;  // tail merge: merging CTA + 1 (set below)
-      g[7] = 0;  // tail merge: arrival counter (int offset into ws_ml) + 1
+      g[6] = 0;
+      g[7] = 0;
       for (size_t x = i; x < k; ++x) slot[byu[x]] = n_partials++;
     }
     i = k;
-  }
-  // Tail-merged plan: group g's pieces arrive on the library's device counter g (K2
-  // keeps the counters zero between launches); each piece's record names it.
-  std::vector<int> cnt_of(P.size(), 0);
-  if (which == 4) {
-    for (int gi = 0; gi < n_groups; ++gi) {
-      groups[8 * gi + 6] = static_cast<int32_t>(merge_cta[group_unit[gi]]);
-      groups[8 * gi + 7] = gi + 1;
-    }
-    for (size_t i = 0, gi = 0; i < byu.size();) {
-      size_t k = i + 1;
-      while (k < byu.size() && P[byu[k]].unit == P[byu[i]].unit) ++k;
-      if (k - i > 1) {
-        for (size_t x = i; x < k; ++x) cnt_of[byu[x]] = static_cast<int>(gi) + 1;
-        ++gi;
-      }
-      i = k;
-    }
   }
   // Work list in CTA order (stable: a CTA runs its pieces in placement order).
   std::vector<int> cnt(grid + 1, 0);
@@ -727,7 +669,7 @@ int optimus_attn_plan(int n_req, const int32_t* cu, const int32_t* key_end, int 
     w[4] = pc.t0 * 64;
     w[5] = std::min(key_end[u.req], (pc.t0 + pc.nt) * 64);
     w[6] = slot[x];
-    w[7] = cnt_of[x];
+    w[7] = 0;
   }
   *n_groups_out = n_groups;
   *n_partials_out = n_partials;
@@ -760,14 +702,10 @@ static int paged_attn_impl(const void* q, int64_t q_stride_tok, int n_tok_total,
     return fail("paged_attn: q_stride_tok must be >= Hq*head_dim and a multiple of 8");
   if (out_stride_tok % 8 || out_stride_tok < static_cast<int64_t>(hq) * head_dim)
     return fail("paged_attn: out_stride_tok must be >= Hq*head_dim and a multiple of 8");
-  // n_groups < 0: a tail-merged plan (optimus_attn_plan, candidate E): the -n_groups
-  // groups are merged inside K2 by the CTAs their records name, and no combine follows
-  if (grid < 0 || num_pages < 1 || max_pages < 1)
+  if (grid < 0 || n_groups < 0 || num_pages < 1 || max_pages < 1)
     return fail("paged_attn: bad sizes");
   if (n_tok_total == 0 || grid == 0) return 0;
-  if (n_groups != 0 && (!ws_o || !ws_ml)) return fail("paged_attn: split-KV needs a workspace");
-  if (n_groups < 0 && !groups) return fail("paged_attn: tail-merged plan without its groups");
-  if (n_groups < -optimus::kMaxTailGroups) return fail("paged_attn: too many tail-merged groups");
+  if (n_groups > 0 && (!ws_o || !ws_ml)) return fail("paged_attn: split-KV needs a workspace");
   if (reinterpret_cast<uintptr_t>(q) % 16 || reinterpret_cast<uintptr_t>(k_cache) % 16 ||
       reinterpret_cast<uintptr_t>(v_cache) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
     return fail("paged_attn: tensors must be 16-byte aligned");
@@ -824,8 +762,6 @@ static int paged_attn_impl(const void* q, int64_t q_stride_tok, int n_tok_total,
   prm.out_stride_tok = out_stride_tok;
   prm.ws_o = ws_o;
   prm.ws_ml = ws_ml;
-  prm.groups = groups;
-  prm.n_tail = n_groups < 0 ? -n_groups : 0;
   prm.max_pages = max_pages;
   prm.block_size = block_size;
   prm.num_q_heads = hq;
@@ -841,7 +777,7 @@ static int paged_attn_impl(const void* q, int64_t q_stride_tok, int n_tok_total,
     prm.dbg = e ? atoi(e) : 0;
   }
   return cuda_status(launch_paged_attn(head_dim, v_dtype == 1, tq, tk, tv, prm, grid, groups,
-                                       n_groups > 0 ? n_groups : 0, static_cast<cudaStream_t>(stream)),
+                                       n_groups, static_cast<cudaStream_t>(stream)),
                      "paged_attn");
 }
 

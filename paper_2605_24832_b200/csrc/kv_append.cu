@@ -140,8 +140,12 @@ int launch_kv_append_dev(const void* k_new, const void* v_new, int64_t new_strid
 __global__ void __launch_bounds__(256) kv_append_slots_kernel(
     const uint4* __restrict__ k_new, const uint4* __restrict__ v_new, int64_t new_stride_vec,
     const int2* __restrict__ slot_abs, int n_tok, int hkv, int vec_per_head, int page_size,
-    int page_shift, uint4* __restrict__ k_cache, uint4* __restrict__ v_cache, int v_fp16) {
+    int page_shift, uint4* __restrict__ k_cache, uint4* __restrict__ v_cache, int v_fp16,
+    const int32_t* __restrict__ n_tok_dev) {
   grid_dep_launch();
+  // device-planned step: the count (and slot_abs, from the non-PDL slot-map launch
+  // earlier in the step) are complete before this grid starts
+  if (n_tok_dev != nullptr) n_tok = *n_tok_dev;
   const int per_tok = hkv * vec_per_head;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= static_cast<int64_t>(n_tok) * per_tok) return;
@@ -175,7 +179,23 @@ int launch_kv_append_slots(const void* k_new, const void* v_new, int64_t new_str
       kv_append_slots_kernel, blocks, 256, stream, static_cast<const uint4*>(k_new),
       static_cast<const uint4*>(v_new), new_stride_tok / 8, reinterpret_cast<const int2*>(slot_abs), n_tok,
       hkv, vec_per_head, page_size, __builtin_ctz(static_cast<unsigned>(page_size)),
-      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), v_fp16));
+      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), v_fp16, static_cast<const int32_t*>(nullptr)));
+}
+
+// Same, with the token count read from device memory (n_tok_cap sizes the grid).
+int launch_kv_append_slots_dev(const void* k_new, const void* v_new, int64_t new_stride_tok,
+                               const int32_t* slot_abs, int n_tok_cap, const int32_t* n_tok_dev, int hkv,
+                               int head_dim, int page_size, void* k_cache, void* v_cache, int v_fp16,
+                               cudaStream_t stream) {
+  if (n_tok_cap == 0) return 0;
+  const int vec_per_head = head_dim / 8;
+  const int64_t total = static_cast<int64_t>(n_tok_cap) * hkv * vec_per_head;
+  const int blocks = static_cast<int>((total + 255) / 256);
+  return static_cast<int>(launch_pdl(
+      kv_append_slots_kernel, blocks, 256, stream, static_cast<const uint4*>(k_new),
+      static_cast<const uint4*>(v_new), new_stride_tok / 8, reinterpret_cast<const int2*>(slot_abs), n_tok_cap,
+      hkv, vec_per_head, page_size, __builtin_ctz(static_cast<unsigned>(page_size)),
+      static_cast<uint4*>(k_cache), static_cast<uint4*>(v_cache), v_fp16, n_tok_dev));
 }
 
 // Per-step slot map for the fused append (K2 with k_new): out[t] = {prompt + pos,
@@ -183,7 +203,8 @@ int launch_kv_append_slots(const void* k_new, const void* v_new, int64_t new_str
 __global__ void __launch_bounds__(256) slot_map_kernel(
     const int32_t* __restrict__ tok_req, const int32_t* __restrict__ tok_pos,
     const int32_t* __restrict__ prompt_len, const int32_t* __restrict__ block_tables, int max_pages,
-    int n_tok, int page_size, int32_t* __restrict__ out) {
+    int n_tok, int page_size, int32_t* __restrict__ out, const int32_t* __restrict__ n_tok_dev) {
+  if (n_tok_dev != nullptr) n_tok = *n_tok_dev;  // device-planned step (grid sized for capacity)
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tok) return;
   const int r = __ldg(tok_req + t);
@@ -197,7 +218,18 @@ int launch_slot_map(const int32_t* tok_req, const int32_t* tok_pos, const int32_
                     int32_t* out, cudaStream_t stream) {
   if (n_tok == 0) return 0;
   slot_map_kernel<<<(n_tok + 255) / 256, 256, 0, stream>>>(tok_req, tok_pos, prompt_len, block_tables,
-                                                           max_pages, n_tok, page_size, out);
+                                                           max_pages, n_tok, page_size, out, nullptr);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Same, with the token count read from device memory (a plain launch: the per-layer K1
+// of the step, PDL-launched behind it, reads its output before their PDL wait).
+int launch_slot_map_dev(const int32_t* tok_req, const int32_t* tok_pos, const int32_t* prompt_len,
+                        const int32_t* block_tables, int max_pages, int n_tok_cap, const int32_t* n_tok_dev,
+                        int page_size, int32_t* out, cudaStream_t stream) {
+  if (n_tok_cap == 0) return 0;
+  slot_map_kernel<<<(n_tok_cap + 255) / 256, 256, 0, stream>>>(tok_req, tok_pos, prompt_len, block_tables,
+                                                               max_pages, n_tok_cap, page_size, out, n_tok_dev);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -38,11 +38,6 @@
 
 namespace optimus {
 
-// Arrival counters of tail-merged split groups (one per group of a launch): two pieces
-// add one each, the merging CTA waits for 2 and stores 0, so they are zero between
-// launches (zero-initialised at load).
-__device__ int g_tail_cnt[kMaxTailGroups];
-
 // Set when the fused append clamps a bf16 V value beyond the fp16 range (see K1).
 __device__ int g_v_saturated_k2;
 
@@ -103,7 +98,7 @@ struct UnitInfo {
   uint32_t words[kMaxUnitWords];
   int pages[kMaxUnitPages];
 };
-// epilogue record of item u at [u % kEpiRing]: {head, tok_begin, n_tok, slot, n_tiles, counter + 1}
+// epilogue record of item u at [u % kEpiRing]: {head, tok_begin, n_tok, slot, n_tiles}
 constexpr int kEpiInts = 8;
 
 template <int HD, int KST, int VST>
@@ -119,7 +114,7 @@ struct AttnSmem {
   static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * 2 * kBlockM * 4;
   static constexpr uint32_t OFF_APP = OFF_EPI + kEpiRing * kEpiInts * 4;  // fused-append scratch
   static constexpr uint32_t OFF_BAR = (OFF_APP + (kAppItems * 9 + 1) * 4 + 15) / 16 * 16;
-  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 6 + 2 * kInfo + 3;
+  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 6 + 2 * kInfo + 2;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
@@ -162,8 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* info_empty = info_full + kInfo;
   uint64_t* append_done = info_empty + kInfo;  // fused KV append of this CTA's items landed
   uint64_t* append_issued = append_done + 1;   // ... and its first loads are in flight
-  uint64_t* merge_bar = append_issued + 1;     // tail merge: both partials landed in smem
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_bar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(append_issued + 1);
   UnitInfo* info = reinterpret_cast<UnitInfo*>(smem + L::OFF_INFO);
   float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // epilogue (m, l) exchange
   int* epi = reinterpret_cast<int*>(smem + L::OFF_EPI);
@@ -203,7 +197,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&red_full[i], 256);
       mbar_init(&red_empty[i], 128);
     }
-    mbar_init(merge_bar, 1);
     mbar_init(append_done, 256);
     mbar_init(append_issued, 256);
     mbar_fence_init();
@@ -335,85 +328,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (valid && slot >= 0)
         reinterpret_cast<float2*>(p.ws_ml)[static_cast<int64_t>(slot) * kBlockM + row] = make_float2(mx, l_tot);
-      if (p.n_tail > 0 && slot >= 0 && er[5] > 0) {
-        // a piece of a tail-merged group: publish it (every writer fences, then one
-        // arrival on the group's counter)
-        __threadfence();
-        named_bar_sync(3, 128);
-        if (threadIdx.x == 384) atomicAdd(&g_tail_cnt[er[5] - 1], 1);
-      }
-    }
-    if (p.n_tail > 0) {
-      // Tail merges named for this CTA (planner candidate E: two pieces per group, placed
-      // early on other CTAs; each 32-row slab of a group's output is merged by the CTA
-      // its record names).  The K/V rings are idle now: the slab's rows of both partials
-      // land there by bulk copy, their (m, l) in the reduction scratch; each thread forms
-      // one row's weights, then each warp merges rows (lane = 4 columns) into bf16 rows.
-      static_assert(2 * 32 * HD * 4 <= L::OFF_INFO, "tail merge staging exceeds the rings");
-      const float* so = reinterpret_cast<const float*>(smem);                 // [2][32][HD]
-      const float2* sml = reinterpret_cast<const float2*>(smem + L::OFF_RED);  // [2][32]
-      float2* swt = reinterpret_cast<float2*>(smem + L::OFF_RED + 512);       // [32] weights
-      grid_dep_wait();  // a CTA without items must not see the previous launch's counters
-      int jobs = 0;
-      for (int gi = 0; gi < p.n_tail; ++gi) {
-        const int* gr = p.groups + 8 * gi;
-        const unsigned g6 = static_cast<unsigned>(__ldg(gr + 6));
-        const int n_tok = __ldg(gr + 3);
-        const int rows = min(n_tok * G, kBlockM);
-        const int n_slabs = (rows + 31) / 32;
-        for (int sl = 0; sl < n_slabs; ++sl) {
-          if (((g6 >> (8 * sl)) & 255u) != blockIdx.x + 1) continue;
-          const int head = __ldg(gr + 1), tok_begin = __ldg(gr + 2), slot0 = __ldg(gr + 4);
-          int* cnt = &g_tail_cnt[__ldg(gr + 7) - 1];
-          const int r0 = 32 * sl, nr = min(32, rows - r0);
-          if (threadIdx.x == 384) {
-            long long spins = 0;
-            while (ld_acquire_gpu(cnt) < 2) {  // both pieces published
-              __nanosleep(64);
-              if (++spins > (1LL << 26)) __trap();  // seconds: a lost arrival must not hang the GPU
-            }
-            fence_proxy_async_global();  // the partials (generic stores elsewhere) feed the bulk copies
-            const uint32_t ob = static_cast<uint32_t>(nr) * HD * 4;
-            mbar_arrive_expect_tx(merge_bar, 2 * ob + 2 * 256);
-            for (int s2 = 0; s2 < 2; ++s2) {
-              const int64_t sr = static_cast<int64_t>(slot0 + s2) * kBlockM + r0;
-              bulk_g2s(smem + s2 * (32 * HD * 4), p.ws_o + sr * HD, ob, merge_bar);
-              bulk_g2s(smem + L::OFF_RED + s2 * 256, p.ws_ml + sr * 2, 256, merge_bar);
-            }
-          }
-          mbar_wait(merge_bar, jobs & 1);
-          const int et = threadIdx.x - 384;
-          if (et < nr) {
-            const float2 a = sml[et], b = sml[32 + et];
-            const float mx = fmaxf(a.y > 0.f ? a.x : -INFINITY, b.y > 0.f ? b.x : -INFINITY);
-            const float wa = a.y > 0.f ? exp2f(a.x - mx) : 0.f;
-            const float wb = b.y > 0.f ? exp2f(b.x - mx) : 0.f;
-            const float den = wa * a.y + wb * b.y;
-            const float inv = den > 0.f ? 1.f / den : 0.f;
-            swt[et] = make_float2(wa * inv, wb * inv);
-          }
-          named_bar_sync(3, 128);
-          const int c4 = lane * 4;  // this lane's 4 columns (HD = 64: lanes 0-15)
-#pragma unroll 8
-          for (int i = ew; i < nr; i += 4) {
-            if (c4 < HD) {
-              const float2 w = swt[i];
-              const float4 oa = *reinterpret_cast<const float4*>(so + i * HD + c4);
-              const float4 ob2 = *reinterpret_cast<const float4*>(so + (32 + i) * HD + c4);
-              const int r = r0 + i, t = r / G, g = r - t * G;
-              __nv_bfloat16* dst = p.out + static_cast<int64_t>(tok_begin + t) * p.out_stride_tok +
-                                   static_cast<int64_t>(head * G + g) * HD + c4;
-              *reinterpret_cast<uint2*>(dst) =
-                  make_uint2(pack_bf16x2(w.x * oa.x + w.y * ob2.x, w.x * oa.y + w.y * ob2.y),
-                             pack_bf16x2(w.x * oa.z + w.y * ob2.z, w.x * oa.w + w.y * ob2.w));
-            }
-          }
-          named_bar_sync(3, 128);  // staging reusable
-          // the last slab to finish re-arms the counter for the next launch
-          if (threadIdx.x == 384 && atomicAdd(cnt, 1) == 2 + n_slabs - 1) atomicExch(cnt, 0);
-          ++jobs;
-        }
-      }
     }
   } else if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kCtrlRegs));
@@ -641,7 +555,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int key_begin = __shfl_sync(0xFFFFFFFFu, f[4], k);
           const int key_end = __shfl_sync(0xFFFFFFFFu, f[5], k);
           const int slot = __shfl_sync(0xFFFFFFFFu, f[6], k);
-          const int mrg = __shfl_sync(0xFFFFFFFFu, f[7], k);
           const int prompt = __shfl_sync(0xFFFFFFFFu, prompt_l, k);
           const int vb = __shfl_sync(0xFFFFFFFFu, vb_l, k);
           const int voff = __shfl_sync(0xFFFFFFFFu, voff_l, k);
@@ -658,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane < kEpiInts) {
             const int n_tiles = (key_end - key_begin + kTileN - 1) / kTileN;
             const int v = lane == 0 ? head : lane == 1 ? tok_begin : lane == 2 ? n_tok
-                        : lane == 3 ? slot : lane == 4 ? n_tiles : lane == 5 ? mrg : 0;
+                        : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
             epi[(unit % kEpiRing) * kEpiInts + lane] = v;
           }
           if (lane < 11) {

@@ -14,8 +14,6 @@
 // applies threshold + progress rule per request (one warp per request).
 #include "ptx.cuh"
 
-#include <cstdlib>
-
 namespace optimus {
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -47,11 +45,8 @@ struct VecLoad;
 template <>
 struct VecLoad<__nv_bfloat16> {
   static constexpr int N = 8;  // elements per 16-byte vector
-  __device__ static uint4 raw(const __nv_bfloat16* base, int64_t i) {
-    return __ldg(reinterpret_cast<const uint4*>(base) + i);
-  }
-  __device__ static void load(const __nv_bfloat16* base, int64_t i, float (&v)[8]) { unpack(raw(base, i), v); }
-  __device__ static void unpack(const uint4 u, float (&v)[8]) {
+  __device__ static void load(const __nv_bfloat16* base, int64_t i, float (&v)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(base) + i);
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -64,15 +59,12 @@ struct VecLoad<__nv_bfloat16> {
 template <>
 struct VecLoad<float> {
   static constexpr int N = 4;
-  __device__ static uint4 raw(const float* base, int64_t i) {
-    return __ldg(reinterpret_cast<const uint4*>(base) + i);
-  }
-  __device__ static void load(const float* base, int64_t i, float (&v)[4]) { unpack(raw(base, i), v); }
-  __device__ static void unpack(const uint4 u, float (&v)[4]) {
-    v[0] = __uint_as_float(u.x);
-    v[1] = __uint_as_float(u.y);
-    v[2] = __uint_as_float(u.z);
-    v[3] = __uint_as_float(u.w);
+  __device__ static void load(const float* base, int64_t i, float (&v)[4]) {
+    const float4 u = __ldg(reinterpret_cast<const float4*>(base) + i);
+    v[0] = u.x;
+    v[1] = u.y;
+    v[2] = u.z;
+    v[3] = u.w;
   }
 };
 
@@ -171,8 +163,8 @@ struct FuseArgs {
   int64_t state_stride;
 };
 
-template <typename T, int THREADS, int PIPE>
-__global__ void __launch_bounds__(THREADS, PIPE == 1 ? 4 : PIPE == 2 ? 6 : 7) unmask_partial_kernel(
+template <typename T, int THREADS>
+__global__ void __launch_bounds__(THREADS) unmask_partial_kernel(
     const T* __restrict__ logits, int64_t row_stride, const int32_t* __restrict__ row_src,
     int vocab, int vocab_offset, int n_vsplit, Part* __restrict__ part,
     const int32_t* __restrict__ n_rows_dev, const FuseArgs fuse) {
@@ -192,65 +184,36 @@ __global__ void __launch_bounds__(THREADS, PIPE == 1 ? 4 : PIPE == 2 ? 6 : 7) un
   // Each thread walks its vectors in increasing index order; within the thread the
   // first maximum wins (strict >), so the kept index is the lowest among equals.
   int i = v0 + threadIdx.x;
-  constexpr int U = PIPE == 2 ? 2 : 4;  // vectors per thread per batch
-  // one batch of U vectors (vector index i + u * THREADS): vector max by a 3-input
-  // FMNMX tree; the position of the max is searched only when it beats the running max
-  // (rare after the first vectors)
-  auto batch = [&](const uint4 (&r)[U], int ib) {
+  constexpr int U = 4;
+  for (; i + (U - 1) * THREADS < v1; i += U * THREADS) {
+    float v[U][N];
+#pragma unroll
+    for (int u = 0; u < U; ++u) VecLoad<T>::load(base, i + u * THREADS, v[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      float v[N];
-      VecLoad<T>::unpack(r[u], v);
-      float cm = v[0];
+      // vector max by a 3-input FMNMX tree; the position of the max is searched only
+      // when it beats the running max (rare after the first vectors)
+      float cm = v[u][0];
 #pragma unroll
-      for (int k = 1; k + 1 < N; k += 2) cm = fmax3(cm, v[k], v[k + 1]);
-      if constexpr (N % 2 == 0) cm = fmaxf(cm, v[N - 1]);
+      for (int k = 1; k + 1 < N; k += 2) cm = fmax3(cm, v[u][k], v[u][k + 1]);
+      if constexpr (N % 2 == 0) cm = fmaxf(cm, v[u][N - 1]);
       if (__builtin_expect(cm > m, 0)) {
         int ci = N - 1;
 #pragma unroll
-        for (int k = N - 2; k >= 0; --k) ci = (v[k] == cm) ? k : ci;
+        for (int k = N - 2; k >= 0; --k) ci = (v[u][k] == cm) ? k : ci;
         s = (m == -INFINITY) ? 0.f : s * fast_exp2((m - cm) * kLog2e);
         m = cm;
-        idx = (ib + u * THREADS) * N + ci;
+        idx = (i + u * THREADS) * N + ci;
       }
       const float mb = -m * kLog2e;
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
       for (int k = 0; k + 1 < N; k += 2) {
         float e0, e1;
-        ffma2(e0, e1, v[k], v[k + 1], kLog2e, kLog2e, mb, mb);
+        ffma2(e0, e1, v[u][k], v[u][k + 1], kLog2e, kLog2e, mb, mb);
         fadd2(s0, s1, s0, s1, fast_exp2(e0), fast_exp2(e1));
       }
       s += s0 + s1;
-    }
-  };
-  if constexpr (PIPE > 0) {
-    // software pipelined: the next batch's loads are in flight while this one is reduced
-    if (i + (U - 1) * THREADS < v1) {
-      uint4 cur[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = VecLoad<T>::raw(base, i + u * THREADS);
-      while (true) {
-        const int in = i + U * THREADS;
-        const bool more = in + (U - 1) * THREADS < v1;
-        uint4 nxt[U];
-        if (more) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) nxt[u] = VecLoad<T>::raw(base, in + u * THREADS);
-        }
-        batch(cur, i);
-        i = in;
-        if (!more) break;
-#pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-      }
-    }
-  } else {
-    for (; i + (U - 1) * THREADS < v1; i += U * THREADS) {
-      uint4 r[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = VecLoad<T>::raw(base, i + u * THREADS);
-      batch(r, i);
     }
   }
   for (; i < v1; i += THREADS) {
@@ -319,43 +282,19 @@ __global__ void __launch_bounds__(THREADS, PIPE == 1 ? 4 : PIPE == 2 ? 6 : 7) un
   }
 }
 
-// Phase (a) loop variant (OPTIMUS_K3_PIPE, read per launch so one process can A/B them):
-// 1 = software pipelined, 4 vectors per thread per batch (default); 2 = pipelined, 2
-// vectors; 0 = one batch of 4 loads at a time.
-static int k3_pipe() {
-  const char* e = getenv("OPTIMUS_K3_PIPE");
-  return e ? atoi(e) : 1;
-}
-
 int launch_unmask_partials(const void* logits, int dtype, int64_t row_stride,
                            const int32_t* row_src, int n_rows, int vocab, int vocab_offset,
                            int n_vsplit, float* part, cudaStream_t stream) {
   if (n_rows == 0) return 0;
   dim3 grid(n_rows, n_vsplit);
   if (dtype == 0) {
-    switch (k3_pipe()) {
-      case 0: unmask_partial_kernel<__nv_bfloat16, 256, 0><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset,
-        n_vsplit, reinterpret_cast<Part*>(part), nullptr, FuseArgs{}); break;
-      case 2: unmask_partial_kernel<__nv_bfloat16, 256, 2><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset,
-        n_vsplit, reinterpret_cast<Part*>(part), nullptr, FuseArgs{}); break;
-      default: unmask_partial_kernel<__nv_bfloat16, 256, 1><<<grid, 256, 0, stream>>>(
+    unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset,
         n_vsplit, reinterpret_cast<Part*>(part), nullptr, FuseArgs{});
-    }
   } else {
-    switch (k3_pipe()) {
-      case 0: unmask_partial_kernel<float, 256, 0><<<grid, 256, 0, stream>>>(
-        static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), nullptr, FuseArgs{}); break;
-      case 2: unmask_partial_kernel<float, 256, 2><<<grid, 256, 0, stream>>>(
-        static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), nullptr, FuseArgs{}); break;
-      default: unmask_partial_kernel<float, 256, 1><<<grid, 256, 0, stream>>>(
+    unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
         static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
         reinterpret_cast<Part*>(part), nullptr, FuseArgs{});
-    }
   }
   return static_cast<int>(cudaGetLastError());
 }
@@ -367,29 +306,13 @@ int launch_unmask_partials_dev(const void* logits, int dtype, int64_t row_stride
   if (n_rows_cap == 0) return 0;
   dim3 grid(n_rows_cap, n_vsplit);
   if (dtype == 0) {
-    switch (k3_pipe()) {
-      case 0: unmask_partial_kernel<__nv_bfloat16, 256, 0><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{}); break;
-      case 2: unmask_partial_kernel<__nv_bfloat16, 256, 2><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{}); break;
-      default: unmask_partial_kernel<__nv_bfloat16, 256, 1><<<grid, 256, 0, stream>>>(
+    unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
         reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{});
-    }
   } else {
-    switch (k3_pipe()) {
-      case 0: unmask_partial_kernel<float, 256, 0><<<grid, 256, 0, stream>>>(
-        static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{}); break;
-      case 2: unmask_partial_kernel<float, 256, 2><<<grid, 256, 0, stream>>>(
-        static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{}); break;
-      default: unmask_partial_kernel<float, 256, 1><<<grid, 256, 0, stream>>>(
+    unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
         static_cast<const float*>(logits), row_stride, row_src, vocab, vocab_offset, n_vsplit,
         reinterpret_cast<Part*>(part), n_rows_dev, FuseArgs{});
-    }
   }
   return static_cast<int>(cudaGetLastError());
 }
@@ -407,29 +330,13 @@ int launch_unmask_commit(const void* logits, int dtype, int64_t row_stride, cons
                    state, token_buf, state_stride};
   dim3 grid(n_rows, n_vsplit);
   if (dtype == 0) {
-    switch (k3_pipe()) {
-      case 0: unmask_partial_kernel<__nv_bfloat16, 256, 0><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, 0, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev, f); break;
-      case 2: unmask_partial_kernel<__nv_bfloat16, 256, 2><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, 0, n_vsplit,
-        reinterpret_cast<Part*>(part), n_rows_dev, f); break;
-      default: unmask_partial_kernel<__nv_bfloat16, 256, 1><<<grid, 256, 0, stream>>>(
+    unmask_partial_kernel<__nv_bfloat16, 256><<<grid, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(logits), row_stride, row_src, vocab, 0, n_vsplit,
         reinterpret_cast<Part*>(part), n_rows_dev, f);
-    }
   } else {
-    switch (k3_pipe()) {
-      case 0: unmask_partial_kernel<float, 256, 0><<<grid, 256, 0, stream>>>(
-        static_cast<const float*>(logits), row_stride, row_src, vocab, 0, n_vsplit, reinterpret_cast<Part*>(part),
-        n_rows_dev, f); break;
-      case 2: unmask_partial_kernel<float, 256, 2><<<grid, 256, 0, stream>>>(
-        static_cast<const float*>(logits), row_stride, row_src, vocab, 0, n_vsplit, reinterpret_cast<Part*>(part),
-        n_rows_dev, f); break;
-      default: unmask_partial_kernel<float, 256, 1><<<grid, 256, 0, stream>>>(
+    unmask_partial_kernel<float, 256><<<grid, 256, 0, stream>>>(
         static_cast<const float*>(logits), row_stride, row_src, vocab, 0, n_vsplit, reinterpret_cast<Part*>(part),
         n_rows_dev, f);
-    }
   }
   return static_cast<int>(cudaGetLastError());
 }

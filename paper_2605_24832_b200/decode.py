@@ -146,7 +146,10 @@ class StreamingDecoder:
         # slot map, "fused" = K1 folded into K2 (needs one query tile per request).
         # Interleaved A/B (tools/ab_step.py): fused -0.8% at ShareGPT, +4.6% at 4K;
         # slots = k1 within noise.
-        self.append_mode = os.environ.get("OPTIMUS_APPEND", "k1")
+        # K1 form: "slots" = the step's slot map once, then one round trip per row in every
+        # layer (default: ShareGPT / LLaDA whole step -1.2% against "k1", gpurun r2d7);
+        # "k1" = each layer's K1 derives the slots itself; "fused" = K1 folded into K2
+        self.append_mode = os.environ.get("OPTIMUS_APPEND", "slots")
         self._native = None
 
     # ------------------------------------------------------------------ admission
@@ -296,7 +299,7 @@ class StreamingDecoder:
             dm.vis_base.data_ptr(), dm.vis_off.data_ptr(), dm.vis_words.data_ptr(),
             dm.block_tables.data_ptr(), dm.block_tables.shape[1], plan.work.data_ptr(),
             plan.cta_off.data_ptr(), plan.grid if plan.n_work else 0, plan.groups.data_ptr(),
-            plan.n_groups_arg, cfg.block_size, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+            plan.n_groups, cfg.block_size, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
             cfg.page_size, 1.0 / float(cfg.head_dim) ** 0.5, out_a, out.stride(0),
             self._ws_o.data_ptr() if plan.n_partials else None,
             self._ws_ml.data_ptr() if plan.n_partials else None,

@@ -5,7 +5,9 @@
 
     optimus_device_plan       plan_chunk for every request + the step metadata
     optimus_device_attn_plan  the attention work list (LPT placement, balanced split-KV cuts)
-    L x (optimus_kv_append_dev, optimus_paged_attn, optimus_paged_attn_combine_dev)
+    optimus_slot_mapping_dev  the step's slot map (append mode "slots", the default)
+    L x (optimus_kv_append_slots_dev | optimus_kv_append_dev, optimus_paged_attn,
+         optimus_paged_attn_combine_dev)
     optimus_device_row_src, optimus_unmask_commit (K3 in one launch)
     optimus_device_apply      apply_chunk + advance_blocks
     D2H of the plan arrays and the commit mask into pinned buffers
@@ -108,7 +110,7 @@ class DeviceLoop:
         z = lambda m, dt=torch.int32: torch.zeros(max(m, 1), dtype=dt, device=dev)
         M = dict(cu_seqlens=z(n + 1), tok_req=z(ct), tok_pos=z(ct), prompt_len=z(n), key_end=z(n), vis_base=z(n),
                  vis_off=z(n + 1), vis_words=z(cw), cu_rows=z(n + 1), row_tok=z(cr), row_pos=z(cr), row_req=z(cr),
-                 counts=z(4), row_src=z(cr), commits=z(n))
+                 counts=z(4), row_src=z(cr), commits=z(n), slot_abs=z(2 * ct))
         M["block_tables"] = torch.zeros((n, max_pages), dtype=torch.int32, device=dev)
         G = cfg.num_q_heads // cfg.num_kv_heads
         T = 128 // G
@@ -204,6 +206,14 @@ class DeviceLoop:
         fwd = self.dec.forward
         scale = 1.0 / float(cfg.head_dim) ** 0.5
         v_dtype = ops._v_dtype(self.dec.cache.v)
+        # K1 over the step's slot map (the decoder's append mode "slots", default): the
+        # map once per iteration, then one round trip per row in every layer
+        slots = self.dec.append_mode != "k1"
+        if slots:
+            _lib.check(L.call(
+                "optimus_slot_mapping_dev", p(M["tok_req"]), p(M["tok_pos"]), p(M["prompt_len"]),
+                p(M["block_tables"]), M["block_tables"].shape[1], ct, p(M["counts"]), cfg.page_size,
+                p(M["slot_abs"]), stream), "slot_mapping_dev")
         if self.model:
             fwd.loop_begin(self, M)
         for layer in range(cfg.num_layers):
@@ -216,10 +226,16 @@ class DeviceLoop:
                 buf = fwd.qkv_buf[layer]
                 q, k, v = buf, buf[:, hq], buf[:, hq + hkv]
             kc, vc = self.dec.cache.layer(layer)
-            _lib.check(L.call(
-                "optimus_kv_append_dev", p(k), p(v), k.stride(0), p(M["tok_req"]),
-                p(M["tok_pos"]), p(M["prompt_len"]), p(M["block_tables"]), M["block_tables"].shape[1], ct,
-                p(M["counts"]), hkv, cfg.head_dim, cfg.page_size, p(kc), p(vc), v_dtype, stream), "kv_append_dev")
+            if slots:
+                _lib.check(L.call(
+                    "optimus_kv_append_slots_dev", p(k), p(v), k.stride(0), p(M["slot_abs"]), ct, p(M["counts"]),
+                    hkv, cfg.head_dim, cfg.page_size, p(kc), p(vc), v_dtype, stream), "kv_append_slots_dev")
+            else:
+                _lib.check(L.call(
+                    "optimus_kv_append_dev", p(k), p(v), k.stride(0), p(M["tok_req"]),
+                    p(M["tok_pos"]), p(M["prompt_len"]), p(M["block_tables"]), M["block_tables"].shape[1], ct,
+                    p(M["counts"]), hkv, cfg.head_dim, cfg.page_size, p(kc), p(vc), v_dtype, stream),
+                    "kv_append_dev")
             _lib.check(L.call(
                 "optimus_paged_attn", p(q), q.stride(0), q.shape[0], p(kc), p(vc), kc.shape[0],
                 p(M["tok_pos"]), p(M["prompt_len"]), p(M["vis_base"]), p(M["vis_off"]), p(M["vis_words"]),

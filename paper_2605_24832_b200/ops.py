@@ -134,12 +134,6 @@ class AttnPlan:
     cta_off_host: np.ndarray
     groups_host: np.ndarray
     single_tile: bool = False  # every (request, KV head) is one query tile: K1 may fold into K2
-    tail_merge: bool = False   # split groups merged inside K2 (planner candidate E), no combine launch
-
-    @property
-    def n_groups_arg(self) -> int:
-        """The group count as the K2 entry points take it: negative for a tail-merged plan."""
-        return -self.n_groups if self.tail_merge else self.n_groups
 
 
 def single_query_tile(cu_seqlens_q: np.ndarray, num_q_heads: int, num_kv_heads: int) -> bool:
@@ -198,7 +192,7 @@ def plan_attention(
         dev_off = torch.from_numpy(cta_off).to(device)
         dev_groups = torch.from_numpy(groups).to(device)
     return AttnPlan(grid, n, ng.value, npart.value, dev_work, dev_off, dev_groups, work, cta_off, groups,
-                    single_query_tile(cu, num_q_heads, num_kv_heads), bool(len(groups) and (groups[:, 6] > 0).all()))
+                    single_query_tile(cu, num_q_heads, num_kv_heads))
 
 
 # --------------------------------------------------------------------------- K2
@@ -249,7 +243,7 @@ def paged_attention(
         _ptr(q_pos), _ptr(prompt_len), _ptr(vis_base), _ptr(vis_off), _ptr(vis_words),
         _ptr(block_tables), block_tables.shape[1],
         _ptr(plan.work), _ptr(plan.cta_off), plan.grid if plan.n_work else 0,
-        _ptr(plan.groups), plan.n_groups_arg,
+        _ptr(plan.groups), plan.n_groups,
         block_size, hq, hkv, d, page, scale,
         _ptr(out), out.stride(0),
         _ptr(ws_o) if plan.n_partials else None, _ptr(ws_ml) if plan.n_partials else None,
@@ -321,7 +315,7 @@ def paged_attention_append(
         _ptr(q_pos), _ptr(prompt_len), _ptr(vis_base), _ptr(vis_off), _ptr(vis_words),
         _ptr(block_tables), block_tables.shape[1],
         _ptr(plan.work), _ptr(plan.cta_off), plan.grid if plan.n_work else 0,
-        _ptr(plan.groups), plan.n_groups_arg,
+        _ptr(plan.groups), plan.n_groups,
         block_size, hq, hkv, d, page, scale,
         _ptr(out), out.stride(0),
         _ptr(ws_o) if plan.n_partials else None, _ptr(ws_ml) if plan.n_partials else None,

@@ -272,6 +272,7 @@ def test_graph_captured_host_step_matches_eager(monkeypatch):
     batch, chunk = 12, 16
     reqs_e, dec_e = _setup(8, batch, chunk)
     reqs_g, dec_g = _setup(8, batch, chunk)
+    dec_g.append_mode = "k1"  # the graph-captured host step runs the k1 form of K1
     steps = 0
     while not all(r.finished for r in reqs_e):
         ae = [r for r in reqs_e if not r.finished]

@@ -60,7 +60,7 @@ def _run_append(s):
     return kc, vc, slots
 
 
-@pytest.mark.parametrize("slot_map", [False, True])
+@pytest.mark.parametrize("slot_map", [False, True, "dev"])
 @pytest.mark.parametrize("v_dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("page,d,hkv", [(16, 128, 8), (64, 128, 2), (16, 64, 4), (32, 64, 2)])
 def test_kv_append_bit_exact(page, d, hkv, v_dtype, slot_map):
@@ -69,7 +69,35 @@ def test_kv_append_bit_exact(page, d, hkv, v_dtype, slot_map):
     s["v_new"][0, 0, :4] = torch.tensor([1e6, -1e6, 70000.0, 3.0e-8], dtype=torch.bfloat16)
     m = s["meta"]
     ref_slots = on.slot_mapping(m.tok_req, m.tok_pos, m.prompt_len, m.block_tables, page)
-    if slot_map:
+    if slot_map == "dev":
+        # the DeviceLoop's form: token count in device memory, grids sized for a larger
+        # capacity (optimus_slot_mapping_dev + optimus_kv_append_slots_dev)
+        from paper_2605_24832_b200 import _lib
+        dev = torch.device("cuda")
+        dm = s["dm"]
+        cap = m.n_tok + 37
+        cnt = torch.tensor([m.n_tok], dtype=torch.int32, device=dev)
+        tok_req = torch.zeros(cap, dtype=torch.int32, device=dev)
+        tok_pos = torch.zeros(cap, dtype=torch.int32, device=dev)
+        tok_req[: m.n_tok] = dm.tok_req[: m.n_tok]
+        tok_pos[: m.n_tok] = dm.tok_pos[: m.n_tok]
+        sa = torch.full((cap, 2), -7, dtype=torch.int32, device=dev)
+        kc, vc = s["k_cache"].to(dev), s["v_cache"].to(dev)
+        kn = torch.zeros((cap,) + tuple(s["k_new"].shape[1:]), dtype=s["k_new"].dtype, device=dev)
+        vn = torch.zeros_like(kn)
+        kn[: m.n_tok] = s["k_new"].to(dev)[: m.n_tok]
+        vn[: m.n_tok] = s["v_new"].to(dev)[: m.n_tok]
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.check(_lib.call("optimus_slot_mapping_dev", tok_req.data_ptr(), tok_pos.data_ptr(),
+                             dm.prompt_len.data_ptr(), dm.block_tables.data_ptr(), dm.block_tables.shape[1], cap,
+                             cnt.data_ptr(), page, sa.data_ptr(), st), "slot_mapping_dev")
+        _lib.check(_lib.call("optimus_kv_append_slots_dev", kn.data_ptr(), vn.data_ptr(), kn.stride(0),
+                             sa.data_ptr(), cap, cnt.data_ptr(), hkv, d, page, kc.data_ptr(), vc.data_ptr(),
+                             ops._v_dtype(vc), st), "kv_append_slots_dev")
+        torch.cuda.synchronize()
+        assert (sa[m.n_tok:] == -7).all()  # nothing past the device count
+        slots = sa[:, 1].long()
+    elif slot_map:
         # K1 over the step's slot map (optimus_slot_mapping + optimus_kv_append_slots)
         dev = torch.device("cuda")
         dm = s["dm"]

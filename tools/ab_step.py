@@ -33,21 +33,12 @@ fwd = SyntheticForward(cfg, a.batch * a.chunk, a.batch, device=dev)
 dec = StreamingDecoder(cfg, fwd, device=dev)
 for l in range(cfg.num_layers):
     dec.cache.k[l].normal_(); dec.cache.v[l].normal_()
+dm = dec.prepare(reqs, plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule))
 graphs = {}
-dms = []
 import os
 for mode in a.modes.split(","):
-    # "k1@43": append mode k1 with OPTIMUS_K2_RINGS=43 (K2 variant chosen at capture);
-    # "k1#notail": the step planned with OPTIMUS_PLAN_NOTAIL=1 (no tail-merged split-KV)
-    mode_, _, pl = mode.partition("#")
-    am, _, rings = mode_.partition("@")
-    if pl == "notail":
-        os.environ["OPTIMUS_PLAN_NOTAIL"] = "1"
-    else:
-        os.environ.pop("OPTIMUS_PLAN_NOTAIL", None)
-    dm = dec.prepare(reqs, plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule))
-    dms.append(dm)  # the graph reads its buffers
-    print(f"{mode}: split groups {dm.attn_plan.n_groups} tail_merge {dm.attn_plan.tail_merge}", flush=True)
+    # "k1@43": append mode k1 with OPTIMUS_K2_RINGS=43 (K2 variant chosen at capture)
+    am, _, rings = mode.partition("@")
     if rings:
         os.environ["OPTIMUS_K2_RINGS"] = rings
     else:

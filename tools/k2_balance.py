@@ -69,10 +69,3 @@ fit = np.linalg.lstsq(np.stack([np.ones_like(e), tiles, items], 1), e, rcond=Non
 print(f"end ~ {fit[0]:.2f} + {fit[1]:.3f}/tile + {fit[2]:.3f}/item us")
 order = np.argsort(-e)[:8]
 print("latest CTAs (end us, tiles, items):", [(round(float(e[c]), 2), int(tiles[c]), int(items[c])) for c in order])
-if plan.tail_merge:
-    mc = plan.groups_host[:, 6] - 1
-    print("tail merges: merging CTAs (end us, tiles, items):",
-          [(int(c), round(float(e[c]), 2), int(tiles[c]), int(items[c])) for c in mc])
-    for gi, g in enumerate(plan.groups_host):
-        pcs = [c for c in range(plan.grid) for w in work[off[c]: off[c + 1]] if w[7] == gi + 1]
-        print(f"  group {gi}: pieces on CTAs {pcs} (ends {[round(float(e[c]), 2) for c in pcs]}), merged by {int(mc[gi])}")

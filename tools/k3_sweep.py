@@ -26,7 +26,6 @@ ap.add_argument("--step", type=int, default=50)
 ap.add_argument("--reqs", type=int, default=64)
 ap.add_argument("--out", default="")
 ap.add_argument("--splits", default="", help="comma list: time these vocab split counts too (default: the chooser's)")
-ap.add_argument("--pipes", default="", help="comma list of OPTIMUS_K3_PIPE loop variants to A/B (default: the library's)")
 ap.add_argument("--lib", default="", help="time another build of the C-ABI library (tools/build_variant.py)")
 a = ap.parse_args()
 if a.lib:
@@ -38,14 +37,8 @@ REPS = 8
 hbm, _ = bench.peaks()
 V = a.vocab
 x = torch.randn((a.hi, V), device=dev).to(torch.bfloat16)
-import os
 points = []
-pipes = [p for p in a.pipes.split(",") if p] or [None]
-for rows, pipe in [(r, p) for r in range(a.lo, a.hi + 1, a.step) for p in pipes]:
-    if pipe is None:
-        os.environ.pop("OPTIMUS_K3_PIPE", None)
-    else:
-        os.environ["OPTIMUS_K3_PIPE"] = pipe
+for rows in range(a.lo, a.hi + 1, a.step):
     cu = torch.linspace(0, rows, a.reqs + 1, device=dev).round().to(torch.int32)
     chosen = ops.unmask_splits(rows, V)
     cands = sorted({chosen, *[int(v) for v in a.splits.split(",") if v]})
@@ -63,7 +56,7 @@ for rows, pipe in [(r, p) for r in range(a.lo, a.hi + 1, a.step) for p in pipes]
                     ops.unmask_finalize(ops.unmask_partials(x[:rows], None, rows, ns, part=part), 1, rows, ns, cu,
                                         0.9)
         torch.cuda.synchronize()
-        points.append([(rows, ns, pipe), ns == chosen, g, part, cu])  # the graph reads these buffers: keep them alive
+        points.append([(rows, ns), ns == chosen, g, part, cu])  # the graph reads these buffers: keep them alive
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 times = {p[0]: [] for p in points}
 for _ in range(12):
@@ -74,13 +67,13 @@ for _ in range(12):
         torch.cuda.synchronize()
         times[key].append(e0.elapsed_time(e1) * 1e3 / REPS)
 out = []
-for (rows, ns, pipe), chosen, *_ in points:
-    us = float(np.median(times[(rows, ns, pipe)][2:]))
+for (rows, ns), chosen, *_ in points:
+    us = float(np.median(times[(rows, ns)][2:]))
     byts = rows * V * 2 + 9 * rows
     gbs = byts / (us * 1e-6) / 1e9
-    out.append({"rows": rows, "n_vsplit": ns, "pipe": pipe, "chosen": chosen, "us": round(us, 2), "gbs": round(gbs, 1),
+    out.append({"rows": rows, "n_vsplit": ns, "chosen": chosen, "us": round(us, 2), "gbs": round(gbs, 1),
                 "frac": round(gbs / hbm, 4)})
-    print(f"rows {rows:5d} pipe {pipe} splits {ns:3d}{'*' if chosen else ' '} {us:7.1f} us  {gbs:7.0f} GB/s  {gbs / hbm:.3f}")
+    print(f"rows {rows:5d} splits {ns:3d}{'*' if chosen else ' '} {us:7.1f} us  {gbs:7.0f} GB/s  {gbs / hbm:.3f}")
 fr = [o["frac"] for o in out if o["chosen"]]
 summary = {"vocab": V, "peak_gbs": hbm, "reps_per_graph": REPS, "min_frac": min(fr), "median_frac": float(np.median(fr)),
            "points": out}
