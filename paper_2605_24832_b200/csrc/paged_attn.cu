@@ -114,7 +114,7 @@ struct AttnSmem {
   static constexpr uint32_t OFF_EPI = OFF_RED + 2 * 2 * 2 * kBlockM * 4;
   static constexpr uint32_t OFF_APP = OFF_EPI + kEpiRing * kEpiInts * 4;  // fused-append scratch
   static constexpr uint32_t OFF_BAR = (OFF_APP + (kAppItems * 9 + 1) * 4 + 15) / 16 * 16;
-  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 6 + 2 * kInfo + 2;
+  static constexpr int NUM_BARS = 2 * KST + 2 * VST + 2 + 3 * kSBuf + 6 + 3 * kInfo + 2;
   static constexpr uint32_t BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t ALLOC = BYTES + 1024;  // slack for 1024-byte alignment
   static_assert(ALLOC <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100");
@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* red_empty = red_full + 2; // [item & 1]: the epilogue warpgroup has read them
   uint64_t* info_full = red_empty + 2;
   uint64_t* info_empty = info_full + kInfo;
-  uint64_t* append_done = info_empty + kInfo;  // fused KV append of this CTA's items landed
+  uint64_t* pg_full = info_empty + kInfo;      // [kInfo]: the record's key range, page ids, query positions
+  uint64_t* append_done = pg_full + kInfo;     // fused KV append of this CTA's items landed
   uint64_t* append_issued = append_done + 1;   // ... and its first loads are in flight
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(append_issued + 1);
   UnitInfo* info = reinterpret_cast<UnitInfo*>(smem + L::OFF_INFO);
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(q_empty, 1);
     for (int i = 0; i < kInfo; ++i) {
       mbar_init(&info_full[i], 33);  // 32 cp.async arrivals + lane 0's store arrival
+      mbar_init(&pg_full[i], 33);    // the same, for the part the TMA producers need
       mbar_init(&info_empty[i], 256 + 2);  // softmax threads + K and V producers
     }
     for (int i = 0; i < kSBuf; ++i) {
@@ -359,7 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int w = w_begin; w < w_end; ++w, ++unit) {
         const int ib = unit % kInfo;
-        mbar_wait(&info_full[ib], (unit / kInfo) & 1);
+        // the key range and page ids land one round trip before the visibility words
+        // (which need the request's scalars): the first loads of a launch go out on them
+        mbar_wait(need_append ? &info_full[ib] : &pg_full[ib], (unit / kInfo) & 1);
         // Q/K/V are written by the preceding kernels (QKV producer, K1 append):
         // everything above overlapped their tail under PDL; the loads may not.
         if (unit == 0) grid_dep_wait();
@@ -555,9 +559,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int key_begin = __shfl_sync(0xFFFFFFFFu, f[4], k);
           const int key_end = __shfl_sync(0xFFFFFFFFu, f[5], k);
           const int slot = __shfl_sync(0xFFFFFFFFu, f[6], k);
-          const int prompt = __shfl_sync(0xFFFFFFFFu, prompt_l, k);
-          const int vb = __shfl_sync(0xFFFFFFFFu, vb_l, k);
-          const int voff = __shfl_sync(0xFFFFFFFFu, voff_l, k);
           mbar_wait(&info_empty[ib], ((unit / kInfo) & 1) ^ 1);
           UnitInfo& u = info[ib];
           const int pg0 = key_begin >> p.page_shift;
@@ -565,6 +566,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int32_t* bt = p.block_tables + static_cast<int64_t>(req) * p.max_pages + pg0;
           for (int i = lane; i < npg; i += 32) cp_async_4(&u.pages[i], bt + i);
           for (int i = lane; i < n_tok; i += 32) cp_async_4(&u.qpos[i], p.q_pos + tok_begin + i);
+          cp_async_arrive_noinc(&pg_full[ib]);
+          if (lane < 7) {
+            const int v = lane == 0 ? req : lane == 1 ? head : lane == 2 ? tok_begin : lane == 3 ? n_tok
+                        : lane == 4 ? key_begin : lane == 5 ? key_end : slot;
+            (&u.req)[lane] = v;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pg_full[ib]);
+          // the request's scalars (loaded for the batch, in flight beside the copies above)
+          const int prompt = __shfl_sync(0xFFFFFFFFu, prompt_l, k);
+          const int vb = __shfl_sync(0xFFFFFFFFu, vb_l, k);
+          const int voff = __shfl_sync(0xFFFFFFFFu, voff_l, k);
           const int nw = key_end > vb ? (key_end - vb + 31) / 32 : 0;
           if (nw <= kMaxUnitWords && lane < nw) cp_async_4(&u.words[lane], p.vis_words + voff + lane);
           cp_async_arrive_noinc(&info_full[ib]);
@@ -574,10 +587,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         : lane == 3 ? slot : lane == 4 ? n_tiles : 0;
             epi[(unit % kEpiRing) * kEpiInts + lane] = v;
           }
-          if (lane < 11) {
-            const int v = lane == 0 ? req : lane == 1 ? head : lane == 2 ? tok_begin : lane == 3 ? n_tok
-                        : lane == 4 ? key_begin : lane == 5 ? key_end : lane == 6 ? slot : lane == 7 ? vb
-                        : lane == 8 ? nw : lane == 9 ? voff : prompt;
+          if (lane >= 7 && lane < 11) {
+            const int v = lane == 7 ? vb : lane == 8 ? nw : lane == 9 ? voff : prompt;
             (&u.req)[lane] = v;
           }
           __syncwarp();
