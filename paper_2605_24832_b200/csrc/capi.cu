@@ -901,11 +901,14 @@ int optimus_attn_layers(int n_layers, const void* const* q, const void* const* k
 int optimus_unmask_splits(int n_rows, int vocab) {
   if (n_rows <= 0 || vocab <= 0) return 1;
   // Measured table (tools/k3_sweep.py --splits, profiles/r2h_k3_splits*.txt: fused K3 on
-  // B200 over 32..2,100 rows x 151,936 bf16, every split count timed in one process).
-  // Rows are scaled to that vocabulary so the table is in CTA bytes.  Few large CTAs win
-  // once the grid fills the machine; small batches need slices to reach every SM.
+  // B200 over 32..2,100 rows x 151,936 bf16, every split count timed in one process; the
+  // 2-split band re-measured up to 1,550 rows, profiles/r2d2_k3_splits_pipes.txt, "pipe 0":
+  // 1,300 / 1,400 / 1,500 rows 72.7 / 76.0 / 82.0 us with 2 splits against 77.3 / 79.7 /
+  // 83.3 with 1).  Rows are scaled to that vocabulary so the table is in CTA bytes.  Few
+  // large CTAs win once the grid fills the machine; small batches need slices to reach
+  // every SM.
   const double eq = static_cast<double>(n_rows) * vocab / 151936.0;
-  int s = eq < 64 ? 8 : eq < 256 ? 4 : eq < 400 ? 2 : eq < 650 ? 3 : eq < 1250 ? 2 : 1;
+  int s = eq < 64 ? 8 : eq < 256 ? 4 : eq < 400 ? 2 : eq < 650 ? 3 : eq < 1550 ? 2 : 1;
   s = std::min(s, std::max(1, vocab / 8192));
   return s;
 }
