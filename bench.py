@@ -521,10 +521,15 @@ def kernel_times(W, dm, dev, use_graph=True):
     plan = dm.__dict__["attn_plan"]
     out = dec._workspaces(plan, m.n_tok)
 
+    # K1 in the form the step runs: over the step's slot map (computed once per step,
+    # outside this per-layer timing) when the decoder's append mode is "slots"
+    sa = (ops.slot_mapping(dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, cfg.page_size, n_tok=m.n_tok)
+          if dec.append_mode != "k1" and m.n_tok else None)
+
     def k1(l):
         q, k, v = fwd.qkv(l, dm)
         kc, vc = dec.cache.layer(l)
-        ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc)
+        ops.kv_append(k, v, dm.tok_req, dm.tok_pos, dm.prompt_len, dm.block_tables, kc, vc, slot_abs=sa)
 
     def k2(l):
         q, k, v = fwd.qkv(l, dm)
@@ -796,6 +801,7 @@ def main():
     clocks = sampler.stop()
 
     k1_us, k2_us, k3_us = kernel_times(W, dm, dev, use_graph=world == 1 or backend == "nccl")
+    k1_form = dec.append_mode
     parity = parity_check(W, dm, res) if world == 1 and not args.no_parity else None
 
     # ---- end to end through the public per-step call (closed loop, live state)
@@ -856,7 +862,7 @@ def main():
                      "frac": achieved / hbm, "traffic": traffic, "kernel": "paged_attn_kernel (K2)",
                      "peak_kind": peak_kind, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": k2b, "launch_us": k2_us},
-        "kernels_us": {"k1_kv_append": k1_us, "k2_paged_attn": k2_us, "k3_unmask": k3_us,
+        "kernels_us": {"k1_form": k1_form, "k1_kv_append": k1_us, "k2_paged_attn": k2_us, "k3_unmask": k3_us,
                        "k2_share_of_step": k2_us * L / (ms * 1e3),
                        "k1_gbs": k1b / (k1_us * 1e-6) / 1e9, "k3_gbs": k3b / (k3_us * 1e-6) / 1e9,
                        "k2_tflops": flops / (k2_us * 1e-6) / 1e12},

@@ -35,15 +35,26 @@ for l in range(cfg.num_layers):
     dec.cache.k[l].normal_(); dec.cache.v[l].normal_()
 dm = dec.prepare(reqs, plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule))
 graphs = {}
+dms = []
 import os
 for mode in a.modes.split(","):
-    # "k1@43": append mode k1 with OPTIMUS_K2_RINGS=43 (K2 variant chosen at capture)
-    am, _, rings = mode.partition("@")
+    # "k1@43": append mode k1 with OPTIMUS_K2_RINGS=43 (K2 variant chosen at capture);
+    # "slots:OPTIMUS_PLAN_KITEM=2.0": any environment knob, set while this mode is planned
+    # and captured
+    mode_, _, kv = mode.partition(":")
+    for k in [k for k in os.environ if k.startswith("OPTIMUS_PLAN_")]:
+        os.environ.pop(k)
+    if kv:
+        k, _, v = kv.partition("=")
+        os.environ[k] = v
+    am, _, rings = mode_.partition("@")
     if rings:
         os.environ["OPTIMUS_K2_RINGS"] = rings
     else:
         os.environ.pop("OPTIMUS_K2_RINGS", None)
     dec.append_mode = am
+    dm = dec.prepare(reqs, plan_batch(reqs, a.chunk, cfg.block_size, cfg.window_rule))
+    dms.append(dm)  # the graph reads its buffers
     s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
