@@ -1,6 +1,6 @@
 import sys, cProfile, pstats, time
 sys.path.insert(0, '.')
-sys.argv = ['bench.py', '--no-cpu-baseline', '--no-target', '--steps', '5', '--warmup', '3', '--e2e-steps', '200']
+sys.argv = ['bench.py', '--no-cpu-baseline', '--quick', '--no-parity', '--steps', '5', '--warmup', '3', '--e2e-steps', '200']
 import bench
 import paper_2605_24832_b200.native_step as ns
 pr = cProfile.Profile()
